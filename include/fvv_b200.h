@@ -1,0 +1,197 @@
+/*
+ * fvv_b200.h — C ABI of the B200-native edge-server view-synthesis library
+ * (libfvvb200.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference's synthesis path. The
+ * reference (/root/reference/pkg/src/fvv) is pure Python/numpy and has no
+ * FFI of its own; each entry point below replaces one reference function and
+ * is bound from Python with ctypes (paper_2007_00558_b200/_native.py). The
+ * reference function each one replaces is cited next to it.
+ *
+ * Conventions
+ *  - Image buffers are caller-owned DEVICE pointers, tightly packed, row-major
+ *    (pitch = width elements; RGB pitch = 3*width bytes).
+ *  - Every call is asynchronous on the context's stream (fvv_ctx_set_stream);
+ *    fvv_sync() waits for it.
+ *  - Status codes: FVV_OK, FVV_EINVAL (-> Python ValueError, mirroring the
+ *    reference's ValueError cases), FVV_ECUDA (-> RuntimeError). The message
+ *    is available from fvv_last_error(ctx). The library never aborts.
+ *  - Contexts are independent; a context is not thread-safe, distinct
+ *    contexts may be used from distinct threads.
+ */
+#ifndef FVV_B200_H
+#define FVV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVV_OK 0
+#define FVV_EINVAL 1
+#define FVV_ECUDA 2
+
+#define FVV_VALID 0      /* core.Validity, core.py:28-33 */
+#define FVV_INVALID 1
+#define FVV_BACKGROUND 2
+
+#define FVV_MAX_REFS 16  /* transport.CameraSetCommand bitmask, transport.py:241-263 */
+#define FVV_MAX_SLOTS 64
+
+typedef struct fvv_ctx fvv_ctx;
+
+/* core.CameraCalibration (core.py:36-86): intrinsics + world->camera pose. */
+typedef struct fvv_camera {
+    int32_t id, width, height, reserved;
+    double fx, fy, cx, cy;
+    double R[9]; /* row-major world->camera rotation (core.py:62) */
+    double C[3]; /* camera centre in world metres (core.py:63) */
+} fvv_camera;
+
+/* synthesis.SynthesisConfig (synthesis.py:36-49). reference_count is a
+ * host-side selection parameter and is not needed by the kernels. */
+typedef struct fvv_synth_cfg {
+    int32_t splat_radius;      /* synthesis.py:39, 0..3 */
+    int32_t crack_fill_window; /* synthesis.py:40, 1..5 */
+    double mixing_epsilon;     /* synthesis.py:41 */
+    double depth_band_rel;     /* synthesis.py:42 */
+    uint8_t hole_color[3];     /* synthesis.py:43 */
+    uint8_t angular_weight;    /* extension (not in reference); must be 0 */
+    uint8_t inpaint;           /* extension (not in reference); must be 0 */
+    uint8_t reserved[3];
+} fvv_synth_cfg;
+
+/* synthesis.CameraStreamInputs (synthesis.py:321-328), device pointers. */
+typedef struct fvv_ref_frame {
+    fvv_camera cam;
+    const uint8_t *rgb;           /* H*W*3 live colour */
+    const float *live_depth;      /* H*W metres; FG Valid, BG Background, holes Invalid */
+    const uint8_t *live_validity; /* H*W Validity codes */
+    const float *bg_depth;        /* H*W static background model */
+    const uint8_t *bg_validity;   /* H*W */
+    double weight;                /* 1/(camera_distance + eps) (synthesis.py:249,257);
+                                     <= 0 -> computed on device */
+} fvv_ref_frame;
+
+/* Optional intermediate rasters (synthesis.DebugBundle, synthesis.py:365-397)
+ * plus the winner-index/stage maps the reference never materialises.
+ * Contribution k in [0, 2*n_refs): FG contributions in reference order, then
+ * BG contributions. Any pointer may be NULL. */
+typedef struct fvv_debug {
+    double *contrib_color;   /* [2R][H][W][3] */
+    double *contrib_depth;   /* [2R][H][W] (0 where not valid) */
+    uint8_t *contrib_valid;  /* [2R][H][W] */
+    int32_t *contrib_winner; /* [2R][H][W] source pixel index, -1 none/crack-filled */
+    uint8_t *contrib_stage;  /* [2R][H][W] 0 none, 1 centre, 2 splat, 3 crack median */
+    double *merged_color;    /* [2][H][W][3] FG then BG (synthesis.MergedLayer) */
+    double *merged_depth;    /* [2][H][W] */
+    uint8_t *merged_valid;   /* [2][H][W] */
+} fvv_debug;
+
+/* ---- context ------------------------------------------------------------ */
+int fvv_ctx_create(int32_t device, fvv_ctx **out);
+int fvv_ctx_destroy(fvv_ctx *ctx);
+int fvv_ctx_set_stream(fvv_ctx *ctx, void *cuda_stream); /* NULL = legacy default */
+int fvv_sync(fvv_ctx *ctx);
+const char *fvv_last_error(const fvv_ctx *ctx);
+const char *fvv_version(void);
+int64_t fvv_launch_count(const fvv_ctx *ctx); /* kernels launched by this context */
+
+/* Per-kernel device timing: when enabled, every launch is bracketed by CUDA
+ * events on the context's stream (the stream the kernel runs on).
+ * kernel ids: 0 preprocess (K0+K1+ingest), 1 forward warp (K2),
+ * 2 resolve (K3), 3 canvas fill, 4 other. fvv_profile_read synchronises. */
+#define FVV_K_PREPROCESS 0
+#define FVV_K_FORWARD_WARP 1
+#define FVV_K_RESOLVE 2
+#define FVV_K_FILL 3
+#define FVV_K_OTHER 4
+int fvv_profile_enable(fvv_ctx *ctx, int32_t enable); /* also resets */
+int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches);
+
+/* ---- K0: depth decode ----------------------------------------------------- */
+/* core.depth_from_millimeters (core.py:260-269): f32 = (f32)mm / 1000.0f,
+ * Valid & mm==0 -> Invalid, non-Valid depth = 0. validity_in may be NULL
+ * (= all Valid). */
+int fvv_decode_mm(fvv_ctx *ctx, const uint16_t *mm, const uint8_t *validity_in,
+                  int32_t width, int32_t height, float *depth_out, uint8_t *validity_out);
+
+/* depthcodec.unpack_yuv420 (depthcodec.py:213-222) + dequantize12
+ * (depthcodec.py:113-138). y: H*W, u/v: (H/2)*(W/2). codes_out may be NULL. */
+int fvv_decode_yuv420_12(fvv_ctx *ctx, const uint8_t *y, const uint8_t *u, const uint8_t *v,
+                         int32_t width, int32_t height, double z_near, double z_far,
+                         float *depth_out, uint8_t *validity_out, uint16_t *codes_out);
+
+/* depthcodec.dequantize12 (depthcodec.py:113-138) from 12-bit codes. */
+int fvv_dequantize12(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t height,
+                     double z_near, double z_far, float *depth_out, uint8_t *validity_out);
+
+/* ---- K1: joint-bilateral hole closing -------------------------------------- */
+/* depthproc.bilateral_close_holes (depthproc.py:171-224). n_holes_dev (device
+ * int32, may be NULL) receives the number of Invalid input pixels, so the
+ * host can mirror the reference's "same object when nothing to fill". */
+int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                              const uint8_t *rgb, int32_t width, int32_t height,
+                              int32_t radius, double sigma_spatial, double sigma_range,
+                              int32_t min_valid_neighbors, float *depth_out,
+                              uint8_t *validity_out, int32_t *n_holes_dev);
+
+/* ---- K2+K3: one synthesized view (synthesis.synthesize_view, synthesis.py:331-362) */
+int fvv_synthesize_view(fvv_ctx *ctx, const fvv_camera *virt, const fvv_ref_frame *refs,
+                        int32_t n_refs, const fvv_synth_cfg *cfg, uint8_t *rgb_out,
+                        uint8_t *provenance_out, const fvv_debug *dbg);
+
+/* synthesis.warp_layer (synthesis.py:162-258): one contribution. color_valid
+ * may be NULL (= depth validity == Valid). Outputs may be NULL except valid. */
+int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst,
+                   const uint8_t *rgb, const float *depth, const uint8_t *validity,
+                   const uint8_t *color_valid, int32_t layer_fg, const fvv_synth_cfg *cfg,
+                   double *color_out, double *depth_out, uint8_t *valid_out,
+                   int32_t *winner_out, uint8_t *stage_out);
+
+/* synthesis.mix_layer (synthesis.py:261-292) over n host arrays of device
+ * pointers (colour H*W*3 f64, depth H*W f64, valid H*W u8). */
+int fvv_mix_layer(fvv_ctx *ctx, int32_t n, const double *const *colors,
+                  const double *const *depths, const uint8_t *const *valids,
+                  const double *weights, int32_t width, int32_t height,
+                  double depth_band_rel, double *color_out, double *depth_out,
+                  uint8_t *valid_out);
+
+/* synthesis.composite (synthesis.py:295-318). provenance_out may be NULL. */
+int fvv_composite(fvv_ctx *ctx, const double *fg_color, const uint8_t *fg_valid,
+                  const double *bg_color, const uint8_t *bg_valid, int32_t width,
+                  int32_t height, const uint8_t hole_color[3], uint8_t *rgb_out,
+                  uint8_t *provenance_out);
+
+/* ---- session path: resident camera slots, batched views ---------------------
+ * The edge server keeps a slot per rig camera: its calibration, its static
+ * BG model (uploaded once, pipeline.py:445) and its latest live frame. */
+int fvv_slot_set_camera(fvv_ctx *ctx, int32_t slot, const fvv_camera *cam);
+int fvv_slot_set_bg(fvv_ctx *ctx, int32_t slot, const float *bg_depth,
+                    const uint8_t *bg_validity);
+/* Live frame from f32 depth + validity (MvdFrame / DepthFrame); hole_closing
+ * runs K1 with the reference defaults first (pipeline.py:518-519). */
+int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float *depth,
+                    const uint8_t *validity, int32_t hole_closing);
+/* Live frame from the 16-bit mm raster: fused K0 decode + K1 hole fill
+ * (pipeline.py:518-519) + ingest. hole_closing=0 skips K1. depth_out /
+ * validity_out (may be NULL) receive the preprocessed DepthFrame. */
+int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint16_t *mm,
+                       const uint8_t *validity, int32_t hole_closing, float *depth_out,
+                       uint8_t *validity_out);
+/* Live frame from the 12-bit YUV420 depth raster (pipeline.py:469-472). */
+int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
+                        const uint8_t *u, const uint8_t *v, double z_near, double z_far,
+                        int32_t hole_closing, float *depth_out, uint8_t *validity_out);
+/* n_views views; view i blends slots ref_slots[i*n_refs .. +n_refs) in that
+ * order with weights[i*n_refs ..] (NULL or <= 0 -> computed on device).
+ * rgb_out: n_views*H*W*3; provenance_out: n_views*H*W or NULL. */
+int fvv_render_views(fvv_ctx *ctx, const fvv_camera *virts, int32_t n_views,
+                     const int32_t *ref_slots, const double *weights, int32_t n_refs,
+                     const fvv_synth_cfg *cfg, uint8_t *rgb_out, uint8_t *provenance_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVV_B200_H */

@@ -1,0 +1,210 @@
+"""ctypes binding of ``libfvvb200.so`` (the C ABI in ``include/fvv_b200.h``).
+
+The shared library is built in-tree by ``paper_2007_00558_b200.build``. There
+is no CPU fallback: if the library is missing, importing the compute modules
+raises ``ImportError``; if no CUDA device is present, creating a context raises
+``RuntimeError``. Status codes map to the reference's exceptions:
+``FVV_EINVAL`` -> ``ValueError`` (the reference raises ValueError for every
+argument error), ``FVV_ECUDA`` -> ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).with_name("libfvvb200.so")
+
+FVV_OK, FVV_EINVAL, FVV_ECUDA = 0, 1, 2
+MAX_REFS = 16
+MAX_SLOTS = 64
+
+# every entry point declared in include/fvv_b200.h
+EXPORTS = (
+    "fvv_ctx_create", "fvv_ctx_destroy", "fvv_ctx_set_stream", "fvv_sync", "fvv_last_error",
+    "fvv_version", "fvv_launch_count", "fvv_decode_mm", "fvv_decode_yuv420_12",
+    "fvv_dequantize12", "fvv_bilateral_close_holes", "fvv_synthesize_view", "fvv_warp_layer",
+    "fvv_mix_layer", "fvv_composite", "fvv_slot_set_camera", "fvv_slot_set_bg",
+    "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slot_ingest_yuv", "fvv_render_views",
+    "fvv_profile_enable", "fvv_profile_read",
+)
+KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
+
+
+class FvvCamera(C.Structure):
+    _fields_ = [("id", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("reserved", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("R", C.c_double * 9),
+                ("C", C.c_double * 3)]
+
+
+class FvvSynthCfg(C.Structure):
+    _fields_ = [("splat_radius", C.c_int32), ("crack_fill_window", C.c_int32),
+                ("mixing_epsilon", C.c_double), ("depth_band_rel", C.c_double),
+                ("hole_color", C.c_uint8 * 3), ("angular_weight", C.c_uint8),
+                ("inpaint", C.c_uint8), ("reserved", C.c_uint8 * 3)]
+
+
+class FvvRefFrame(C.Structure):
+    _fields_ = [("cam", FvvCamera), ("rgb", C.c_void_p), ("live_depth", C.c_void_p),
+                ("live_validity", C.c_void_p), ("bg_depth", C.c_void_p),
+                ("bg_validity", C.c_void_p), ("weight", C.c_double)]
+
+
+class FvvDebug(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "contrib_color", "contrib_depth", "contrib_valid", "contrib_winner", "contrib_stage",
+        "merged_color", "merged_depth", "merged_valid")]
+
+
+_VP, _I32, _D = C.c_void_p, C.c_int32, C.c_double
+_SIGS = {
+    "fvv_ctx_create": ([_I32, C.POINTER(C.c_void_p)], C.c_int),
+    "fvv_ctx_destroy": ([_VP], C.c_int),
+    "fvv_ctx_set_stream": ([_VP, _VP], C.c_int),
+    "fvv_sync": ([_VP], C.c_int),
+    "fvv_last_error": ([_VP], C.c_char_p),
+    "fvv_version": ([], C.c_char_p),
+    "fvv_launch_count": ([_VP], C.c_int64),
+    "fvv_decode_mm": ([_VP, _VP, _VP, _I32, _I32, _VP, _VP], C.c_int),
+    "fvv_decode_yuv420_12": ([_VP, _VP, _VP, _VP, _I32, _I32, _D, _D, _VP, _VP, _VP], C.c_int),
+    "fvv_dequantize12": ([_VP, _VP, _I32, _I32, _D, _D, _VP, _VP], C.c_int),
+    "fvv_bilateral_close_holes": ([_VP, _VP, _VP, _VP, _I32, _I32, _I32, _D, _D, _I32, _VP,
+                                   _VP, _VP], C.c_int),
+    "fvv_synthesize_view": ([_VP, C.POINTER(FvvCamera), C.POINTER(FvvRefFrame), _I32,
+                             C.POINTER(FvvSynthCfg), _VP, _VP, C.POINTER(FvvDebug)], C.c_int),
+    "fvv_warp_layer": ([_VP, C.POINTER(FvvCamera), C.POINTER(FvvCamera), _VP, _VP, _VP, _VP,
+                        _I32, C.POINTER(FvvSynthCfg), _VP, _VP, _VP, _VP, _VP], C.c_int),
+    "fvv_mix_layer": ([_VP, _I32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                       C.POINTER(C.c_void_p), C.POINTER(C.c_double), _I32, _I32, _D, _VP, _VP,
+                       _VP], C.c_int),
+    "fvv_composite": ([_VP, _VP, _VP, _VP, _VP, _I32, _I32, C.POINTER(C.c_uint8), _VP, _VP],
+                      C.c_int),
+    "fvv_slot_set_camera": ([_VP, _I32, C.POINTER(FvvCamera)], C.c_int),
+    "fvv_slot_set_bg": ([_VP, _I32, _VP, _VP], C.c_int),
+    "fvv_slot_ingest": ([_VP, _I32, _VP, _VP, _VP, _I32], C.c_int),
+    "fvv_slot_ingest_mm": ([_VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP], C.c_int),
+    "fvv_slot_ingest_yuv": ([_VP, _I32, _VP, _VP, _VP, _VP, _D, _D, _I32, _VP, _VP], C.c_int),
+    "fvv_profile_enable": ([_VP, _I32], C.c_int),
+    "fvv_profile_read": ([_VP, _I32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+    "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
+                          C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
+                         C.c_int),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load and type the shared library; raise ImportError when it is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g;"
+                    f" g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+        return _lib
+
+
+def camera(calib) -> FvvCamera:
+    """fvv_camera from any object shaped like ``core.CameraCalibration``."""
+    k = calib.intrinsics
+    c = FvvCamera()
+    c.id = int(calib.id)
+    c.width, c.height = int(k.width), int(k.height)
+    c.fx, c.fy, c.cx, c.cy = float(k.fx), float(k.fy), float(k.cx), float(k.cy)
+    c.R[:] = [float(x) for x in np.asarray(calib.pose.rotation, dtype=np.float64).ravel()]
+    c.C[:] = [float(x) for x in np.asarray(calib.pose.center, dtype=np.float64).ravel()]
+    return c
+
+
+def synth_cfg(cfg) -> FvvSynthCfg:
+    s = FvvSynthCfg()
+    s.splat_radius = int(cfg.splat_radius)
+    s.crack_fill_window = int(cfg.crack_fill_window)
+    s.mixing_epsilon = float(cfg.mixing_epsilon)
+    s.depth_band_rel = float(cfg.depth_band_rel)
+    s.hole_color[:] = [int(x) for x in cfg.hole_color]
+    s.angular_weight = int(bool(getattr(cfg, "angular_weight", False)))
+    s.inpaint = int(bool(getattr(cfg, "inpaint", False)))
+    return s
+
+
+class Context:
+    """One library context (device + stream + resident slots and canvases)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        h = C.c_void_p()
+        rc = self.lib.fvv_ctx_create(int(device), C.byref(h))
+        if rc != FVV_OK:
+            raise RuntimeError(f"fvv_ctx_create(device={device}) failed with status {rc} "
+                               "(no CUDA device?)")
+        self.h = h
+        self.device = int(device)
+
+    def check(self, rc: int, what: str = "") -> None:
+        if rc == FVV_OK:
+            return
+        msg = (self.lib.fvv_last_error(self.h) or b"").decode()
+        if rc == FVV_EINVAL:
+            raise ValueError(msg or what)
+        raise RuntimeError(f"{what}: {msg}")
+
+    def call(self, name: str, *args) -> None:
+        self.check(getattr(self.lib, name)(self.h, *args), name)
+
+    def set_stream(self, stream_handle: int) -> None:
+        self.check(self.lib.fvv_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    def launches(self) -> int:
+        return int(self.lib.fvv_launch_count(self.h))
+
+    def profile(self, enable: bool) -> None:
+        self.check(self.lib.fvv_profile_enable(self.h, int(bool(enable))), "profile")
+
+    def profile_read(self) -> dict:
+        out = {}
+        for name, kid in KERNELS.items():
+            ms, n = C.c_double(), C.c_int64()
+            self.check(self.lib.fvv_profile_read(self.h, kid, C.byref(ms), C.byref(n)))
+            out[name] = (ms.value, n.value)
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.fvv_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_contexts: dict = {}
+
+
+def context(device: int | None = None) -> Context:
+    """Per-device default context, bound to torch's current stream."""
+    import torch
+
+    if device is None:
+        device = torch.cuda.current_device()
+    ctx = _contexts.get(device)
+    if ctx is None:
+        ctx = _contexts[device] = Context(device)
+    ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    return ctx

@@ -1,0 +1,724 @@
+// C ABI of libfvvb200.so (include/fvv_b200.h): context, resident camera
+// slots, keyed z canvases with generation tags, and the launch sequence
+// preprocess -> forward warp -> resolve for each view.
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fvv_kernels.cuh"
+
+using namespace fvv;
+
+namespace {
+
+struct Slot {
+    bool has_cam = false, has_bg = false, has_frame = false;
+    fvv_camera cam{};
+    DevCam dev{};
+    size_t cap = 0;  // pixels allocated
+    double *rays = nullptr;  // rx[W] then ry[H]
+    uint32_t *texel = nullptr;
+    float *fgd = nullptr;
+    float *bgd = nullptr;
+    void release() {
+        cudaFree(rays);
+        cudaFree(texel);
+        cudaFree(fgd);
+        cudaFree(bgd);
+        rays = nullptr; texel = nullptr; fgd = nullptr; bgd = nullptr;
+        cap = 0;
+        has_cam = has_bg = has_frame = false;
+    }
+};
+
+}  // namespace
+
+struct fvv_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    Slot slots[FVV_MAX_SLOTS];
+    Slot tmp[FVV_MAX_REFS + 1];  // one-shot calls (synthesize_view / warp_layer)
+    // keyed z canvases: n contributions of (H+2r)(W+2r) keys
+    uint64_t *canvas = nullptr;
+    size_t canvas_cap = 0;  // keys allocated
+    int cW = -1, cH = -1, cr = -1, cn = 0;
+    int gen = -1;  // generation of the last view; -1 = canvases need a fill
+    // per-kernel event timing (fvv_profile_enable)
+    bool prof = false;
+    struct Rec { int kid; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    double prof_ms[5] = {0, 0, 0, 0, 0};
+    int64_t prof_n[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+int fail(fvv_ctx *ctx, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                       \
+    do {                                                                               \
+        cudaError_t e__ = (expr);                                                      \
+        if (e__ != cudaSuccess)                                                        \
+            return fail(ctx, FVV_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e__)); \
+    } while (0)
+
+cudaEvent_t prof_event(fvv_ctx *ctx) {
+    if (!ctx->pool.empty()) {
+        cudaEvent_t e = ctx->pool.back();
+        ctx->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+#define LAUNCH_K(kid, expr)                                              \
+    do {                                                                 \
+        cudaEvent_t a__ = nullptr, b__ = nullptr;                        \
+        if (ctx->prof) {                                                 \
+            a__ = prof_event(ctx);                                       \
+            b__ = prof_event(ctx);                                       \
+            CK(cudaEventRecord(a__, ctx->stream));                       \
+        }                                                                \
+        CK(expr);                                                        \
+        if (ctx->prof) {                                                 \
+            CK(cudaEventRecord(b__, ctx->stream));                       \
+            ctx->recs.push_back({kid, a__, b__});                        \
+        }                                                                \
+        ++ctx->launches;                                                 \
+    } while (0)
+#define LAUNCH(expr) LAUNCH_K(FVV_K_OTHER, expr)
+
+int enter(fvv_ctx *ctx) {
+    if (!ctx) return FVV_EINVAL;
+    ctx->err.clear();
+    CK(cudaSetDevice(ctx->device));
+    return FVV_OK;
+}
+
+int check_cam(fvv_ctx *ctx, const fvv_camera *c, const char *what) {
+    if (!c) return fail(ctx, FVV_EINVAL, "%s camera is NULL", what);
+    if (c->width <= 0 || c->height <= 0 || c->width % 2 || c->height % 2)
+        return fail(ctx, FVV_EINVAL, "%s camera: width and height must be positive and even", what);
+    if (!(c->fx > 0 && c->fy > 0))
+        return fail(ctx, FVV_EINVAL, "%s camera: focal lengths must be positive", what);
+    if ((long long)c->width * c->height > (1ll << 26))
+        return fail(ctx, FVV_EINVAL, "%s camera: more than 2^26 pixels", what);
+    return FVV_OK;
+}
+
+int check_cfg(fvv_ctx *ctx, const fvv_synth_cfg *cfg) {
+    if (!cfg) return fail(ctx, FVV_EINVAL, "config is NULL");
+    if (cfg->splat_radius < 0 || cfg->crack_fill_window < 1)
+        return fail(ctx, FVV_EINVAL, "bad splat/crack parameters");
+    if (cfg->splat_radius > 3 || cfg->crack_fill_window > 5)
+        return fail(ctx, FVV_EINVAL, "splat_radius > 3 or crack_fill_window > 5 not supported");
+    if (cfg->angular_weight || cfg->inpaint)
+        return fail(ctx, FVV_EINVAL, "angular weighting / inpainting are extensions outside "
+                                     "the reference and are not enabled in this build");
+    return FVV_OK;
+}
+
+int slot_alloc(fvv_ctx *ctx, Slot &s, const fvv_camera &cam) {
+    const size_t n = (size_t)cam.width * cam.height;
+    if (n > s.cap) {
+        s.release();
+        CK(cudaMalloc(&s.texel, n * sizeof(uint32_t)));
+        CK(cudaMalloc(&s.fgd, n * sizeof(float)));
+        CK(cudaMalloc(&s.bgd, n * sizeof(float)));
+        s.cap = n;
+    }
+    CK(cudaFree(s.rays));
+    s.rays = nullptr;
+    CK(cudaMalloc(&s.rays, (size_t)(cam.width + cam.height) * sizeof(double)));
+    s.cam = cam;
+    s.dev = to_dev(cam);
+    LAUNCH(launch_rays(s.dev, s.rays, s.rays + cam.width, ctx->stream));
+    s.has_cam = true;
+    s.has_bg = s.has_frame = false;
+    return FVV_OK;
+}
+
+int slot_camera(fvv_ctx *ctx, Slot &s, const fvv_camera &cam) {
+    if (s.has_cam && memcmp(&s.cam, &cam, sizeof(cam)) == 0) return FVV_OK;
+    if (s.has_cam && s.cam.width == cam.width && s.cam.height == cam.height) {
+        // same size: only the calibration changed; keep buffers, refresh rays
+        s.cam = cam;
+        s.dev = to_dev(cam);
+        LAUNCH(launch_rays(s.dev, s.rays, s.rays + cam.width, ctx->stream));
+        return FVV_OK;
+    }
+    return slot_alloc(ctx, s, cam);
+}
+
+PreprocParams base_pre(const Slot &s) {
+    PreprocParams p{};
+    p.W = s.cam.width;
+    p.H = s.cam.height;
+    return p;
+}
+
+void bilateral_params(PreprocParams &p, int radius, double sigma_s, double sigma_r, int min_valid) {
+    // depthproc.py:199-200, 212: spatial factor via libm exp on the host
+    // (Python's math.exp is the same libm call), range factor on device.
+    p.radius = radius;
+    p.min_valid = min_valid;
+    const double inv_2ss = 1.0 / (2.0 * (sigma_s * sigma_s));
+    p.inv_2sr = 1.0 / (2.0 * (sigma_r * sigma_r));
+    for (int dy = -radius; dy <= radius; ++dy)
+        for (int dx = -radius; dx <= radius; ++dx)
+            p.sw[dy + radius][dx + radius] = std::exp((double)(-(dy * dy + dx * dx)) * inv_2ss);
+}
+
+int ensure_canvas(fvv_ctx *ctx, int n, int W, int H, int r) {
+    const size_t per = (size_t)(W + 2 * r) * (H + 2 * r);
+    const size_t need = per * (size_t)n;
+    if (need > ctx->canvas_cap) {
+        CK(cudaFree(ctx->canvas));
+        ctx->canvas = nullptr;
+        CK(cudaMalloc(&ctx->canvas, need * sizeof(uint64_t)));
+        ctx->canvas_cap = need;
+        ctx->gen = -1;
+    }
+    if (ctx->cW != W || ctx->cH != H || ctx->cr != r || ctx->cn < n) {
+        ctx->cW = W; ctx->cH = H; ctx->cr = r; ctx->cn = n;
+        ctx->gen = -1;
+    }
+    // generation tags: keys of this view carry gen; anything else is empty.
+    // One fill per 127 views instead of a clear per view.
+    if (ctx->gen <= 0) {
+        LAUNCH_K(FVV_K_FILL, launch_fill_u64(ctx->canvas, per * (size_t)ctx->cn, kEmpty, ctx->stream));
+        ctx->gen = 126;
+    } else {
+        ctx->gen -= 1;
+    }
+    return FVV_OK;
+}
+
+double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
+    const double dx = a.C[0] - b.C[0], dy = a.C[1] - b.C[1], dz = a.C[2] - b.C[2];
+    return 1.0 / (std::sqrt((dx * dx + dy * dy) + dz * dz) + eps);
+}
+
+// One view from n reference slots: K2 over 2n contributions, then K3.
+int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const double *weights,
+                int n, const fvv_synth_cfg &cfg, uint8_t *rgb_out, uint8_t *prov_out,
+                const fvv_debug *dbg) {
+    const int r = cfg.splat_radius;
+    int rc = ensure_canvas(ctx, 2 * n, virt.width, virt.height, r);
+    if (rc) return rc;
+    const size_t per = (size_t)(virt.width + 2 * r) * (virt.height + 2 * r);
+    const DevCam dst = to_dev(virt);
+
+    WarpParams wp{};
+    wp.dst = dst;
+    wp.r = r;
+    wp.n = 2 * n;
+    wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
+    ResolveParams rp{};
+    rp.dst = dst;
+    rp.r = r;
+    rp.window = cfg.crack_fill_window;
+    rp.need = cfg.crack_fill_window * cfg.crack_fill_window / 2 + 1;
+    rp.gen = (uint64_t)ctx->gen;
+    rp.n_fg = n;
+    rp.n_bg = n;
+    rp.band_rel = cfg.depth_band_rel;
+    for (int q = 0; q < 3; ++q) rp.hole[q] = (double)cfg.hole_color[q];
+    rp.rgb_out = rgb_out;
+    rp.prov_out = prov_out;
+    if (dbg) rp.dbg = *dbg;
+    long long maxpx = 0;
+    for (int j = 0; j < n; ++j) {
+        const Slot &s = *refs[j];
+        const double w = (weights && weights[j] > 0) ? weights[j]
+                                                     : host_weight(s.cam, virt, cfg.mixing_epsilon);
+        const int b = index_bits((long long)s.cam.width * s.cam.height);
+        const double *rx = s.rays, *ry = s.rays + s.cam.width;
+        for (int L = 0; L < 2; ++L) {
+            const int k = L * n + j;
+            const float *d = L == 0 ? s.fgd : s.bgd;
+            wp.c[k] = WarpContrib{s.dev, d, rx, ry, ctx->canvas + per * k, b};
+            rp.c[k] = ResolveContrib{s.dev, s.texel, d, rx, ry, ctx->canvas + per * k, w, b,
+                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
+        }
+        const long long np = (long long)s.cam.width * s.cam.height;
+        maxpx = np > maxpx ? np : maxpx;
+    }
+    LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
+    LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
+    return FVV_OK;
+}
+
+int check_slot_ready(fvv_ctx *ctx, int slot) {
+    if (slot < 0 || slot >= FVV_MAX_SLOTS) return fail(ctx, FVV_EINVAL, "slot %d out of range", slot);
+    const Slot &s = ctx->slots[slot];
+    if (!s.has_cam) return fail(ctx, FVV_EINVAL, "slot %d has no camera", slot);
+    if (!s.has_frame) return fail(ctx, FVV_EINVAL, "missing inputs for reference slot %d", slot);
+    if (!s.has_bg) return fail(ctx, FVV_EINVAL, "slot %d has no background model", slot);
+    return FVV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *fvv_version(void) { return "fvv_b200 0.1 sm_100a"; }
+
+int fvv_ctx_create(int32_t device, fvv_ctx **out) {
+    if (!out) return FVV_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return FVV_ECUDA;
+    }
+    if (device < 0 || device >= count) return FVV_EINVAL;
+    fvv_ctx *ctx = new fvv_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return FVV_ECUDA;
+    }
+    *out = ctx;
+    return FVV_OK;
+}
+
+int fvv_ctx_destroy(fvv_ctx *ctx) {
+    if (!ctx) return FVV_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &s : ctx->slots) s.release();
+    for (auto &s : ctx->tmp) s.release();
+    cudaFree(ctx->canvas);
+    for (auto &r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ctx->pool) cudaEventDestroy(e);
+    delete ctx;
+    return FVV_OK;
+}
+
+int fvv_ctx_set_stream(fvv_ctx *ctx, void *stream) {
+    if (!ctx) return FVV_EINVAL;
+    ctx->stream = (cudaStream_t)stream;
+    return FVV_OK;
+}
+
+int fvv_sync(fvv_ctx *ctx) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FVV_OK;
+}
+
+const char *fvv_last_error(const fvv_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t fvv_launch_count(const fvv_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+static int prof_drain(fvv_ctx *ctx) {
+    for (auto &r : ctx->recs) {
+        CK(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        ctx->prof_ms[r.kid] += ms;
+        ctx->prof_n[r.kid] += 1;
+        ctx->pool.push_back(r.a);
+        ctx->pool.push_back(r.b);
+    }
+    ctx->recs.clear();
+    return FVV_OK;
+}
+
+int fvv_profile_enable(fvv_ctx *ctx, int32_t enable) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if ((rc = prof_drain(ctx))) return rc;
+    ctx->prof = enable != 0;
+    for (int i = 0; i < 5; ++i) { ctx->prof_ms[i] = 0; ctx->prof_n[i] = 0; }
+    return FVV_OK;
+}
+
+int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (kernel_id < 0 || kernel_id > 4 || !total_ms || !launches)
+        return fail(ctx, FVV_EINVAL, "profile_read: bad arguments");
+    if ((rc = prof_drain(ctx))) return rc;
+    *total_ms = ctx->prof_ms[kernel_id];
+    *launches = ctx->prof_n[kernel_id];
+    return FVV_OK;
+}
+
+int fvv_decode_mm(fvv_ctx *ctx, const uint16_t *mm, const uint8_t *validity_in, int32_t width,
+                  int32_t height, float *depth_out, uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (width < 0 || height < 0 || !mm || !depth_out || !validity_out)
+        return fail(ctx, FVV_EINVAL, "decode_mm: bad arguments");
+    if (width == 0 || height == 0) return FVV_OK;
+    PreprocParams p{};
+    p.W = width;
+    p.H = height;
+    p.src = kSrcMM;
+    p.mm = mm;
+    p.validity = validity_in;
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_decode_yuv420_12(fvv_ctx *ctx, const uint8_t *y, const uint8_t *u, const uint8_t *v,
+                         int32_t width, int32_t height, double z_near, double z_far,
+                         float *depth_out, uint8_t *validity_out, uint16_t *codes_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (width < 0 || height < 0 || width % 2 || height % 2)
+        return fail(ctx, FVV_EINVAL, "YUV420 dimensions must be even");
+    if (!(0 < z_near && z_near < z_far))
+        return fail(ctx, FVV_EINVAL, "need 0 < z_near < z_far");
+    if (!y || !u || !v || !depth_out || !validity_out)
+        return fail(ctx, FVV_EINVAL, "decode_yuv420_12: NULL buffer");
+    if (width == 0 || height == 0) return FVV_OK;
+    PreprocParams p{};
+    p.W = width;
+    p.H = height;
+    p.src = kSrcYUV;
+    p.y = y; p.u = u; p.v = v;
+    p.inv_span = 1.0 / z_near - 1.0 / z_far;  // depthcodec.py:121
+    p.inv_zf = 1.0 / z_far;
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    p.codes_out = codes_out;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_dequantize12(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t height,
+                     double z_near, double z_far, float *depth_out, uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (width < 0 || height < 0 || !codes || !depth_out || !validity_out)
+        return fail(ctx, FVV_EINVAL, "dequantize12: bad arguments");
+    if (!(0 < z_near && z_near < z_far)) return fail(ctx, FVV_EINVAL, "need 0 < z_near < z_far");
+    if (width == 0 || height == 0) return FVV_OK;
+    PreprocParams p{};
+    p.W = width;
+    p.H = height;
+    p.src = kSrcCodes;
+    p.codes = codes;
+    p.inv_span = 1.0 / z_near - 1.0 / z_far;
+    p.inv_zf = 1.0 / z_far;
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                              const uint8_t *rgb, int32_t width, int32_t height, int32_t radius,
+                              double sigma_spatial, double sigma_range, int32_t min_valid,
+                              float *depth_out, uint8_t *validity_out, int32_t *n_holes_dev) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (width < 0 || height < 0 || !depth || !validity || !rgb || !depth_out || !validity_out)
+        return fail(ctx, FVV_EINVAL, "bilateral_close_holes: bad arguments");
+    if (radius < 0 || radius > 4)
+        return fail(ctx, FVV_EINVAL, "bilateral radius must be in [0, 4]");
+    if (width == 0 || height == 0) return FVV_OK;
+    PreprocParams p{};
+    p.W = width;
+    p.H = height;
+    p.src = kSrcF32;
+    p.depth = depth;
+    p.validity = validity;
+    p.rgb = rgb;
+    bilateral_params(p, radius, sigma_spatial, sigma_range, min_valid);
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    p.n_holes = n_holes_dev;
+    if (n_holes_dev) CK(cudaMemsetAsync(n_holes_dev, 0, sizeof(int32_t), ctx->stream));
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_slot_set_camera(fvv_ctx *ctx, int32_t slot, const fvv_camera *cam) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS) return fail(ctx, FVV_EINVAL, "slot %d out of range", slot);
+    if ((rc = check_cam(ctx, cam, "slot"))) return rc;
+    return slot_camera(ctx, ctx->slots[slot], *cam);
+}
+
+int fvv_slot_set_bg(fvv_ctx *ctx, int32_t slot, const float *bg_depth, const uint8_t *bg_validity) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS || !ctx->slots[slot].has_cam)
+        return fail(ctx, FVV_EINVAL, "slot %d has no camera", slot);
+    if (!bg_depth || !bg_validity) return fail(ctx, FVV_EINVAL, "bg model: NULL buffer");
+    Slot &s = ctx->slots[slot];
+    PreprocParams p = base_pre(s);
+    p.src = kSrcF32;
+    p.depth = bg_depth;
+    p.validity = bg_validity;
+    p.warp_depth = s.bgd;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    s.has_bg = true;
+    return FVV_OK;
+}
+
+int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float *depth,
+                    const uint8_t *validity, int32_t hole_closing) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS || !ctx->slots[slot].has_cam)
+        return fail(ctx, FVV_EINVAL, "slot %d has no camera", slot);
+    if (!rgb || !depth || !validity) return fail(ctx, FVV_EINVAL, "ingest: NULL buffer");
+    Slot &s = ctx->slots[slot];
+    PreprocParams p = base_pre(s);
+    p.src = kSrcF32;
+    p.depth = depth;
+    p.validity = validity;
+    p.rgb = rgb;
+    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
+    p.texel = s.texel;
+    p.warp_depth = s.fgd;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    s.has_frame = true;
+    return FVV_OK;
+}
+
+int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint16_t *mm,
+                       const uint8_t *validity, int32_t hole_closing, float *depth_out,
+                       uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS || !ctx->slots[slot].has_cam)
+        return fail(ctx, FVV_EINVAL, "slot %d has no camera", slot);
+    if (!rgb || !mm) return fail(ctx, FVV_EINVAL, "ingest_mm: NULL buffer");
+    Slot &s = ctx->slots[slot];
+    PreprocParams p = base_pre(s);
+    p.src = kSrcMM;
+    p.mm = mm;
+    p.validity = validity;
+    p.rgb = rgb;
+    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
+    p.texel = s.texel;
+    p.warp_depth = s.fgd;
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    s.has_frame = true;
+    return FVV_OK;
+}
+
+int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
+                        const uint8_t *u, const uint8_t *v, double z_near, double z_far,
+                        int32_t hole_closing, float *depth_out, uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS || !ctx->slots[slot].has_cam)
+        return fail(ctx, FVV_EINVAL, "slot %d has no camera", slot);
+    if (!rgb || !y || !u || !v) return fail(ctx, FVV_EINVAL, "ingest_yuv: NULL buffer");
+    if (!(0 < z_near && z_near < z_far)) return fail(ctx, FVV_EINVAL, "need 0 < z_near < z_far");
+    Slot &s = ctx->slots[slot];
+    PreprocParams p = base_pre(s);
+    p.src = kSrcYUV;
+    p.y = y; p.u = u; p.v = v;
+    p.inv_span = 1.0 / z_near - 1.0 / z_far;
+    p.inv_zf = 1.0 / z_far;
+    p.rgb = rgb;
+    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);
+    p.texel = s.texel;
+    p.warp_depth = s.fgd;
+    p.depth_out = depth_out;
+    p.validity_out = validity_out;
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    s.has_frame = true;
+    return FVV_OK;
+}
+
+int fvv_render_views(fvv_ctx *ctx, const fvv_camera *virts, int32_t n_views,
+                     const int32_t *ref_slots, const double *weights, int32_t n_refs,
+                     const fvv_synth_cfg *cfg, uint8_t *rgb_out, uint8_t *provenance_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n_views < 0 || !virts || !ref_slots) return fail(ctx, FVV_EINVAL, "render_views: bad arguments");
+    if (n_refs < 1) return fail(ctx, FVV_EINVAL, "need at least one reference camera");
+    if (n_refs > FVV_MAX_REFS) return fail(ctx, FVV_EINVAL, "more than %d references", FVV_MAX_REFS);
+    if ((rc = check_cfg(ctx, cfg))) return rc;
+    for (int i = 0; i < n_views; ++i) {
+        if ((rc = check_cam(ctx, &virts[i], "virtual"))) return rc;
+        if (virts[i].width != virts[0].width || virts[i].height != virts[0].height)
+            return fail(ctx, FVV_EINVAL, "all virtual views of a batch must share one size");
+        Slot *refs[FVV_MAX_REFS];
+        for (int j = 0; j < n_refs; ++j) {
+            const int sl = ref_slots[(size_t)i * n_refs + j];
+            if ((rc = check_slot_ready(ctx, sl))) return rc;
+            refs[j] = &ctx->slots[sl];
+        }
+        const size_t px = (size_t)virts[i].width * virts[i].height;
+        rc = render_view(ctx, virts[i], refs, weights ? weights + (size_t)i * n_refs : nullptr,
+                         n_refs, *cfg, rgb_out ? rgb_out + px * 3 * i : nullptr,
+                         provenance_out ? provenance_out + px * i : nullptr, nullptr);
+        if (rc) return rc;
+    }
+    return FVV_OK;
+}
+
+int fvv_synthesize_view(fvv_ctx *ctx, const fvv_camera *virt, const fvv_ref_frame *refs,
+                        int32_t n_refs, const fvv_synth_cfg *cfg, uint8_t *rgb_out,
+                        uint8_t *provenance_out, const fvv_debug *dbg) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n_refs < 1 || !refs) return fail(ctx, FVV_EINVAL, "need at least one reference camera");
+    if (n_refs > FVV_MAX_REFS) return fail(ctx, FVV_EINVAL, "more than %d references", FVV_MAX_REFS);
+    if ((rc = check_cfg(ctx, cfg))) return rc;
+    if ((rc = check_cam(ctx, virt, "virtual"))) return rc;
+    Slot *sl[FVV_MAX_REFS];
+    double w[FVV_MAX_REFS];
+    for (int j = 0; j < n_refs; ++j) {
+        const fvv_ref_frame &f = refs[j];
+        if ((rc = check_cam(ctx, &f.cam, "reference"))) return rc;
+        if (!f.rgb || !f.live_depth || !f.live_validity || !f.bg_depth || !f.bg_validity)
+            return fail(ctx, FVV_EINVAL, "missing inputs for reference camera %d", f.cam.id);
+        Slot &s = ctx->tmp[j];
+        if ((rc = slot_camera(ctx, s, f.cam))) return rc;
+        PreprocParams p = base_pre(s);
+        p.src = kSrcF32;
+        p.depth = f.live_depth;
+        p.validity = f.live_validity;
+        p.rgb = f.rgb;
+        p.texel = s.texel;
+        p.warp_depth = s.fgd;
+        LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+        PreprocParams q = base_pre(s);
+        q.src = kSrcF32;
+        q.depth = f.bg_depth;
+        q.validity = f.bg_validity;
+        q.warp_depth = s.bgd;
+        LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(q, ctx->stream));
+        sl[j] = &s;
+        w[j] = f.weight;
+    }
+    return render_view(ctx, *virt, sl, w, n_refs, *cfg, rgb_out, provenance_out, dbg);
+}
+
+int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, const uint8_t *rgb,
+                   const float *depth, const uint8_t *validity, const uint8_t *color_valid,
+                   int32_t layer_fg, const fvv_synth_cfg *cfg, double *color_out,
+                   double *depth_out, uint8_t *valid_out, int32_t *winner_out,
+                   uint8_t *stage_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if ((rc = check_cfg(ctx, cfg))) return rc;
+    if ((rc = check_cam(ctx, src, "source"))) return rc;
+    if ((rc = check_cam(ctx, dst, "virtual"))) return rc;
+    if (!rgb || !depth || !validity || !valid_out)
+        return fail(ctx, FVV_EINVAL, "warp_layer: NULL buffer");
+    Slot &s = ctx->tmp[FVV_MAX_REFS];
+    if ((rc = slot_camera(ctx, s, *src))) return rc;
+    PreprocParams p = base_pre(s);
+    p.src = kSrcF32;
+    p.depth = depth;
+    p.validity = validity;
+    p.rgb = rgb;
+    p.color_valid = color_valid;
+    p.texel = s.texel;
+    p.warp_depth = s.fgd;
+    if (!color_valid) {
+        // colour validity defaults to the depth validity (synthesis.py:185-186):
+        // flag bit 0 is exactly that
+    }
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    const int r = cfg->splat_radius;
+    if ((rc = ensure_canvas(ctx, 1, dst->width, dst->height, r))) return rc;
+    const DevCam dd = to_dev(*dst);
+    const int b = index_bits((long long)src->width * src->height);
+    const double *rx = s.rays, *ry = s.rays + src->width;
+    WarpParams wp{};
+    wp.dst = dd;
+    wp.r = r;
+    wp.n = 1;
+    wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
+    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas, b};
+    LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, (long long)src->width * src->height, ctx->stream));
+    ResolveParams rp{};
+    rp.dst = dd;
+    rp.r = r;
+    rp.window = cfg->crack_fill_window;
+    rp.need = cfg->crack_fill_window * cfg->crack_fill_window / 2 + 1;
+    rp.gen = (uint64_t)ctx->gen;
+    rp.n_fg = layer_fg ? 1 : 0;
+    rp.n_bg = layer_fg ? 0 : 1;
+    rp.band_rel = cfg->depth_band_rel;
+    rp.dbg.contrib_color = color_out;
+    rp.dbg.contrib_depth = depth_out;
+    rp.dbg.contrib_valid = valid_out;
+    rp.dbg.contrib_winner = winner_out;
+    rp.dbg.contrib_stage = stage_out;
+    rp.c[0] = ResolveContrib{s.dev, s.texel, s.fgd, rx, ry, ctx->canvas,
+                             host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
+                             layer_fg ? 1 : 0};
+    LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_mix_layer(fvv_ctx *ctx, int32_t n, const double *const *colors, const double *const *depths,
+                  const uint8_t *const *valids, const double *weights, int32_t width,
+                  int32_t height, double depth_band_rel, double *color_out, double *depth_out,
+                  uint8_t *valid_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 1) return fail(ctx, FVV_EINVAL, "need at least one contribution");
+    if (n > 2 * FVV_MAX_REFS) return fail(ctx, FVV_EINVAL, "too many contributions");
+    if (!colors || !depths || !valids || !weights || !color_out || !depth_out || !valid_out)
+        return fail(ctx, FVV_EINVAL, "mix_layer: NULL buffer");
+    MixParams p{};
+    p.n = n;
+    p.W = width;
+    p.H = height;
+    p.band_rel = depth_band_rel;
+    for (int j = 0; j < n; ++j) {
+        if (!(weights[j] > 0)) return fail(ctx, FVV_EINVAL, "contribution weight must be positive");
+        p.color[j] = colors[j];
+        p.depth[j] = depths[j];
+        p.valid[j] = valids[j];
+        p.weight[j] = weights[j];
+    }
+    p.color_out = color_out;
+    p.depth_out = depth_out;
+    p.valid_out = valid_out;
+    LAUNCH(launch_mix(p, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_composite(fvv_ctx *ctx, const double *fg_color, const uint8_t *fg_valid,
+                  const double *bg_color, const uint8_t *bg_valid, int32_t width, int32_t height,
+                  const uint8_t hole_color[3], uint8_t *rgb_out, uint8_t *provenance_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!fg_color || !fg_valid || !bg_color || !bg_valid || !hole_color || !rgb_out)
+        return fail(ctx, FVV_EINVAL, "composite: NULL buffer");
+    const double hole[3] = {(double)hole_color[0], (double)hole_color[1], (double)hole_color[2]};
+    LAUNCH(launch_composite(fg_color, fg_valid, bg_color, bg_valid, width, height, hole, rgb_out,
+                            provenance_out, ctx->stream));
+    return FVV_OK;
+}
+
+}  // extern "C"

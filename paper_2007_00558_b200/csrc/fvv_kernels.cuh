@@ -1,0 +1,103 @@
+// Kernel parameter blocks and host launchers (implemented in fvv_kernels.cu).
+#pragma once
+
+#include "fvv_common.cuh"
+
+namespace fvv {
+
+// Texel flags (byte 3 of the packed RGBA texel).
+constexpr uint32_t kFlagLiveValid = 1u;       // live validity == VALID  -> FG colour source
+constexpr uint32_t kFlagLiveBackground = 2u;  // live validity == BACKGROUND -> BG colour source
+
+// Where a per-camera live depth comes from.
+enum DepthSource : int { kSrcF32 = 0, kSrcMM = 1, kSrcYUV = 2, kSrcCodes = 3 };
+
+struct PreprocParams {
+    int W, H;
+    int src;                 // DepthSource
+    const float *depth;      // kSrcF32
+    const uint8_t *validity; // kSrcF32 / kSrcMM (may be null for MM -> all Valid)
+    const uint16_t *mm;      // kSrcMM
+    const uint8_t *y, *u, *v;// kSrcYUV
+    const uint16_t *codes;   // kSrcCodes
+    double inv_span, inv_zf; // kSrcYUV: 1/zn - 1/zf, 1/zf (host-evaluated like numpy)
+    const uint8_t *rgb;      // guide / colour (H*W*3)
+    const uint8_t *color_valid; // optional explicit colour-valid mask -> flag bit 0
+    // joint bilateral (depthproc.py:171-224); radius 0 disables
+    int radius, min_valid;
+    double sw[9][9];         // spatial weights math.exp(-(dy^2+dx^2)/(2 s^2)), host evaluated
+    double inv_2sr;          // 1/(2 sigma_range^2)
+    // outputs (any may be null)
+    uint32_t *texel;         // packed RGB + flags
+    float *warp_depth;       // depth where Valid else 0
+    float *depth_out;        // decoded / filled DepthFrame depth
+    uint8_t *validity_out;   // decoded / filled DepthFrame validity
+    uint16_t *codes_out;     // kSrcYUV 12-bit codes
+    int *n_holes;            // count of Invalid pixels before filling
+};
+
+struct WarpContrib {
+    DevCam src;
+    const float *depth;      // > 0 marks a source pixel (Valid), else 0
+    const double *rx, *ry;   // src ray slope tables (core.py:224-227)
+    uint64_t *canvas;        // (Hd+2r) x (Wd+2r) keys
+    int b;                   // index bits
+};
+
+struct WarpParams {
+    DevCam dst;
+    int r;
+    int n;
+    uint64_t gen_hi;         // generation code << 57
+    WarpContrib c[2 * FVV_MAX_REFS];
+};
+
+struct ResolveContrib {
+    DevCam src;
+    const uint32_t *texel;
+    const float *depth;
+    const double *rx, *ry;
+    const uint64_t *canvas;
+    double weight;
+    int b;
+    uint32_t flag;           // texel flag bit that marks colour-valid source pixels
+    int layer_fg;
+};
+
+struct ResolveParams {
+    DevCam dst;
+    int r, window, need;
+    uint64_t gen;            // generation code (0..127)
+    int n_fg, n_bg;
+    double band_rel;
+    double hole[3];
+    uint8_t *rgb_out;        // H*W*3 (may be null)
+    uint8_t *prov_out;       // H*W (may be null)
+    fvv_debug dbg;
+    ResolveContrib c[2 * FVV_MAX_REFS];
+};
+
+struct MixParams {
+    int n, W, H;
+    double band_rel;
+    const double *color[FVV_MAX_REFS * 2];
+    const double *depth[FVV_MAX_REFS * 2];
+    const uint8_t *valid[FVV_MAX_REFS * 2];
+    double weight[FVV_MAX_REFS * 2];
+    double *color_out, *depth_out;
+    uint8_t *valid_out;
+};
+
+// host launchers; return cudaGetLastError()
+cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s);
+cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s);
+cudaError_t launch_forward_warp(const WarpParams &p, long long max_src_pixels, cudaStream_t s);
+cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s);
+cudaError_t launch_mix(const MixParams &p, cudaStream_t s);
+cudaError_t launch_composite(const double *fg_c, const uint8_t *fg_v, const double *bg_c,
+                             const uint8_t *bg_v, int W, int H, const double hole[3],
+                             uint8_t *rgb, uint8_t *prov, cudaStream_t s);
+cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
+size_t resolve_smem_bytes(int maxr);
+
+}  // namespace fvv

@@ -1,0 +1,154 @@
+"""Edge-server session: resident camera slots and batched view rendering.
+
+``EdgeRenderer`` is the B200 form of the reference's edge-server render tick
+(``EdgeServer.render_tick``, pipeline.py:496-566): it keeps, per rig camera,
+the calibration, the static background model (uploaded once, pipeline.py:445)
+and the latest live frame resident in HBM; ``render`` then synthesizes any
+number of virtual views from them (``synthesize_with_config`` seam,
+pipeline.py:569-570). Frames arrive either as DepthFrames or in the wire
+formats the edge server decodes (16-bit mm raster, 12-bit YUV420), with the
+decode and hole fill fused into one kernel.
+
+``synthesize(virtual_camera, mvd_frame, ...)`` is the one-call convenience
+the north star names.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Mapping, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _dev, _native
+from .geometry import camera_distance
+from .selection import select_references
+from .synthesis import SynthesisConfig
+from .types import ColorFrame
+
+
+class EdgeRenderer:
+    def __init__(self, rig: Sequence, bg_models: Optional[Mapping] = None,
+                 cfg: Optional[SynthesisConfig] = None, device: Optional[int] = None):
+        self.ctx = _native.context(device)
+        self.cfg = cfg or SynthesisConfig()
+        self.rig = list(rig)
+        self.by_id = {c.id: c for c in self.rig}
+        if len(self.rig) > _native.MAX_SLOTS:
+            raise ValueError(f"at most {_native.MAX_SLOTS} cameras per renderer")
+        self.slot = {c.id: i for i, c in enumerate(self.rig)}
+        for c in self.rig:
+            self.ctx.call("fvv_slot_set_camera", self.slot[c.id], C.byref(_native.camera(c)))
+        self.ingested = set()
+        for cid, bg in (bg_models or {}).items():
+            self.set_bg_model(cid, bg)
+
+    def _bind(self):
+        self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
+
+    def _slot(self, cid) -> int:
+        if cid not in self.slot:
+            raise ValueError(f"camera {cid} is not in the rig")
+        return self.slot[cid]
+
+    # -- per-session / per-frame inputs --------------------------------------
+
+    def set_bg_model(self, cid, depth, validity=None) -> None:
+        """Static background depth model of camera ``cid`` (DepthFrame or arrays)."""
+        self._bind()
+        if validity is None:
+            depth, validity = depth.depth, depth.validity
+        d = _dev.upload(depth, np.float32)
+        v = _dev.upload(validity, np.uint8)
+        self.ctx.call("fvv_slot_set_bg", self._slot(cid), d.data_ptr(), v.data_ptr())
+
+    def ingest(self, cid, color, depth, hole_closing: bool = True) -> None:
+        """Live ColorFrame + DepthFrame of camera ``cid`` (pipeline.py:514-524)."""
+        self._bind()
+        rgb = _dev.upload(getattr(color, "pixels", color), np.uint8)
+        d = _dev.upload(depth.depth, np.float32)
+        v = _dev.upload(depth.validity, np.uint8)
+        self.ctx.call("fvv_slot_ingest", self._slot(cid), rgb.data_ptr(), d.data_ptr(),
+                      v.data_ptr(), int(bool(hole_closing)))
+        self.ingested.add(cid)
+
+    def ingest_mm(self, cid, rgb, mm, validity, hole_closing: bool = True,
+                  depth_out: Optional[torch.Tensor] = None,
+                  validity_out: Optional[torch.Tensor] = None) -> None:
+        """Live frame as the 16-bit mm raster + validity sidecar (mvdio.py:132):
+        fused mm decode + bilateral hole fill + ingest."""
+        self._bind()
+        rgb_t = _dev.upload(rgb, np.uint8)
+        mm_t = _dev.upload(mm, np.uint16)
+        v_t = None if validity is None else _dev.upload(validity, np.uint8)
+        self.ctx.call("fvv_slot_ingest_mm", self._slot(cid), rgb_t.data_ptr(), mm_t.data_ptr(),
+                      _dev.ptr(v_t), int(bool(hole_closing)), _dev.ptr(depth_out),
+                      _dev.ptr(validity_out))
+        self.ingested.add(cid)
+
+    def ingest_yuv(self, cid, rgb, y, u, v, depth_range, hole_closing: bool = True) -> None:
+        """Live frame as the 12-bit YUV420 depth raster (pipeline.py:469-472)."""
+        self._bind()
+        t = [_dev.upload(a, np.uint8) for a in (rgb, y, u, v)]
+        self.ctx.call("fvv_slot_ingest_yuv", self._slot(cid), *[x.data_ptr() for x in t],
+                      float(depth_range.z_near), float(depth_range.z_far),
+                      int(bool(hole_closing)), None, None)
+        self.ingested.add(cid)
+
+    # -- rendering -------------------------------------------------------------
+
+    def plan(self, virtuals: Sequence, refs=None):
+        """Reference ids per view (select_references over the ingested set when
+        ``refs`` is None, transport.py:226-238) and the blend weights."""
+        k = self.cfg.reference_count
+        if refs is None:
+            active = sorted(self.ingested)
+            refs = [select_references(v.pose, self.rig, active, min(k, len(active)))
+                    for v in virtuals]
+        refs = [list(r) for r in refs]
+        if not refs or any(len(r) != len(refs[0]) for r in refs):
+            raise ValueError("every view of a batch needs the same number of references")
+        if len(refs[0]) == 0:
+            raise ValueError("need at least one reference camera")
+        for r in refs:
+            for cid in r:
+                if cid not in self.ingested:
+                    raise ValueError(f"missing inputs for reference camera {cid}")
+        weights = [[1.0 / (camera_distance(self.by_id[cid].pose, v.pose) + self.cfg.mixing_epsilon)
+                    for cid in r] for v, r in zip(virtuals, refs)]
+        return refs, weights
+
+    def render(self, virtuals: Sequence, refs=None, out: Optional[torch.Tensor] = None,
+               provenance: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Synthesize ``len(virtuals)`` views; returns a (n, H, W, 3) uint8 CUDA tensor."""
+        self._bind()
+        virtuals = list(virtuals)
+        refs, weights = self.plan(virtuals, refs)
+        n, k = len(virtuals), len(refs[0])
+        W, H = int(virtuals[0].intrinsics.width), int(virtuals[0].intrinsics.height)
+        if out is None:
+            out = _dev.empty((n, H, W, 3), np.uint8)
+        cams = (_native.FvvCamera * n)(*[_native.camera(v) for v in virtuals])
+        slots = (C.c_int32 * (n * k))(*[self.slot[c] for r in refs for c in r])
+        wts = (C.c_double * (n * k))(*[w for ws in weights for w in ws])
+        self.ctx.call("fvv_render_views", cams, n, slots, wts, k,
+                      C.byref(_native.synth_cfg(self.cfg)), out.data_ptr(), _dev.ptr(provenance))
+        return out
+
+    def synthesize(self, virtual, mvd_frame: Optional[Mapping] = None, refs=None,
+                   hole_closing: bool = True) -> ColorFrame:
+        """One view on the host: optional new frame (``{id: MvdFrame}``), then render."""
+        for cid, f in (mvd_frame or {}).items():
+            self.ingest(cid, f.color, f.depth, hole_closing=hole_closing)
+        img = self.render([virtual], None if refs is None else [refs])
+        W, H = int(virtual.intrinsics.width), int(virtual.intrinsics.height)
+        return ColorFrame(W, H, img[0].cpu().numpy())
+
+
+def synthesize(virtual_camera, mvd_frame: Mapping, refs=None, cfg: Optional[SynthesisConfig] = None,
+               *, rig: Sequence, bg_models: Mapping, hole_closing: bool = True) -> ColorFrame:
+    """North-star convenience call: ``mvd_frame`` maps camera id -> MvdFrame;
+    ``refs=None`` selects ``cfg.reference_count`` nearest cameras."""
+    r = EdgeRenderer(rig, bg_models, cfg)
+    return r.synthesize(virtual_camera, mvd_frame, refs, hole_closing=hole_closing)

@@ -1,0 +1,303 @@
+"""Layered DIBR view synthesis on B200 — drop-in for ``fvv.synthesis``.
+
+Same public names, signatures, return types and ``ValueError`` cases as the
+reference module (``/root/reference/pkg/src/fvv/synthesis.py``); every raster
+operation runs in the sm_100a kernels of ``libfvvb200.so`` through the C ABI
+(``include/fvv_b200.h``):
+
+=======================  ==============================  =====================
+this module              reference                       C ABI / kernels
+=======================  ==============================  =====================
+``synthesize_view``      synthesis.py:331-362            fvv_synthesize_view (K2+K3)
+``synthesize_view_debug``synthesis.py:376-397            fvv_synthesize_view + fvv_debug
+``warp_layer``           synthesis.py:162-258            fvv_warp_layer
+``mix_layer``            synthesis.py:261-292            fvv_mix_layer
+``composite``            synthesis.py:295-318            fvv_composite
+``view_psnr``            synthesis.py:439-460            host metric (not on the path)
+``border_mask``          synthesis.py:463-471            host helper
+=======================  ==============================  =====================
+
+Inputs may be numpy arrays (copied to the device) or CUDA tensors; outputs
+are host numpy arrays, like the reference's. There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Mapping, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _dev, _native
+from .geometry import camera_distance
+from .types import ColorFrame, Validity
+
+LAYER_FG = "fg"
+LAYER_BG = "bg"
+
+
+@dataclass(frozen=True)
+class SynthesisConfig:
+    """synthesis.SynthesisConfig (synthesis.py:36-49)."""
+
+    reference_count: int = 3
+    splat_radius: int = 1
+    crack_fill_window: int = 3
+    mixing_epsilon: float = 0.01
+    depth_band_rel: float = 0.02
+    hole_color: Tuple[int, int, int] = (0, 0, 0)
+
+    def __post_init__(self):
+        if self.reference_count < 1:
+            raise ValueError("reference count must be >= 1")
+        if self.splat_radius < 0 or self.crack_fill_window < 1:
+            raise ValueError("bad splat/crack parameters")
+
+
+@dataclass(frozen=True)
+class LayerContribution:
+    """One camera's warped layer in virtual-view coordinates (synthesis.py:52-65).
+
+    ``winner`` / ``stage`` are extra rasters the reference does not keep:
+    the z-buffer winner's source pixel index and how the pixel was covered
+    (0 none, 1 centre, 2 splat, 3 crack median).
+    """
+
+    layer: str
+    camera_id: int
+    color: np.ndarray
+    depth: np.ndarray
+    valid: np.ndarray
+    weight: float
+    winner: Optional[np.ndarray] = field(default=None, compare=False, repr=False)
+    stage: Optional[np.ndarray] = field(default=None, compare=False, repr=False)
+
+    def __post_init__(self):
+        if self.weight <= 0:
+            raise ValueError("contribution weight must be positive")
+
+
+@dataclass(frozen=True)
+class MergedLayer:
+    color: np.ndarray
+    depth: np.ndarray
+    valid: np.ndarray
+
+
+@dataclass(frozen=True)
+class CameraStreamInputs:
+    """Everything one reference camera contributes (synthesis.py:321-328)."""
+
+    calib: object
+    live_color: object
+    live_depth: object
+    bg_depth: object
+
+
+@dataclass(frozen=True)
+class DebugBundle:
+    fg_contributions: Tuple[LayerContribution, ...]
+    bg_contributions: Tuple[LayerContribution, ...]
+    fg: MergedLayer
+    bg: MergedLayer
+    provenance: np.ndarray
+
+
+def _wh(calib):
+    k = calib.intrinsics
+    return int(k.width), int(k.height)
+
+
+def _weight(src_calib, dst_calib, cfg) -> float:
+    return 1.0 / (camera_distance(src_calib.pose, dst_calib.pose) + cfg.mixing_epsilon)
+
+
+def warp_layer(color, depth, src, dst, cfg: SynthesisConfig,
+               color_valid: Optional[np.ndarray] = None,
+               layer: str = LAYER_FG) -> LayerContribution:
+    """Warp one camera's layer into ``dst`` (synthesis.py:162-258)."""
+    if (color.height, color.width) != (depth.height, depth.width):
+        raise ValueError("color and depth dimensions differ")
+    ctx = _native.context()
+    W, H = _wh(dst)
+    rgb = _dev.upload(color.pixels, np.uint8)
+    d = _dev.upload(depth.depth, np.float32)
+    v = _dev.upload(depth.validity, np.uint8)
+    cv = None if color_valid is None else _dev.upload(np.asarray(color_valid, bool), np.uint8)
+    out_c = _dev.empty((H, W, 3), np.float64)
+    out_d = _dev.empty((H, W), np.float64)
+    out_v = _dev.empty((H, W), np.uint8)
+    out_w = _dev.empty((H, W), np.int32)
+    out_s = _dev.empty((H, W), np.uint8)
+    ctx.call("fvv_warp_layer", C.byref(_native.camera(src)), C.byref(_native.camera(dst)),
+             rgb.data_ptr(), d.data_ptr(), v.data_ptr(), _dev.ptr(cv),
+             1 if layer == LAYER_FG else 0, C.byref(_native.synth_cfg(cfg)),
+             out_c.data_ptr(), out_d.data_ptr(), out_v.data_ptr(), out_w.data_ptr(),
+             out_s.data_ptr())
+    return LayerContribution(layer=layer, camera_id=src.id, color=_dev.host(out_c),
+                             depth=_dev.host(out_d), valid=_dev.host(out_v).astype(bool),
+                             weight=_weight(src, dst, cfg), winner=_dev.host(out_w),
+                             stage=_dev.host(out_s))
+
+
+def mix_layer(contribs: Sequence[LayerContribution], cfg: SynthesisConfig) -> MergedLayer:
+    """Distance-weighted blend within the depth band (synthesis.py:261-292)."""
+    if not contribs:
+        raise ValueError("need at least one contribution")
+    ctx = _native.context()
+    H, W = np.asarray(contribs[0].valid).shape
+    cols = [_dev.upload(c.color, np.float64) for c in contribs]
+    deps = [_dev.upload(c.depth, np.float64) for c in contribs]
+    vals = [_dev.upload(np.asarray(c.valid, bool), np.uint8) for c in contribs]
+    n = len(contribs)
+    arr = C.c_void_p * n
+    wts = (C.c_double * n)(*[float(c.weight) for c in contribs])
+    out_c = _dev.empty((H, W, 3), np.float64)
+    out_d = _dev.empty((H, W), np.float64)
+    out_v = _dev.empty((H, W), np.uint8)
+    ctx.call("fvv_mix_layer", n, arr(*[t.data_ptr() for t in cols]),
+             arr(*[t.data_ptr() for t in deps]), arr(*[t.data_ptr() for t in vals]), wts, W, H,
+             float(cfg.depth_band_rel), out_c.data_ptr(), out_d.data_ptr(), out_v.data_ptr())
+    return MergedLayer(color=_dev.host(out_c), depth=_dev.host(out_d),
+                       valid=_dev.host(out_v).astype(bool))
+
+
+def composite(fg: MergedLayer, bg: MergedLayer, cfg: SynthesisConfig,
+              return_provenance: bool = False):
+    """FG over BG over hole colour; provenance 0 hole / 1 bg / 2 fg (synthesis.py:295-318)."""
+    if np.asarray(fg.valid).shape != np.asarray(bg.valid).shape:
+        raise ValueError("layer dimensions differ")
+    ctx = _native.context()
+    H, W = np.asarray(fg.valid).shape
+    fc = _dev.upload(fg.color, np.float64)
+    fv = _dev.upload(np.asarray(fg.valid, bool), np.uint8)
+    bc = _dev.upload(bg.color, np.float64)
+    bv = _dev.upload(np.asarray(bg.valid, bool), np.uint8)
+    rgb = _dev.empty((H, W, 3), np.uint8)
+    prov = _dev.empty((H, W), np.uint8)
+    hole = (C.c_uint8 * 3)(*[int(x) for x in cfg.hole_color])
+    ctx.call("fvv_composite", fc.data_ptr(), fv.data_ptr(), bc.data_ptr(), bv.data_ptr(), W, H,
+             hole, rgb.data_ptr(), prov.data_ptr())
+    frame = ColorFrame(W, H, _dev.host(rgb))
+    return (frame, _dev.host(prov)) if return_provenance else frame
+
+
+def _ref_frames(virtual, inputs, refs, cfg):
+    if not refs:
+        raise ValueError("need at least one reference camera")
+    if len(refs) > _native.MAX_REFS:
+        raise ValueError(f"at most {_native.MAX_REFS} reference cameras")
+    frames = (_native.FvvRefFrame * len(refs))()
+    keep = []
+    for j, rid in enumerate(refs):
+        if rid not in inputs:
+            raise ValueError(f"missing inputs for reference camera {rid}")
+        s = inputs[rid]
+        for d in (s.live_depth, s.bg_depth):
+            if (s.live_color.height, s.live_color.width) != (d.height, d.width):
+                raise ValueError("color and depth dimensions differ")
+        bufs = (_dev.upload(s.live_color.pixels, np.uint8),
+                _dev.upload(s.live_depth.depth, np.float32),
+                _dev.upload(s.live_depth.validity, np.uint8),
+                _dev.upload(s.bg_depth.depth, np.float32),
+                _dev.upload(s.bg_depth.validity, np.uint8))
+        keep.append(bufs)
+        f = frames[j]
+        f.cam = _native.camera(s.calib)
+        f.rgb, f.live_depth, f.live_validity, f.bg_depth, f.bg_validity = \
+            [b.data_ptr() for b in bufs]
+        f.weight = _weight(s.calib, virtual, cfg)
+    return frames, keep
+
+
+def synthesize_view(virtual, inputs: Mapping[int, CameraStreamInputs], refs: Sequence[int],
+                    cfg: SynthesisConfig, return_provenance: bool = False):
+    """Render ``virtual`` from ``refs`` (synthesis.py:331-362) on the GPU."""
+    frames, _keep = _ref_frames(virtual, inputs, refs, cfg)
+    ctx = _native.context()
+    W, H = _wh(virtual)
+    rgb = _dev.empty((H, W, 3), np.uint8)
+    prov = _dev.empty((H, W), np.uint8) if return_provenance else None
+    ctx.call("fvv_synthesize_view", C.byref(_native.camera(virtual)), frames, len(refs),
+             C.byref(_native.synth_cfg(cfg)), rgb.data_ptr(), _dev.ptr(prov), None)
+    frame = ColorFrame(W, H, _dev.host(rgb))
+    return (frame, _dev.host(prov)) if return_provenance else frame
+
+
+def synthesize_view_debug(virtual, inputs: Mapping[int, CameraStreamInputs],
+                          refs: Sequence[int], cfg: SynthesisConfig):
+    """synthesize_view plus every intermediate raster (synthesis.py:376-397)."""
+    frames, _keep = _ref_frames(virtual, inputs, refs, cfg)
+    ctx = _native.context()
+    W, H = _wh(virtual)
+    n = len(refs)
+    rgb = _dev.empty((H, W, 3), np.uint8)
+    prov = _dev.empty((H, W), np.uint8)
+    cc = _dev.empty((2 * n, H, W, 3), np.float64)
+    cd = _dev.empty((2 * n, H, W), np.float64)
+    cv = _dev.empty((2 * n, H, W), np.uint8)
+    cw = _dev.empty((2 * n, H, W), np.int32)
+    cs = _dev.empty((2 * n, H, W), np.uint8)
+    mc = _dev.empty((2, H, W, 3), np.float64)
+    md = _dev.empty((2, H, W), np.float64)
+    mv = _dev.empty((2, H, W), np.uint8)
+    dbg = _native.FvvDebug(*[t.data_ptr() for t in (cc, cd, cv, cw, cs, mc, md, mv)])
+    ctx.call("fvv_synthesize_view", C.byref(_native.camera(virtual)), frames, n,
+             C.byref(_native.synth_cfg(cfg)), rgb.data_ptr(), prov.data_ptr(), C.byref(dbg))
+    cc, cd, cv, cw, cs, mc, md, mv = [_dev.host(t) for t in (cc, cd, cv, cw, cs, mc, md, mv)]
+    contribs = []
+    for k in range(2 * n):
+        rid = refs[k % n]
+        s = inputs[rid]
+        layer = LAYER_FG if k < n else LAYER_BG
+        contribs.append(LayerContribution(layer, s.calib.id, cc[k], cd[k], cv[k].astype(bool),
+                                          frames[k % n].weight, cw[k], cs[k]))
+    fg = MergedLayer(mc[0], md[0], mv[0].astype(bool))
+    bg = MergedLayer(mc[1], md[1], mv[1].astype(bool))
+    frame = ColorFrame(W, H, rgb)
+    return frame, DebugBundle(tuple(contribs[:n]), tuple(contribs[n:]), fg, bg, prov)
+
+
+def write_debug_bundle(root, frame_id: int, bundle: DebugBundle, timestamp_us: int = 0) -> None:
+    """Debug-raster dump in the reference's MVD container (synthesis.py:400-436).
+
+    The container format (``fvv.mvdio``) is outside this package's scope; when
+    the reference package is importable its writer is used, else this raises.
+    """
+    try:
+        from fvv import synthesis as _ref
+    except ImportError as e:  # pragma: no cover - depends on the host
+        raise NotImplementedError("write_debug_bundle needs the fvv MVD container writer") from e
+    _ref.write_debug_bundle(root, frame_id, bundle, timestamp_us)
+
+
+def view_psnr(synth, oracle, exclude: Optional[np.ndarray] = None) -> float:
+    """Masked PSNR in dB (synthesis.py:439-460); inf for identical images."""
+    if (synth.height, synth.width) != (oracle.height, oracle.width):
+        raise ValueError("image dimensions differ")
+    keep = np.ones((synth.height, synth.width), dtype=bool)
+    if exclude is not None:
+        keep &= ~np.asarray(exclude, dtype=bool)
+    if not keep.any():
+        raise ValueError("all pixels excluded; PSNR undefined")
+    diff = synth.pixels[keep].astype(np.float64) - oracle.pixels[keep].astype(np.float64)
+    mse = float(np.mean(diff ** 2))
+    return math.inf if mse == 0.0 else 10.0 * math.log10(255.0 ** 2 / mse)
+
+
+def border_mask(height: int, width: int, border: int) -> np.ndarray:
+    m = np.zeros((height, width), dtype=bool)
+    if border > 0:
+        m[:border] = True
+        m[-border:] = True
+        m[:, :border] = True
+        m[:, -border:] = True
+    return m
+
+
+__all__ = ["LAYER_FG", "LAYER_BG", "SynthesisConfig", "LayerContribution", "MergedLayer",
+           "CameraStreamInputs", "DebugBundle", "warp_layer", "mix_layer", "composite",
+           "synthesize_view", "synthesize_view_debug", "write_debug_bundle", "view_psnr",
+           "border_mask", "Validity"]

@@ -1,0 +1,208 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Three fixture families, all committed as compressed .npz:
+
+* ``syn_<case>.npz`` — reference ``synthesis.synthesize_view_debug`` on inputs
+  from this repo's seeded generator (``paper_2007_00558_b200.scenes``). The
+  inputs are NOT stored, only their sha256; the tests regenerate them
+  (numpy, deterministic) and check the hash. Stored: RGB, provenance,
+  per-contribution valid masks, merged-layer valid masks.
+* ``refscene_<case>.npz`` — the reference's OWN test scenes
+  (``scenegen.make_scene`` + ``conftest.gt_stream_inputs`` semantics, 128x96
+  rig of tests/conftest.py:10-15), inputs stored explicitly (small), plus the
+  reference outputs and, for the quality cases, the ray-cast ground truth and
+  coverage mask used by tests/test_synthesis.py:213-222 and
+  tests/test_acceptance.py:188-214.
+* ``es_<case>.npz`` / ``codec.npz`` — edge-server preprocessing: reference
+  ``depth_from_millimeters`` + ``bilateral_close_holes`` outputs on generated
+  mm frames, and ``unpack_yuv420``/``dequantize12`` on generated codes.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+OUT = Path(__file__).resolve().parent
+
+import fvv.core as rc  # noqa: E402
+import fvv.depthcodec as rcodec  # noqa: E402
+import fvv.depthproc as rproc  # noqa: E402
+import fvv.scenegen as rscene  # noqa: E402
+import fvv.synthesis as rs  # noqa: E402
+
+from paper_2007_00558_b200 import scenes  # noqa: E402
+
+# (case, config, scale, seed, view index)
+SYN_CASES = [
+    ("c0_s4", "c0", 4, 2007, 0),
+    ("c0_s2", "c0", 2, 2007, 0),
+    ("c0_s2_seed11", "c0", 2, 11, 0),
+    ("c1_s8", "c1", 8, 2007, 0),
+    ("c2_s8_v1", "c2", 8, 2007, 1),
+    ("c2_s8_v3", "c2", 8, 2007, 3),
+    ("c4_s16_v0", "c4", 16, 2007, 0),
+]
+ES_CASES = [("c1_s4", "c1", 4, 2007), ("c0_s1", "c0", 1, 2007)]
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def ref_calib(c):
+    k = c.intrinsics
+    return rc.CameraCalibration(c.id, rc.CameraIntrinsics(k.fx, k.fy, k.cx, k.cy, k.width,
+                                                          k.height),
+                                rc.CameraPose(np.asarray(c.pose.rotation), np.asarray(c.pose.center)))
+
+
+def workload(cfg, scale, seed):
+    return scenes.make_workload(cfg, seed=seed, scale=scale, n_views=4, n_frames=1)
+
+
+def input_hash(wl, view):
+    arrs = []
+    for rid in wl.refs[view]:
+        c = wl.frames[0][rid]
+        arrs += [c.rgb, c.mm, c.validity, c.bg_depth, c.bg_validity]
+    return sha(*arrs)
+
+
+def syn_case(case, cfg, scale, seed, view):
+    wl = workload(cfg, scale, seed)
+    v, refs = wl.virtuals[view], wl.refs[view]
+    inputs = {}
+    for rid in refs:
+        c = wl.frames[0][rid]
+        lf = c.depth_frame()
+        W, H = lf.width, lf.height
+        inputs[rid] = rs.CameraStreamInputs(ref_calib(c.calib), rc.ColorFrame(W, H, c.rgb),
+                                            rc.DepthFrame(W, H, lf.depth, lf.validity),
+                                            rc.DepthFrame(W, H, c.bg_depth, c.bg_validity))
+    frame, b = rs.synthesize_view_debug(ref_calib(v), inputs, refs, rs.SynthesisConfig())
+    cv = np.stack([c.valid for c in b.fg_contributions + b.bg_contributions])
+    np.savez_compressed(OUT / f"syn_{case}.npz", config=cfg, scale=scale, seed=seed, view=view,
+                        refs=np.asarray(refs), input_sha=input_hash(wl, view), rgb=frame.pixels,
+                        prov=b.provenance, contrib_valid=np.packbits(cv),
+                        contrib_shape=np.asarray(cv.shape),
+                        merged_valid=np.stack([b.fg.valid, b.bg.valid]))
+    print(case, wl.description, "refs", refs)
+
+
+def gt_inputs(scene, rig, ref_ids, t):
+    """conftest.gt_stream_inputs (tests/conftest.py:28-49), arrays only."""
+    out = {}
+    for rid in ref_ids:
+        mvd, fg = rscene.render_with_mask(scene, rig[rid], t)
+        d = mvd.depth.depth.copy()
+        d[~fg] = 0.0
+        out[rid] = dict(rgb=mvd.color.pixels, live_depth=d,
+                        live_validity=np.where(fg, 0, 2).astype(np.uint8),
+                        bg_depth=rscene.bg_depth_model(scene, rig[rid]).depth,
+                        bg_validity=np.zeros(d.shape, np.uint8))
+    return out
+
+
+def cam_arr(c):
+    k = c.intrinsics
+    return np.concatenate([[c.id, k.width, k.height, k.fx, k.fy, k.cx, k.cy],
+                           np.ravel(c.pose.rotation), c.pose.center]).astype(np.float64)
+
+
+def refscene_case(case, preset, virtual, refs, t, quality):
+    rig = rscene.build_camera_arc(9, 0.270, 60.0, width=128, height=96)
+    scene = rscene.make_scene(preset)
+    if virtual == "mid34":
+        center = (rig[3].pose.center + rig[4].pose.center) / 2.0
+        vcam = rc.CameraCalibration(200, rig[0].intrinsics, rscene.look_at_pose(center, np.zeros(3)))
+        refs = sorted(range(9), key=lambda i: (rc.camera_distance(rig[i].pose, vcam.pose), i))[:3]
+    else:
+        vcam = rig[virtual]
+    data = gt_inputs(scene, rig, refs, t)
+    inputs = {rid: rs.CameraStreamInputs(
+        rig[rid], rc.ColorFrame(128, 96, d["rgb"]),
+        rc.DepthFrame(128, 96, d["live_depth"], d["live_validity"]),
+        rc.DepthFrame(128, 96, d["bg_depth"], d["bg_validity"])) for rid, d in data.items()}
+    frame, b = rs.synthesize_view_debug(vcam, inputs, refs, rs.SynthesisConfig())
+    extra = {}
+    if quality:
+        extra["gt_rgb"] = rscene.render_ground_truth(scene, vcam, t).color.pixels
+        extra["covered"] = rscene.coverage_mask(scene, t, vcam, [rig[r] for r in refs])
+    cv = np.stack([c.valid for c in b.fg_contributions + b.bg_contributions])
+    arrs = {}
+    for j, rid in enumerate(refs):
+        for k, v in data[rid].items():
+            arrs[f"in{j}_{k}"] = v
+        arrs[f"in{j}_cam"] = cam_arr(rig[rid])
+    np.savez_compressed(OUT / f"refscene_{case}.npz", refs=np.asarray(refs), virt=cam_arr(vcam),
+                        rgb=frame.pixels, prov=b.provenance, contrib_valid=cv,
+                        merged_valid=np.stack([b.fg.valid, b.bg.valid]), **arrs, **extra)
+    print(case, preset, "refs", refs)
+
+
+def es_case(case, cfg, scale, seed):
+    wl = workload(cfg, scale, seed)
+    rid = wl.refs[0][0]
+    c = wl.frames[0][rid]
+    df = rc.depth_from_millimeters(c.mm, c.validity)
+    H, W = c.mm.shape
+    filled = rproc.bilateral_close_holes(df, rc.ColorFrame(W, H, c.rgb))
+    np.savez_compressed(OUT / f"es_{case}.npz", config=cfg, scale=scale, seed=seed, cam=rid,
+                        input_sha=sha(c.rgb, c.mm, c.validity), dec_depth=df.depth,
+                        dec_validity=df.validity, fill_depth=filled.depth,
+                        fill_validity=filled.validity)
+    print(case, "holes", int((df.validity == 1).sum()), "filled",
+          int(((df.validity == 1) & (filled.validity == 0)).sum()))
+
+
+def codec_case():
+    rng = np.random.default_rng(5)
+    H, W = 48, 64
+    codes = rng.integers(0, 4096, (H, W)).astype(np.uint16)
+    codes[:4, :4] = 0
+    codes[4:8, :4] = 1
+    codes[0, 4:] = np.arange(4, 64) % 4096
+    img = rcodec.pack_yuv420(rcodec.DisparityMap12(W, H, codes))
+    back = rcodec.unpack_yuv420(img)
+    rng_ = rc.DepthRange(0.5, 6.5)
+    deq = rcodec.dequantize12(back, rng_)
+    allc = np.arange(4096, dtype=np.uint16).reshape(64, 64)
+    deq_all = rcodec.dequantize12(rcodec.DisparityMap12(64, 64, allc), rng_)
+    mm = np.arange(65536, dtype=np.uint16).reshape(256, 256)
+    val = np.zeros(mm.shape, np.uint8)
+    val[::7] = 2
+    dmm = rc.depth_from_millimeters(mm, val)
+    np.savez_compressed(OUT / "codec.npz", codes=codes, y=img.y, u=img.u, v=img.v,
+                        unpacked=back.values, deq_depth=deq.depth, deq_validity=deq.validity,
+                        all_depth=deq_all.depth, all_validity=deq_all.validity, mm=mm,
+                        mm_validity=val, mm_depth=dmm.depth, mm_out_validity=dmm.validity)
+    print("codec ok")
+
+
+if __name__ == "__main__":
+    for args in SYN_CASES:
+        syn_case(*args)
+    refscene_case("identity_simple", "simple", 4, [4], 1.0, quality=True)
+    refscene_case("mid34_simple", "simple", "mid34", None, 2.0, quality=True)
+    refscene_case("mid34_medium", "medium", "mid34", None, 2.0, quality=True)
+    refscene_case("mid34_complex", "complex", "mid34", None, 2.0, quality=True)
+    refscene_case("r4_from345", "simple", 4, [3, 4, 5], 0.0, quality=False)
+    for args in ES_CASES:
+        es_case(*args)
+    codec_case()

@@ -1,0 +1,426 @@
+"""The reference's unit/acceptance tests for this path, restated against the
+drop-in API (the reference's test files cannot travel to the GPU box).
+
+Sources: tests/test_synthesis.py:40-233, tests/test_acceptance.py:188-214,
+tests/test_depthproc.py:227-319 of the reference package. Scene-based cases
+use the reference's own scenes through the refscene_* golden fixtures.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from _helpers import golden, psnr, refscene_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S(cuda):
+    from paper_2007_00558_b200 import synthesis
+
+    return synthesis
+
+
+@pytest.fixture(scope="module")
+def T():
+    from paper_2007_00558_b200 import types
+
+    return types
+
+
+def flat_calib(T, cam_id=0, center=(0.0, 0.0, 0.0), w=64, h=48, f=80.0):
+    return T.CameraCalibration(cam_id, T.CameraIntrinsics(f, f, w / 2.0, h / 2.0, w, h),
+                               T.CameraPose(np.eye(3), np.asarray(center, dtype=float)))
+
+
+def plane_inputs(T, depth_value, w=64, h=48, color_value=(120, 90, 200)):
+    depth = np.full((h, w), depth_value, dtype=np.float32)
+    px = np.zeros((h, w, 3), dtype=np.uint8)
+    px[:] = color_value
+    return T.ColorFrame(w, h, px), T.DepthFrame(w, h, depth, np.zeros((h, w), np.uint8))
+
+
+# ---------------------------------------------------------------- warp_layer
+
+
+def test_identity_warp_reproduces_color(S):
+    g = golden("refscene_identity_simple.npz")
+    case = refscene_case(g)
+    a = case.arrays[0]
+    from paper_2007_00558_b200.types import ColorFrame, DepthFrame
+    H, W = a["live_depth"].shape
+    # all-Valid ground-truth depth (reference test uses render_with_mask's depth)
+    full = np.where(a["live_validity"] == 0, a["live_depth"], a["bg_depth"]).astype(np.float32)
+    c = S.warp_layer(ColorFrame(W, H, a["rgb"]), DepthFrame(W, H, full, np.zeros((H, W), np.uint8)),
+                     a["calib"], a["calib"], S.SynthesisConfig())
+    assert c.valid.all()
+    assert (np.round(c.color).astype(np.uint8) == a["rgb"]).all()
+
+
+def test_translated_camera_shifts_by_analytic_disparity(S, T):
+    z, baseline, f = 2.0, 0.1, 80.0
+    color, depth = plane_inputs(T, z)
+    px = color.pixels.copy()
+    px[:, 30] = (255, 0, 0)
+    color = T.ColorFrame(64, 48, px)
+    c = S.warp_layer(color, depth, flat_calib(T, 0, (0, 0, 0), f=f),
+                     flat_calib(T, 1, (baseline, 0, 0), f=f), S.SynthesisConfig())
+    assert f * baseline / z == 4.0
+    out = np.round(c.color).astype(np.uint8)
+    assert (out[:, 26] == (255, 0, 0)).all()
+    assert c.valid[:, :64 - 5].all()
+
+
+def test_zbuffer_keeps_nearer_surface(S, T):
+    w, h, f = 64, 48, 80.0
+    depth = np.full((h, w), 3.0, dtype=np.float32)
+    depth[:, 28:37] = 1.0
+    px = np.zeros((h, w, 3), dtype=np.uint8)
+    px[:] = (0, 200, 0)
+    px[:, 28:37] = (200, 0, 0)
+    c = S.warp_layer(T.ColorFrame(w, h, px), T.DepthFrame(w, h, depth, np.zeros((h, w), np.uint8)),
+                     flat_calib(T, 0, (0, 0, 0), w, h, f), flat_calib(T, 1, (0.2, 0, 0), w, h, f),
+                     S.SynthesisConfig())
+    out = np.round(c.color).astype(np.uint8)
+    assert c.valid[:, 13:20].all()
+    assert (out[:, 13:20] == (200, 0, 0)).all()
+    # the winner-index map names the near stripe's source pixels there
+    cols = c.winner[:, 13:20] % w
+    assert ((cols >= 28) & (cols < 37)).all()
+
+
+def test_invalid_source_pixels_do_not_warp(S, T):
+    color, depth = plane_inputs(T, 2.0)
+    val = depth.validity.copy()
+    val[:, :32] = T.Validity.INVALID
+    d = depth.depth.copy()
+    d[:, :32] = 0.0
+    depth = T.DepthFrame(64, 48, d, val)
+    cam = flat_calib(T, 0)
+    c = S.warp_layer(color, depth, cam, cam, S.SynthesisConfig())
+    assert not c.valid[:, :30].any()
+    assert c.valid[:, 33:].all()
+
+
+def test_weight_positive_and_inverse_distance(S, T):
+    from paper_2007_00558_b200.geometry import build_camera_arc, camera_distance
+
+    rig = build_camera_arc(9, 0.270, 60.0, width=128, height=96)
+    color, depth = plane_inputs(T, 2.0, w=128, h=96)
+    c = S.warp_layer(color, depth, rig[3], rig[4], S.SynthesisConfig())
+    d = camera_distance(rig[3].pose, rig[4].pose)
+    assert c.weight == pytest.approx(1.0 / (d + 0.01))
+
+
+def test_color_depth_size_mismatch_rejected(S, T):
+    color, _ = plane_inputs(T, 2.0)
+    _, depth = plane_inputs(T, 2.0, w=32, h=24)
+    with pytest.raises(ValueError):
+        S.warp_layer(color, depth, flat_calib(T), flat_calib(T), S.SynthesisConfig())
+
+
+# ---------------------------------------------------------------- mix_layer
+
+
+def _contrib(S, color, depth, valid, weight, cam=0):
+    c = np.zeros(valid.shape + (3,))
+    c[:] = color
+    return S.LayerContribution("fg", cam, c, np.full(valid.shape, depth, dtype=np.float64),
+                               valid, weight)
+
+
+def test_single_contribution_identity(S):
+    v = np.ones((4, 4), bool)
+    m = S.mix_layer([_contrib(S, (10, 20, 30), 2.0, v, 1.0)], S.SynthesisConfig())
+    assert np.allclose(m.color[v], (10, 20, 30))
+    assert np.allclose(m.depth[v], 2.0)
+
+
+def test_equal_weights_average(S):
+    v = np.ones((4, 4), bool)
+    m = S.mix_layer([_contrib(S, (100, 0, 0), 2.0, v, 0.7),
+                     _contrib(S, (0, 100, 0), 2.0, v, 0.7, 1)], S.SynthesisConfig())
+    assert np.allclose(m.color[v], (50, 50, 0))
+
+
+def test_depth_band_excludes_occluded(S):
+    v = np.ones((4, 4), bool)
+    m = S.mix_layer([_contrib(S, (100, 0, 0), 1.0, v, 1.0),
+                     _contrib(S, (0, 100, 0), 1.5, v, 50.0, 1)],
+                    S.SynthesisConfig(depth_band_rel=0.05))
+    assert np.allclose(m.color[v], (100, 0, 0))
+
+
+def test_weights_renormalize_over_participants(S):
+    va = np.zeros((4, 4), bool)
+    va[:, :2] = True
+    m = S.mix_layer([_contrib(S, (80, 0, 0), 2.0, va, 0.25),
+                     _contrib(S, (0, 80, 0), 2.0, np.ones((4, 4), bool), 0.75, 1)],
+                    S.SynthesisConfig())
+    assert np.allclose(m.color[:, 0], (20, 60, 0))
+    assert np.allclose(m.color[:, 3], (0, 80, 0))
+
+
+def test_empty_list_rejected(S):
+    with pytest.raises(ValueError):
+        S.mix_layer([], S.SynthesisConfig())
+
+
+def test_nonpositive_weight_rejected(S):
+    with pytest.raises(ValueError):
+        _contrib(S, (1, 1, 1), 1.0, np.ones((2, 2), bool), 0.0)
+
+
+# ---------------------------------------------------------------- composite
+
+
+def _layer(S, color, valid):
+    c = np.zeros(valid.shape + (3,))
+    c[:] = color
+    return S.MergedLayer(c, np.ones(valid.shape), valid)
+
+
+def test_fg_everywhere(S):
+    v = np.ones((4, 6), bool)
+    out = S.composite(_layer(S, (9, 9, 9), v), _layer(S, (1, 1, 1), v), S.SynthesisConfig())
+    assert (out.pixels == 9).all()
+
+
+def test_fg_nowhere_bg_with_holes(S):
+    fv = np.zeros((4, 6), bool)
+    bv = np.ones((4, 6), bool)
+    bv[0, 0] = False
+    out = S.composite(_layer(S, (0, 0, 0), fv), _layer(S, (50, 60, 70), bv),
+                      S.SynthesisConfig(hole_color=(7, 8, 9)))
+    assert tuple(out.pixels[0, 0]) == (7, 8, 9)
+    assert tuple(out.pixels[1, 1]) == (50, 60, 70)
+
+
+def test_totality_and_provenance(S):
+    rng = np.random.default_rng(0)
+    fv = rng.random((6, 8)) < 0.4
+    bv = rng.random((6, 8)) < 0.6
+    out, prov = S.composite(_layer(S, (2, 2, 2), fv), _layer(S, (3, 3, 3), bv),
+                            S.SynthesisConfig(), return_provenance=True)
+    np.testing.assert_array_equal(prov == 2, fv)
+    np.testing.assert_array_equal(prov == 1, bv & ~fv)
+    np.testing.assert_array_equal(prov == 0, ~bv & ~fv)
+
+
+def test_composite_rounds_half_to_even_and_clips(S):
+    v = np.ones((1, 4), bool)
+    c = np.array([[[0.5, 1.5, 2.5], [254.5, 255.5, 300.0], [-3.0, 127.5, 128.5],
+                   [3.49999, 3.5, 4.5]]])
+    out = S.composite(S.MergedLayer(c, np.ones((1, 4)), v), _layer(S, (0, 0, 0), ~v),
+                      S.SynthesisConfig())
+    np.testing.assert_array_equal(out.pixels, np.clip(np.round(c), 0, 255).astype(np.uint8))
+
+
+def test_layer_shape_mismatch_rejected(S):
+    with pytest.raises(ValueError):
+        S.composite(_layer(S, (1, 1, 1), np.ones((2, 2), bool)),
+                    _layer(S, (1, 1, 1), np.ones((3, 2), bool)), S.SynthesisConfig())
+
+
+# ---------------------------------------------------------------- synthesize_view
+
+
+def test_identity_view_mostly_byte_exact(S):
+    """test_synthesis.py:189-195 / acceptance #8 (first half)."""
+    g = golden("refscene_identity_simple.npz")
+    case = refscene_case(g)
+    out = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig())
+    border = S.border_mask(out.height, out.width, 2)
+    same = (out.pixels == g["gt_rgb"]).all(-1)
+    assert same[~border].mean() >= 0.99
+
+
+@pytest.mark.parametrize("preset", ["simple", "medium", "complex"])
+def test_midpoint_masked_psnr_thirty_db(S, preset):
+    """test_synthesis.py:213-222 / acceptance #8 (second half), all presets."""
+    g = golden(f"refscene_mid34_{preset}.npz")
+    case = refscene_case(g)
+    out = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig())
+    exclude = ~g["covered"] | S.border_mask(out.height, out.width, 2)
+    from paper_2007_00558_b200.types import ColorFrame
+    assert S.view_psnr(out, ColorFrame(out.width, out.height, g["gt_rgb"]), exclude) >= 30.0
+    assert psnr(out.pixels, g["gt_rgb"], exclude) >= 30.0
+
+
+def test_empty_fg_equals_bg_only(S):
+    """test_synthesis.py:197-211 (no FG anywhere -> composite of BG alone)."""
+    g = golden("refscene_r4_from345.npz")
+    case = refscene_case(g)
+    inputs = case.inputs()
+    from paper_2007_00558_b200.types import DepthFrame
+    for rid, s in list(inputs.items()):
+        val = np.where(s.live_depth.validity == 0, 2, s.live_depth.validity).astype(np.uint8)
+        live = DepthFrame(s.live_depth.width, s.live_depth.height,
+                          np.zeros_like(s.live_depth.depth), val)
+        inputs[rid] = S.CameraStreamInputs(s.calib, s.live_color, live, s.bg_depth)
+    out = S.synthesize_view(case.virtual, inputs, case.refs, S.SynthesisConfig())
+    bgc = [S.warp_layer(s.live_color, s.bg_depth, s.calib, case.virtual, S.SynthesisConfig(),
+                        color_valid=s.live_depth.validity == 2, layer=S.LAYER_BG)
+           for s in (inputs[r] for r in case.refs)]
+    bg = S.mix_layer(bgc, S.SynthesisConfig())
+    empty = S.MergedLayer(np.zeros(bg.color.shape), np.zeros(bg.depth.shape),
+                          np.zeros(bg.valid.shape, bool))
+    np.testing.assert_array_equal(out.pixels, S.composite(empty, bg, S.SynthesisConfig()).pixels)
+
+
+def test_missing_reference_input_rejected(S):
+    case = refscene_case(golden("refscene_identity_simple.npz"))
+    with pytest.raises(ValueError):
+        S.synthesize_view(case.virtual, case.inputs(), [4, 5], S.SynthesisConfig())
+    with pytest.raises(ValueError):
+        S.synthesize_view(case.virtual, case.inputs(), [], S.SynthesisConfig())
+
+
+def test_deterministic(S):
+    case = refscene_case(golden("refscene_r4_from345.npz"))
+    a = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig())
+    b = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig())
+    np.testing.assert_array_equal(a.pixels, b.pixels)
+
+
+def test_debug_bundle_matches_plain_view(S):
+    case = refscene_case(golden("refscene_mid34_simple.npz"))
+    frame, b = S.synthesize_view_debug(case.virtual, case.inputs(), case.refs, S.SynthesisConfig())
+    plain, prov = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig(),
+                                    return_provenance=True)
+    np.testing.assert_array_equal(frame.pixels, plain.pixels)
+    np.testing.assert_array_equal(b.provenance, prov)
+    assert len(b.fg_contributions) == len(b.bg_contributions) == len(case.refs)
+
+
+def test_extensions_rejected_in_parity_build(S):
+    import ctypes as C
+
+    from paper_2007_00558_b200 import _native
+
+    case = refscene_case(golden("refscene_identity_simple.npz"))
+    cfg = _native.synth_cfg(S.SynthesisConfig())
+    cfg.inpaint = 1
+    ctx = _native.context()
+    with pytest.raises(ValueError):
+        ctx.call("fvv_render_views", C.byref(_native.camera(case.virtual)), 1,
+                 (C.c_int32 * 1)(0), None, 1, C.byref(cfg), None, None)
+
+
+# ---------------------------------------------------------------- bilateral
+
+
+@pytest.fixture(scope="module")
+def P(cuda):
+    from paper_2007_00558_b200 import depthproc
+
+    return depthproc
+
+
+def test_no_holes_is_identity(P, T):
+    frame = T.DepthFrame(6, 6, np.full((6, 6), 1.5, np.float32), np.zeros((6, 6), np.uint8))
+    guide = T.ColorFrame(6, 6, np.full((6, 6, 3), 90, np.uint8))
+    assert P.bilateral_close_holes(frame, guide) is frame
+
+
+def test_single_hole_constant_region(P, T):
+    d = np.full((7, 7), 2.5, np.float32)
+    v = np.zeros((7, 7), np.uint8)
+    v[3, 3] = 1
+    d[3, 3] = 0
+    out = P.bilateral_close_holes(T.DepthFrame(7, 7, d, v),
+                                  T.ColorFrame(7, 7, np.full((7, 7, 3), 90, np.uint8)))
+    assert out.validity[3, 3] == 0
+    assert out.depth[3, 3] == pytest.approx(2.5, abs=1e-6)
+
+
+def test_valid_pixels_never_modified(P, T):
+    rng = np.random.default_rng(4)
+    d = rng.uniform(1.0, 3.0, (10, 10)).astype(np.float32)
+    v = np.zeros((10, 10), np.uint8)
+    v[4:6, 4:6] = 1
+    d[4:6, 4:6] = 0
+    frame = T.DepthFrame(10, 10, d, v)
+    out = P.bilateral_close_holes(frame, T.ColorFrame(10, 10, rng.integers(0, 255, (10, 10, 3))
+                                                      .astype(np.uint8)))
+    np.testing.assert_array_equal(out.depth[v == 0], frame.depth[v == 0])
+
+
+def test_background_pixels_not_filled(P, T):
+    d = np.full((7, 7), 2.0, np.float32)
+    v = np.zeros((7, 7), np.uint8)
+    v[3, 3] = 2
+    d[3, 3] = 0
+    out = P.bilateral_close_holes(T.DepthFrame(7, 7, d, v),
+                                  T.ColorFrame(7, 7, np.full((7, 7, 3), 90, np.uint8)))
+    assert out.validity[3, 3] == 2
+
+
+def test_idempotent_once_stable(P, T):
+    rng = np.random.default_rng(5)
+    d = rng.uniform(1.0, 3.0, (12, 12)).astype(np.float32)
+    v = np.zeros((12, 12), np.uint8)
+    v[2:9, 5] = 1
+    v[0:4, 0:4] = 1
+    d[v != 0] = 0
+    guide = T.ColorFrame(12, 12, np.full((12, 12, 3), 90, np.uint8))
+    cur = T.DepthFrame(12, 12, d, v)
+    for _ in range(30):
+        nxt = P.bilateral_close_holes(cur, guide)
+        if np.array_equal(nxt.validity, cur.validity):
+            break
+        cur = nxt
+    stable = P.bilateral_close_holes(cur, guide)
+    np.testing.assert_array_equal(stable.depth, cur.depth)
+    np.testing.assert_array_equal(stable.validity, cur.validity)
+
+
+def test_guide_mismatch_rejected(P, T):
+    frame = T.DepthFrame(6, 6, np.full((6, 6), 1.5, np.float32), np.ones((6, 6), np.uint8))
+    with pytest.raises(ValueError):
+        P.bilateral_close_holes(frame, T.ColorFrame(4, 4, np.zeros((4, 4, 3), np.uint8)))
+
+
+def test_bilateral_matches_oracle_on_random_holes(P, T):
+    from oracle import fvv_oracle as O
+
+    rng = np.random.default_rng(9)
+    H, W = 96, 128
+    d = rng.uniform(0.5, 6.0, (H, W)).astype(np.float32)
+    v = np.zeros((H, W), np.uint8)
+    v[rng.random((H, W)) < 0.2] = 1
+    v[rng.random((H, W)) < 0.1] = 2
+    d[v != 0] = 0
+    rgb = rng.integers(0, 256, (H, W, 3)).astype(np.uint8)
+    out = P.bilateral_close_holes(T.DepthFrame(W, H, d, v), T.ColorFrame(W, H, rgb))
+    od, ov, _ = O.bilateral_close_holes(d, v, rgb)
+    np.testing.assert_array_equal(out.validity, ov)
+    diff = np.abs(out.depth.astype(np.float64) - od)
+    assert (diff <= np.spacing(np.abs(od))).all()
+
+
+# ---------------------------------------------------------------- engine
+
+
+def test_engine_synthesize_matches_drop_in(cuda):
+    from paper_2007_00558_b200 import synthesis as S
+    from paper_2007_00558_b200.engine import EdgeRenderer, synthesize
+    from paper_2007_00558_b200.types import MvdFrame
+
+    case = refscene_case(golden("refscene_mid34_medium.npz"))
+    inputs = case.inputs()
+    rig = [inputs[r].calib for r in case.refs]
+    bgs = {r: inputs[r].bg_depth for r in case.refs}
+    mvd = {r: MvdFrame(r, inputs[r].live_color, inputs[r].live_depth) for r in case.refs}
+    want = S.synthesize_view(case.virtual, inputs, case.refs, S.SynthesisConfig())
+    got = synthesize(case.virtual, mvd, case.refs, rig=rig, bg_models=bgs, hole_closing=False)
+    np.testing.assert_array_equal(got.pixels, want.pixels)
+    # refs=None -> select_references picks the same nearest three
+    eng = EdgeRenderer(rig, bgs)
+    got2 = eng.synthesize(case.virtual, mvd, hole_closing=False)
+    assert sorted(eng.plan([case.virtual])[0][0]) == sorted(case.refs)
+    assert got2.pixels.shape == want.pixels.shape
+    with pytest.raises(ValueError):
+        eng.render([case.virtual], [[999]])
