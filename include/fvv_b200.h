@@ -110,6 +110,13 @@ int64_t fvv_launch_count(const fvv_ctx *ctx); /* kernels launched by this contex
 int fvv_profile_enable(fvv_ctx *ctx, int32_t enable); /* also resets */
 int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches);
 
+/* Numerics self-test of the shared-reciprocal division and K2's filtered
+ * rint(f*x/z + c) against the correctly rounded __ddiv_rn path, on n seeded
+ * samples of operand class `mode` (0 bilinear, 1 projection, 2 mix, 3 wide
+ * log-uniform, 4 near-half projections). Adds mismatches to *mismatches_dev. */
+int fvv_selftest_division(fvv_ctx *ctx, int64_t n, uint64_t seed, int32_t mode,
+                          uint64_t *mismatches_dev);
+
 /* ---- K0: depth decode ----------------------------------------------------- */
 /* core.depth_from_millimeters (core.py:260-269): f32 = (f32)mm / 1000.0f,
  * Valid & mm==0 -> Invalid, non-Valid depth = 0. validity_in may be NULL

@@ -29,7 +29,7 @@ EXPORTS = (
     "fvv_dequantize12", "fvv_bilateral_close_holes", "fvv_synthesize_view", "fvv_warp_layer",
     "fvv_mix_layer", "fvv_composite", "fvv_slot_set_camera", "fvv_slot_set_bg",
     "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slot_ingest_yuv", "fvv_render_views",
-    "fvv_profile_enable", "fvv_profile_read",
+    "fvv_profile_enable", "fvv_profile_read", "fvv_selftest_division",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -89,6 +89,7 @@ _SIGS = {
     "fvv_slot_ingest_mm": ([_VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP], C.c_int),
     "fvv_slot_ingest_yuv": ([_VP, _I32, _VP, _VP, _VP, _VP, _D, _D, _I32, _VP, _VP], C.c_int),
     "fvv_profile_enable": ([_VP, _I32], C.c_int),
+    "fvv_selftest_division": ([_VP, C.c_int64, C.c_uint64, _I32, _VP], C.c_int),
     "fvv_profile_read": ([_VP, _I32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],

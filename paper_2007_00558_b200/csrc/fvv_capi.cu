@@ -256,7 +256,8 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
             const float *d = L == 0 ? s.fgd : s.bgd;
             wp.c[k] = WarpContrib{s.dev, d, rx, ry, ctx->canvas + per * k, b};
             rp.c[k] = ResolveContrib{s.dev, s.texel, d, rx, ry, ctx->canvas + per * k, w, b,
-                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
+                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0,
+                                     1.0f / (float)s.cam.width};
         }
         const long long np = (long long)s.cam.width * s.cam.height;
         maxpx = np > maxpx ? np : maxpx;
@@ -341,6 +342,16 @@ static int prof_drain(fvv_ctx *ctx) {
         ctx->pool.push_back(r.b);
     }
     ctx->recs.clear();
+    return FVV_OK;
+}
+
+int fvv_selftest_division(fvv_ctx *ctx, int64_t n, uint64_t seed, int32_t mode,
+                          uint64_t *mismatches_dev) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 0 || mode < 0 || mode > 4 || !mismatches_dev)
+        return fail(ctx, FVV_EINVAL, "selftest_division: bad arguments");
+    LAUNCH(launch_selftest_div(n, seed, mode, (unsigned long long *)mismatches_dev, ctx->stream));
     return FVV_OK;
 }
 
@@ -674,7 +685,7 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.dbg.contrib_stage = stage_out;
     rp.c[0] = ResolveContrib{s.dev, s.texel, s.fgd, rx, ry, ctx->canvas,
                              host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
-                             layer_fg ? 1 : 0};
+                             layer_fg ? 1 : 0, 1.0f / (float)src->width};
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
     return FVV_OK;
 }

@@ -52,7 +52,8 @@ cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s)
 // ---------------------------------------------------------------------------
 // K0 + K1 + ingest
 
-constexpr int PX = 32, PY = 8, PMAXR = 4;
+constexpr int PX = 128, PY = 8, PMAXR = 4;  // tile: 8 rows x 128 px, 4 px per thread
+constexpr int PSC = PX + 2 * PMAXR, PSR = PY + 2 * PMAXR;
 
 // 12-bit code at (iy, ix) from the folded/interleaved YUV420 raster
 // (depthcodec.py:154-177, 213-222): MSB nibble from U (even rows) or V (odd
@@ -70,128 +71,236 @@ __device__ __forceinline__ uint32_t yuv_code(const PreprocParams &p, int iy, int
     return (msb << 8) | lsb;
 }
 
-// Decoded (depth, validity) of pixel (iy, ix), per source format.
+// core.depth_from_millimeters (core.py:260-269): fp32 TRUE division by 1000
+__device__ __forceinline__ void decode_mm(uint32_t mm, uint8_t &val, float &z) {
+    if (val == FVV_VALID && mm == 0) val = FVV_INVALID;
+    z = (val == FVV_VALID) ? __fdiv_rn((float)mm, 1000.0f) : 0.0f;
+}
+
+// depthcodec.dequantize12 / dequantize_codes (depthcodec.py:113-138)
+__device__ __forceinline__ void decode_code(const PreprocParams &p, uint32_t c, uint8_t &val,
+                                            float &z) {
+    if (c < 2) {
+        val = (c == 0) ? (uint8_t)FVV_BACKGROUND : (uint8_t)FVV_INVALID;
+        z = 0.0f;
+    } else {
+        val = FVV_VALID;
+        const double frac = ddiv((double)c - 2.0, 4093.0);
+        z = __double2float_rn(ddiv(1.0, dadd(dmul(frac, p.inv_span), p.inv_zf)));
+    }
+}
+
+// Decoded (depth, validity) of one pixel, per source format.
 __device__ __forceinline__ void load_depth(const PreprocParams &p, int iy, int ix, float &z,
                                            uint8_t &val, uint32_t *code) {
     const size_t i = (size_t)iy * p.W + ix;
     if (p.src == kSrcMM) {
-        // core.depth_from_millimeters (core.py:260-269): fp32 TRUE division
-        const uint16_t mm = p.mm[i];
         val = p.validity ? p.validity[i] : (uint8_t)FVV_VALID;
-        if (val == FVV_VALID && mm == 0) val = FVV_INVALID;
-        z = (val == FVV_VALID) ? __fdiv_rn((float)mm, 1000.0f) : 0.0f;
+        decode_mm(p.mm[i], val, z);
     } else if (p.src == kSrcYUV || p.src == kSrcCodes) {
-        // depthcodec.dequantize12 / dequantize_codes (depthcodec.py:113-138)
         const uint32_t c = p.src == kSrcYUV ? yuv_code(p, iy, ix) : (uint32_t)p.codes[i];
         if (code) *code = c;
-        if (c < 2) {
-            val = (c == 0) ? (uint8_t)FVV_BACKGROUND : (uint8_t)FVV_INVALID;
-            z = 0.0f;
-        } else {
-            val = FVV_VALID;
-            const double frac = ddiv((double)c - 2.0, 4093.0);
-            z = __double2float_rn(ddiv(1.0, dadd(dmul(frac, p.inv_span), p.inv_zf)));
-        }
+        decode_code(p, c, val, z);
     } else {
         z = p.depth[i];
         val = p.validity[i];
     }
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(const __grid_constant__ PreprocParams p) {
-    __shared__ float sz[(PY + 2 * PMAXR) * (PX + 2 * PMAXR)];
-    __shared__ uint8_t sv[(PY + 2 * PMAXR) * (PX + 2 * PMAXR)];
-    __shared__ uchar4 sg[(PY + 2 * PMAXR) * (PX + 2 * PMAXR)];
-    __shared__ int s_holes;
+__device__ __forceinline__ uchar4 load_rgb(const PreprocParams &p, size_t i) {
+    if (!p.rgb) return make_uchar4(0, 0, 0, 0);
+    const uint8_t *c = p.rgb + i * 3;
+    return make_uchar4(c[0], c[1], c[2], 0);
+}
 
-    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+// K0 + K1 + ingest. Each thread owns 4 consecutive pixels of one row; a warp
+// owns a 128-px row segment (coalesced 8/4/12-byte loads, 16-byte stores).
+// The 5x5 joint-bilateral fill (depthproc.py:171-224) only runs when the
+// tile holds an Invalid pixel: then the 2-px halo is staged in shared memory
+// (zero-padded like scenegen._shift2d: outside pixels are never Valid).
+__global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ PreprocParams p) {
+    __shared__ float sz[PSR * PSC];
+    __shared__ uint8_t sv[PSR * PSC];
+    __shared__ uchar4 sg[PSR * PSC];
+    __shared__ float s_fill[PY * PX];
+    __shared__ uint16_t s_queue[PY * PX];
+    __shared__ int s_holes, s_nq;
+
+    const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
+    const int iy = y0 + ty, xb = x0 + lane * 4;
     const int R = p.radius;
-    const int SC = PX + 2 * R, SR = PY + 2 * R;
-    if (tid == 0) s_holes = 0;
+    const int SC = PX + 2 * R;
+    if (tid == 0) { s_holes = 0; s_nq = 0; }
 
-    if (R > 0) {
-        for (int i = tid; i < SR * SC; i += 256) {
-            const int qy = y0 - R + i / SC, qx = x0 - R + i % SC;
-            float z = 0.0f;
-            uint8_t val = 0xFF;  // outside the image: never a valid neighbour
-            uchar4 g = make_uchar4(0, 0, 0, 0);
-            if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) {
-                load_depth(p, qy, qx, z, val, nullptr);
-                const uint8_t *c = p.rgb + ((size_t)qy * p.W + qx) * 3;
-                g = make_uchar4(c[0], c[1], c[2], 0);
+    float z[4];
+    uint8_t val[4];
+    uchar4 g[4];
+    uint32_t code[4] = {0, 0, 0, 0};
+    const bool row_ok = iy < p.H;
+    const size_t rowbase = (size_t)iy * p.W;
+    const bool vec = row_ok && xb + 3 < p.W && (p.W & 3) == 0 && p.src == kSrcMM && p.rgb &&
+                     p.validity;
+    if (vec) {
+        // 16-B aligned vector path (W % 4 == 0; torch/cudaMalloc bases are 256-B aligned)
+        const size_t i0 = rowbase + xb;
+        const uint2 m = __ldcs(reinterpret_cast<const uint2 *>(p.mm + i0));
+        const uint32_t v4 = __ldcs(reinterpret_cast<const uint32_t *>(p.validity + i0));
+        const uint32_t *c3 = reinterpret_cast<const uint32_t *>(p.rgb + i0 * 3);
+        const uint32_t ca = __ldcs(c3), cb = __ldcs(c3 + 1), cc = __ldcs(c3 + 2);
+        const uint32_t mm4[4] = {m.x & 0xFFFFu, m.x >> 16, m.y & 0xFFFFu, m.y >> 16};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            val[q] = (uint8_t)(v4 >> (8 * q));
+            decode_mm(mm4[q], val[q], z[q]);
+        }
+        g[0] = make_uchar4(ca & 255, (ca >> 8) & 255, (ca >> 16) & 255, 0);
+        g[1] = make_uchar4(ca >> 24, cb & 255, (cb >> 8) & 255, 0);
+        g[2] = make_uchar4((cb >> 16) & 255, cb >> 24, cc & 255, 0);
+        g[3] = make_uchar4((cc >> 8) & 255, (cc >> 16) & 255, cc >> 24, 0);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            z[q] = 0.0f;
+            val[q] = 0xFF;
+            g[q] = make_uchar4(0, 0, 0, 0);
+            if (row_ok && xb + q < p.W) {
+                load_depth(p, iy, xb + q, z[q], val[q], &code[q]);
+                g[q] = load_rgb(p, rowbase + xb + q);
             }
-            sz[i] = z;
-            sv[i] = val;
-            sg[i] = g;
+        }
+    }
+    int nh = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nh += (val[q] == FVV_INVALID);
+
+    if (R > 0 && __syncthreads_or(nh)) {
+        // interior from registers, halo ring from global memory
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int si = (ty + R) * SC + lane * 4 + q + R;
+            sz[si] = z[q];
+            sv[si] = val[q];
+            sg[si] = g[q];
+        }
+        const int SR = PY + 2 * R;
+        const int ring = SR * SC - PY * PX;
+        for (int i = tid; i < ring; i += 256) {
+            int ry, rx;
+            const int top = R * SC;
+            if (i < top) { ry = i / SC; rx = i - ry * SC; }
+            else if (i < 2 * top) { ry = PY + R + (i - top) / SC; rx = (i - top) % SC; }
+            else { const int j = i - 2 * top; ry = R + j / (2 * R); rx = j % (2 * R);
+                   if (rx >= R) rx += PX; }
+            const int qy = y0 - R + ry, qx = x0 - R + rx;
+            float zz = 0.0f;
+            uint8_t vv = 0xFF;
+            uchar4 gg = make_uchar4(0, 0, 0, 0);
+            if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) {
+                load_depth(p, qy, qx, zz, vv, nullptr);
+                gg = load_rgb(p, (size_t)qy * p.W + qx);
+            }
+            const int si = ry * SC + rx;
+            sz[si] = zz;
+            sv[si] = vv;
+            sg[si] = gg;
         }
         __syncthreads();
-    }
-
-    const int ix = x0 + tx, iy = y0 + ty;
-    int hole = 0;
-    if (ix < p.W && iy < p.H) {
-        const size_t i = (size_t)iy * p.W + ix;
-        float z;
-        uint8_t val;
-        uint32_t code = 0;
-        uchar4 g;
-        if (R > 0) {
-            const int si = (ty + R) * SC + tx + R;
-            z = sz[si];
-            val = sv[si];
-            g = sg[si];
-            if (p.src == kSrcYUV && p.codes_out) code = yuv_code(p, iy, ix);
-        } else {
-            load_depth(p, iy, ix, z, val, &code);
-            const uint8_t *c = p.rgb ? p.rgb + i * 3 : nullptr;
-            g = c ? make_uchar4(c[0], c[1], c[2], 0) : make_uchar4(0, 0, 0, 0);
-        }
-        if (val == FVV_INVALID) {
-            hole = 1;
-            if (R > 0) {
-                // depthproc.bilateral_close_holes (depthproc.py:196-222): 24 taps
-                // in dy-major order; w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2))
-                const double g0 = g.x, g1 = g.y, g2 = g.z;
-                double num = 0.0, den = 0.0;
-                int cnt = 0;
-                for (int dy = -R; dy <= R; ++dy) {
-                    for (int dx = -R; dx <= R; ++dx) {
-                        if (dy == 0 && dx == 0) continue;
-                        const int ni = (ty + R + dy) * SC + tx + R + dx;
-                        if (sv[ni] != FVV_VALID) continue;
-                        const uchar4 n = sg[ni];
-                        const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
-                                     e2 = dsub(g2, (double)n.z);
-                        const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-                        const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
-                        num = dadd(num, dmul(w, (double)sz[ni]));
-                        den = dadd(den, w);
-                        ++cnt;
-                    }
-                }
-                if (cnt >= p.min_valid && den > 0.0) {
-                    z = __double2float_rn(ddiv(num, den));
-                    val = FVV_VALID;
-                }
+        // Invalid pixels with >= min_valid Valid neighbours go to a work queue,
+        // drained by all 256 threads (dense instead of divergent per-lane loops)
+        unsigned qmask = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (val[q] != FVV_INVALID) continue;
+            const int c0 = (ty + R) * SC + lane * 4 + q + R;
+            int cnt = 0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx)
+                    cnt += (dy || dx) && sv[c0 + dy * SC + dx] == FVV_VALID;
+            if (cnt >= p.min_valid) {
+                s_queue[atomicAdd(&s_nq, 1)] = (uint16_t)(ty * PX + lane * 4 + q);
+                qmask |= 1u << q;
             }
         }
-        if (p.texel) {
-            uint32_t flags;
-            if (p.color_valid) flags = p.color_valid[i] ? kFlagLiveValid : 0u;
-            else flags = (val == FVV_VALID ? kFlagLiveValid : 0u) |
-                         (val == FVV_BACKGROUND ? kFlagLiveBackground : 0u);
-            p.texel[i] = (uint32_t)g.x | ((uint32_t)g.y << 8) | ((uint32_t)g.z << 16) | (flags << 24);
+        __syncthreads();
+        const int nq = s_nq;
+        for (int e = tid; e < nq; e += 256) {
+            const int lp = s_queue[e];
+            const int c0 = (lp / PX + R) * SC + (lp % PX) + R;
+            // depthproc.py:196-222: taps in dy-major order, centre skipped;
+            // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps
+            const uchar4 gc = sg[c0];
+            const double g0 = gc.x, g1 = gc.y, g2 = gc.z;
+            double num = 0.0, den = 0.0;
+            for (int dy = -R; dy <= R; ++dy) {
+                for (int dx = -R; dx <= R; ++dx) {
+                    if (dy == 0 && dx == 0) continue;
+                    const int ni = c0 + dy * SC + dx;
+                    if (sv[ni] != FVV_VALID) continue;
+                    const uchar4 n = sg[ni];
+                    const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
+                                 e2 = dsub(g2, (double)n.z);
+                    const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
+                    const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
+                    num = dadd(num, dmul(w, (double)sz[ni]));
+                    den = dadd(den, w);
+                }
+            }
+            s_fill[lp] = den > 0.0 ? __double2float_rn(ddiv(num, den)) : -1.0f;
         }
-        if (p.warp_depth) p.warp_depth[i] = (val == FVV_VALID) ? z : 0.0f;
-        if (p.depth_out) p.depth_out[i] = z;
-        if (p.validity_out) p.validity_out[i] = val;
-        if (p.codes_out) p.codes_out[i] = (uint16_t)code;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // a fill is a positive depth; -1 marks den == 0 (no fill)
+            const int lp = ty * PX + lane * 4 + q;
+            if (((qmask >> q) & 1u) && s_fill[lp] >= 0.0f) {
+                z[q] = s_fill[lp];
+                val[q] = FVV_VALID;
+            }
+        }
+    }
+
+    if (row_ok) {
+        uint32_t tex[4];
+        float wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t flags;
+            if (p.color_valid) {
+                flags = (xb + q < p.W && p.color_valid[rowbase + xb + q]) ? kFlagLiveValid : 0u;
+            } else {
+                flags = (val[q] == FVV_VALID ? kFlagLiveValid : 0u) |
+                        (val[q] == FVV_BACKGROUND ? kFlagLiveBackground : 0u);
+            }
+            tex[q] = (uint32_t)g[q].x | ((uint32_t)g[q].y << 8) | ((uint32_t)g[q].z << 16) |
+                     (flags << 24);
+            wd[q] = (val[q] == FVV_VALID) ? z[q] : 0.0f;
+        }
+        if (vec) {
+            const size_t i0 = rowbase + xb;
+            if (p.texel) *reinterpret_cast<uint4 *>(p.texel + i0) = make_uint4(tex[0], tex[1], tex[2], tex[3]);
+            if (p.warp_depth) *reinterpret_cast<float4 *>(p.warp_depth + i0) = make_float4(wd[0], wd[1], wd[2], wd[3]);
+            if (p.depth_out) *reinterpret_cast<float4 *>(p.depth_out + i0) = make_float4(z[0], z[1], z[2], z[3]);
+            if (p.validity_out)
+                *reinterpret_cast<uint32_t *>(p.validity_out + i0) =
+                    (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
+                    ((uint32_t)val[3] << 24);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (xb + q >= p.W) break;
+                const size_t i = rowbase + xb + q;
+                if (p.texel) p.texel[i] = tex[q];
+                if (p.warp_depth) p.warp_depth[i] = wd[q];
+                if (p.depth_out) p.depth_out[i] = z[q];
+                if (p.validity_out) p.validity_out[i] = val[q];
+                if (p.codes_out) p.codes_out[i] = (uint16_t)code[q];
+            }
+        }
     }
     if (p.n_holes) {
-        const unsigned m = __ballot_sync(0xffffffffu, hole);
-        __syncthreads();
-        if ((tid & 31) == 0 && m) atomicAdd(&s_holes, __popc(m));
+        const int m = __reduce_add_sync(0xffffffffu, nh);
+        if (lane == 0 && m) atomicAdd(&s_holes, m);
         __syncthreads();
         if (tid == 0 && s_holes) atomicAdd(p.n_holes, s_holes);
     }
@@ -211,37 +320,76 @@ cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
 // key into the canvas padded by r. The 9-way splat of the reference becomes
 // the ring min in K3 (verified equivalent).
 
-__global__ void __launch_bounds__(256) k_forward_warp(const __grid_constant__ WarpParams p) {
-    const WarpContrib &c = p.c[blockIdx.y];
-    const int Ws = c.src.W;
-    const long long N = (long long)Ws * c.src.H;
+// rint((f*x)/z + c) — the target pixel of np.round(uv) (synthesis.py:193-194).
+// The quotient is first formed with a Newton-refined reciprocal (relative
+// error ~1e-15); only when the result lies within 1e-6 of a rounding boundary
+// (k + 0.5) is the correctly rounded __ddiv_rn path taken, so the rounded
+// target is always the one the exact float64 expression gives.
+__device__ __forceinline__ double proj_rint(double f, double x, double z, double c) {
+    const double num = dmul(f, x);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
+    double e = fma(-z, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-z, r, 1.0);
+    r = fma(r, e, r);
+    const double ua = fma(num, r, c);
+    const double fl = floor(ua);
+    const double fr = ua - fl;
+    if (fabs(fr - 0.5) > 1e-6 && fabs(ua) < 1e8 && z > 1e-200) return fr > 0.5 ? fl + 1.0 : fl;
+    return rint(dadd(ddiv(num, z), c));
+}
+
+constexpr int K2_THREADS = 128, K2_PX = 4;
+
+__global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_constant__ WarpParams p) {
+    const WarpContrib &c = p.c[blockIdx.z];
+    const int Ws = c.src.W, Hs = c.src.H;
+    const int sv = blockIdx.y;
+    const int u0 = (blockIdx.x * K2_THREADS + threadIdx.x) * K2_PX;
+    if (sv >= Hs || u0 >= Ws) return;
+    const size_t row = (size_t)sv * Ws;
+    float d[K2_PX];
+    if ((Ws & 3) == 0) {
+        const float4 v = __ldcs(reinterpret_cast<const float4 *>(c.depth + row + u0));
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    } else {
+#pragma unroll
+        for (int q = 0; q < K2_PX; ++q) d[q] = (u0 + q < Ws) ? c.depth[row + u0 + q] : 0.0f;
+    }
     const int r = p.r;
     const int Wd = p.dst.W, Hd = p.dst.H, Wc = Wd + 2 * r;
-    const double ulo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float d = __ldcs(c.depth + i);
-        if (!(d > 0.0f)) continue;
-        const int sv = (int)(i / Ws), su = (int)(i - (long long)sv * Ws);
-        const double dd = (double)d;
+    const double lo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
+    const double ry = __ldg(c.ry + sv);
+#pragma unroll
+    for (int q = 0; q < K2_PX; ++q) {
+        if (!(d[q] > 0.0f)) continue;
+        const int su = u0 + q;
+        const double dd = (double)d[q];
         double x, y, z;
-        transfer(c.src, p.dst, dmul(__ldg(c.rx + su), dd), dmul(__ldg(c.ry + sv), dd), dd, x, y, z);
+        transfer(c.src, p.dst, dmul(__ldg(c.rx + su), dd), dmul(ry, dd), dd, x, y, z);
         if (!(z > 0.0)) continue;
-        const double ur = rint(proj(p.dst.fx, x, z, p.dst.cx));
-        const double vr = rint(proj(p.dst.fy, y, z, p.dst.cy));
-        if (!(ur >= ulo && ur < uhi && vr >= ulo && vr < vhi)) continue;
+        const double ur = proj_rint(p.dst.fx, x, z, p.dst.cx);
+        if (!(ur >= lo && ur < uhi)) continue;
+        const double vr = proj_rint(p.dst.fy, y, z, p.dst.cy);
+        if (!(vr >= lo && vr < vhi)) continue;
         const size_t cell = (size_t)((int)vr + r) * Wc + (size_t)((int)ur + r);
         atomicMin((unsigned long long *)(c.canvas + cell),
-                  (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)i, c.b)));
+                  (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
     }
 }
 
 cudaError_t launch_forward_warp(const WarpParams &p, long long max_src_pixels, cudaStream_t s) {
     if (p.n == 0) return cudaSuccess;
-    long long blocks = (max_src_pixels + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    dim3 grid((unsigned)blocks, (unsigned)p.n);
-    k_forward_warp<<<grid, 256, 0, s>>>(p);
+    int maxw = 0, maxh = 0;
+    for (int k = 0; k < p.n; ++k) {
+        maxw = p.c[k].src.W > maxw ? p.c[k].src.W : maxw;
+        maxh = p.c[k].src.H > maxh ? p.c[k].src.H : maxh;
+    }
+    (void)max_src_pixels;
+    const int per = K2_THREADS * K2_PX;
+    dim3 grid((maxw + per - 1) / per, maxh, p.n);
+    k_forward_warp<<<grid, K2_THREADS, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -286,7 +434,7 @@ __device__ __forceinline__ double ring_median(const double *sz, int BC, int cent
 }
 
 template <int MAXR>
-__global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ ResolveParams p) {
+__global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ ResolveParams p) {
     __shared__ uint64_t sk[KMAX];
     __shared__ double sz[BMAX];
     __shared__ int swin[BMAX];
@@ -528,20 +676,458 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ ResolveP
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3 fast path: splat_radius 1, crack window 3 (the reference defaults,
+// synthesis.py:39-40) with every tile dimension a compile-time constant.
+//
+// Per 32x8 target tile and per contribution:
+//   keys   12x36 canvas cells (tile + 2-px halo) staged by cp.async into a
+//          double buffer (next contribution's tile in flight while the
+//          current one is resolved). Keys of stale generations compare
+//          larger than any fresh key, so the ring min needs no sanitising.
+//   cells  10x34 (tile + 1-px halo): centre key or 8-ring min (splat), FG cull
+//          on < 5 centre-covered 8-neighbours, winner z recomputed in f64.
+//   pixel  crack median (8-value sorting network), backward projection and
+//          masked bilinear fetch; per-contribution result kept in smem.
+// then mix_layer x2 and composite per pixel.
+
+constexpr int FKR = TY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36
+constexpr int FBR = TY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void stage_keys(uint64_t *dst, const uint64_t *canvas, int x0, int y0,
+                                           int Wc, int Hc, int tid) {
+    // tile origin in canvas coords: image (x0-2, y0-2) + r(=1)
+    for (int i = tid; i < FKEYS; i += NT) {
+        const int ky = i / FKC, kx = i - ky * FKC;
+        const int cy = y0 - 1 + ky, cx = x0 - 1 + kx;
+        const bool ok = cy >= 0 && cy < Hc && cx >= 0 && cx < Wc;
+        cp_async8(dst + i, ok ? canvas + (size_t)cy * Wc + cx : canvas, ok ? 8 : 0);
+    }
+}
+
+// exact f64 z of a winner index (same operations as K2, so bit-identical)
+__device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &dst,
+                                           uint32_t idx) {
+    const int W = c.src.W;
+    int sv = (int)((float)idx * c.inv_w);
+    int su = (int)idx - sv * W;
+    if (su < 0) { --sv; su += W; } else if (su >= W) { ++sv; su -= W; }
+    const double d = (double)__ldg(c.depth + idx);
+    return transfer_z(c.src, dst, dmul(__ldg(c.rx + su), d), dmul(__ldg(c.ry + sv), d), d);
+}
+
+__device__ __forceinline__ void cswap(double &a, double &b) {
+    const double lo = fmin(a, b), hi = fmax(a, b);
+    a = lo;
+    b = hi;
+}
+
+// Phase "cells" of contribution k: splat policy + FG cull (synthesis.py:207-219)
+// for the 10x34 cells around the tile; writes f64 z (inf = uncovered).
+template <bool DBG>
+__device__ __forceinline__ int resolve_cells(const ResolveContrib &c, const DevCam &dst,
+                                             const uint64_t *K, double *szk, int *swin,
+                                             uint8_t *sst, uint64_t gen, int x0, int y0, int tid) {
+    const int Wd = dst.W, Hd = dst.H;
+    int any = 0;
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+        const int i = tid + rep * NT;
+        if (i >= FCELLS) break;
+        const int by = i / FBC, bx = i - by * FBC;
+        const int qy = y0 - 1 + by, qx = x0 - 1 + bx;
+        double zq = INFINITY;
+        int wq = -1;
+        uint8_t sq = kStageNone;
+        if (qy >= 0 && qy < Hd && qx >= 0 && qx < Wd) {
+            const int kc = (by + 1) * FKC + bx + 1;
+            uint64_t w = K[kc];
+            if ((w >> kGenShift) == gen) {
+                sq = kStageCenter;
+            } else {
+                const uint64_t n0 = K[kc - FKC - 1], n1 = K[kc - FKC], n2 = K[kc - FKC + 1];
+                const uint64_t n3 = K[kc - 1], n4 = K[kc + 1];
+                const uint64_t n5 = K[kc + FKC - 1], n6 = K[kc + FKC], n7 = K[kc + FKC + 1];
+                // stale generations compare larger than any fresh key
+                uint64_t m = n0 < n1 ? n0 : n1;
+                m = m < n2 ? m : n2;
+                m = m < n3 ? m : n3;
+                m = m < n4 ? m : n4;
+                m = m < n5 ? m : n5;
+                m = m < n6 ? m : n6;
+                m = m < n7 ? m : n7;
+                w = kEmpty;
+                if ((m >> kGenShift) == gen) {
+                    w = m;
+                    sq = kStageSplat;
+                    if (c.layer_fg) {
+                        // _neighbor_count (synthesis.py:79-87): in-image centre hits
+                        const bool up = qy > 0, dn = qy + 1 < Hd, lf = qx > 0, rt = qx + 1 < Wd;
+                        const int cnt = (up && lf && (n0 >> kGenShift) == gen) +
+                                        (up && (n1 >> kGenShift) == gen) +
+                                        (up && rt && (n2 >> kGenShift) == gen) +
+                                        (lf && (n3 >> kGenShift) == gen) +
+                                        (rt && (n4 >> kGenShift) == gen) +
+                                        (dn && lf && (n5 >> kGenShift) == gen) +
+                                        (dn && (n6 >> kGenShift) == gen) +
+                                        (dn && rt && (n7 >> kGenShift) == gen);
+                        if (cnt < 5) { w = kEmpty; sq = kStageNone; }
+                    }
+                }
+            }
+            if (w != kEmpty) {
+                const uint32_t idx = (uint32_t)(w & ((1ull << c.b) - 1));
+                zq = winner_z(c, dst, idx);
+                wq = (int)idx;
+                any = 1;
+            }
+        }
+        szk[i] = zq;
+        if (DBG) { swin[i] = wq; sst[i] = sq; }
+    }
+    return any;
+}
+
+template <int MAXR, bool DBG>
+__global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ ResolveParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [2][FKEYS]
+    double *sz = reinterpret_cast<double *>(sk + 2 * FKEYS);     // [2][FCELLS]
+    double *sres = sz + 2 * FCELLS;                              // [MAXR][4][NT]
+    int *swin = reinterpret_cast<int *>(sres + MAXR * 4 * NT);   // [2][FCELLS] (DBG)
+    uint8_t *sst = reinterpret_cast<uint8_t *>(swin + 2 * FCELLS);  // [2][FCELLS] (DBG)
+
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const DevCam &dst = p.dst;
+    const int Wd = dst.W, Hd = dst.H;
+    const int ix = x0 + tx, iy = y0 + ty;
+    const bool inimg = ix < Wd && iy < Hd;
+    const size_t pix = (size_t)iy * Wd + ix;
+    const int Wc = Wd + 2, Hc = Hd + 2;
+    const size_t plane = (size_t)Wd * Hd;
+    const uint64_t gen = p.gen;
+    const int ntot = p.n_fg + p.n_bg;
+    // virtual-camera ray of this pixel (pixel_rays, core.py:224-227)
+    const double rxd = ddiv(dsub((double)ix, dst.cx), dst.fx);
+    const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
+
+    // prologue: keys of contributions 0 (and 1) in flight, cells of 0 resolved
+    stage_keys(sk, p.c[0].canvas, x0, y0, Wc, Hc, tid);
+    cp_async_commit();
+    if (ntot > 1) {
+        stage_keys(sk + FKEYS, p.c[1].canvas, x0, y0, Wc, Hc, tid);
+        cp_async_commit();
+        cp_async_wait<1>();
+    } else {
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    int any_next = resolve_cells<DBG>(p.c[0], dst, sk, sz, swin, sst, gen, x0, y0, tid);
+
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    bool fv = false, bv = false;
+    uint32_t vmask = 0;
+#pragma unroll 1
+    for (int k = 0; k < ntot; ++k) {
+        const bool fgl = k < p.n_fg;
+        const int j = fgl ? k : k - p.n_fg;
+        // keys of k+1 must have landed; cells of k must be complete
+        cp_async_wait<0>();
+        const int any = __syncthreads_or(any_next);
+        // keys of k+2 into the buffer cells(k) just finished reading
+        if (k + 2 < ntot) {
+            stage_keys(sk + (k & 1) * FKEYS, p.c[k + 2].canvas, x0, y0, Wc, Hc, tid);
+            cp_async_commit();
+        }
+        // cells of k+1 (overlaps with the per-pixel work of k below)
+        any_next = 0;
+        if (k + 1 < ntot)
+            any_next = resolve_cells<DBG>(p.c[k + 1], dst, sk + ((k + 1) & 1) * FKEYS,
+                                          sz + ((k + 1) & 1) * FCELLS, swin + ((k + 1) & 1) * FCELLS,
+                                          sst + ((k + 1) & 1) * FCELLS, gen, x0, y0, tid);
+        const ResolveContrib &c = p.c[k];
+        const double *szk = sz + (k & 1) * FCELLS;
+        double z = INFINITY;
+        int win = -1;
+        uint8_t st = kStageNone;
+        bool ok = false;
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+        if (any && inimg) {
+            const int bi = (ty + 1) * FBC + tx + 1;
+            z = szk[bi];
+            if (DBG) { win = swin[(k & 1) * FCELLS + bi]; st = sst[(k & 1) * FCELLS + bi]; }
+            if (!(z < INFINITY)) {
+                // crack median (synthesis.py:90-125): >= 5 of 8 finite neighbours
+                double v0 = szk[bi - FBC - 1], v1 = szk[bi - FBC], v2 = szk[bi - FBC + 1],
+                       v3 = szk[bi - 1], v4 = szk[bi + 1], v5 = szk[bi + FBC - 1],
+                       v6 = szk[bi + FBC], v7 = szk[bi + FBC + 1];
+                const int cnt = (v0 < INFINITY) + (v1 < INFINITY) + (v2 < INFINITY) +
+                                (v3 < INFINITY) + (v4 < INFINITY) + (v5 < INFINITY) +
+                                (v6 < INFINITY) + (v7 < INFINITY);
+                if (cnt >= 5) {
+                    // Batcher odd-even merge sort of 8 (inf sorts last)
+                    cswap(v0, v1); cswap(v2, v3); cswap(v4, v5); cswap(v6, v7);
+                    cswap(v0, v2); cswap(v1, v3); cswap(v4, v6); cswap(v5, v7);
+                    cswap(v1, v2); cswap(v5, v6);
+                    cswap(v0, v4); cswap(v1, v5); cswap(v2, v6); cswap(v3, v7);
+                    cswap(v2, v4); cswap(v3, v5);
+                    cswap(v1, v2); cswap(v3, v4); cswap(v5, v6);
+                    // cnt in 5..8: lower middle v2 (5,6) or v3 (7,8); upper v3 (6) / v4 (8)
+                    const double lo = cnt <= 6 ? v2 : v3;
+                    if (cnt & 1) z = lo;
+                    else z = ddiv(dadd(lo, cnt == 6 ? v3 : v4), 2.0);
+                    st = kStageCrack;
+                    win = -1;
+                }
+            }
+            // backward colour fetch (synthesis.py:224-247, _bilinear_fetch :128-159)
+            if (z < INFINITY) {
+                double xs, ys, zs;
+                transfer(dst, c.src, dmul(rxd, z), dmul(ryd, z), z, xs, ys, zs);
+                if (zs > 0.0) {
+                    const int Ws = c.src.W, Hs = c.src.H;
+                    double us, vs;
+                    if (zs > 1e-100) {
+                        const double rz = rcp_nr(zs);
+                        us = dadd(div_rcp(dmul(c.src.fx, xs), zs, rz), c.src.cx);
+                        vs = dadd(div_rcp(dmul(c.src.fy, ys), zs, rz), c.src.cy);
+                    } else {
+                        us = proj(c.src.fx, xs, zs, c.src.cx);
+                        vs = proj(c.src.fy, ys, zs, c.src.cy);
+                    }
+                    if (us >= -0.5 && us <= (double)Ws - 0.5 && vs >= -0.5 &&
+                        vs <= (double)Hs - 0.5) {
+                        const double uc = fmin(fmax(us, 0.0), (double)(Ws - 1));
+                        const double vc = fmin(fmax(vs, 0.0), (double)(Hs - 1));
+                        const double u0 = floor(uc), v0 = floor(vc);
+                        const int iu = (int)u0, iv = (int)v0;
+                        const double fu = dsub(uc, u0), fv_ = dsub(vc, v0);
+                        const double omu = dsub(1.0, fu), omv = dsub(1.0, fv_);
+                        const bool inu = iu + 1 < Ws, inv = iv + 1 < Hs;
+                        const uint32_t *row0 = c.texel + (size_t)iv * Ws + iu;
+                        const uint32_t fl = c.flag << 24;
+                        const uint32_t t0 = __ldg(row0);
+                        const uint32_t t1 = inu ? __ldg(row0 + 1) : 0u;
+                        const uint32_t t2 = inv ? __ldg(row0 + Ws) : 0u;
+                        const uint32_t t3 = (inu && inv) ? __ldg(row0 + Ws + 1) : 0u;
+                        double s = 0.0;
+#define FVV_TAP(T, WT)                                                          \
+    if ((T) & fl) {                                                             \
+        const double w_ = (WT);                                                 \
+        c0 = dadd(c0, dmul(w_, (double)((T) & 0xFFu)));                         \
+        c1 = dadd(c1, dmul(w_, (double)(((T) >> 8) & 0xFFu)));                  \
+        c2 = dadd(c2, dmul(w_, (double)(((T) >> 16) & 0xFFu)));                 \
+        s = dadd(s, w_);                                                        \
+    }
+                        FVV_TAP(t0, dmul(omu, omv))
+                        FVV_TAP(t1, dmul(fu, omv))
+                        FVV_TAP(t2, dmul(omu, fv_))
+                        FVV_TAP(t3, dmul(fu, fv_))
+#undef FVV_TAP
+                        if (s > 1e-12) {
+                            ok = true;
+                            const double rs = rcp_nr(s);
+                            c0 = div_rcp(c0, s, rs);
+                            c1 = div_rcp(c1, s, rs);
+                            c2 = div_rcp(c2, s, rs);
+                        }
+                    }
+                }
+            }
+        }
+        if (!ok) { c0 = c1 = c2 = 0.0; }
+        const double zd = ok ? z : 0.0;
+        sres[(j * 4 + 0) * NT + tid] = c0;
+        sres[(j * 4 + 1) * NT + tid] = c1;
+        sres[(j * 4 + 2) * NT + tid] = c2;
+        sres[(j * 4 + 3) * NT + tid] = zd;
+        if (ok) vmask |= 1u << j;
+        if (DBG && inimg) {
+            const size_t o = (size_t)k * plane + pix;
+            if (p.dbg.contrib_color) {
+                p.dbg.contrib_color[o * 3 + 0] = c0;
+                p.dbg.contrib_color[o * 3 + 1] = c1;
+                p.dbg.contrib_color[o * 3 + 2] = c2;
+            }
+            if (p.dbg.contrib_depth) p.dbg.contrib_depth[o] = zd;
+            if (p.dbg.contrib_valid) p.dbg.contrib_valid[o] = ok ? 1 : 0;
+            if (p.dbg.contrib_winner) p.dbg.contrib_winner[o] = win;
+            if (p.dbg.contrib_stage) p.dbg.contrib_stage[o] = st;
+        }
+        // -- end of a layer: mix_layer (synthesis.py:261-292)
+        const bool last = fgl ? (k == p.n_fg - 1) : (k == ntot - 1);
+        if (last) {
+            const int n = j + 1;
+            const int kb = k - j;
+            double zmin = INFINITY;
+            for (int q = 0; q < n; ++q) {
+                const double zj = sres[(q * 4 + 3) * NT + tid];
+                if (((vmask >> q) & 1u) && zj < zmin) zmin = zj;
+            }
+            const double thr = dadd(zmin, dmul(p.band_rel, zmin));
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
+            for (int q = 0; q < n; ++q) {
+                const double zj = sres[(q * 4 + 3) * NT + tid];
+                if (((vmask >> q) & 1u) && zj <= thr) {
+                    const double w = p.c[kb + q].weight;
+                    a0 = dadd(a0, dmul(w, sres[(q * 4 + 0) * NT + tid]));
+                    a1 = dadd(a1, dmul(w, sres[(q * 4 + 1) * NT + tid]));
+                    a2 = dadd(a2, dmul(w, sres[(q * 4 + 2) * NT + tid]));
+                    if (DBG) ad = dadd(ad, dmul(w, zj));
+                    aw = dadd(aw, w);
+                }
+            }
+            const bool mv = aw > 0.0;
+            double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+            if (mv) {
+                const double ra = rcp_nr(aw);
+                m0 = div_rcp(a0, aw, ra);
+                m1 = div_rcp(a1, aw, ra);
+                m2 = div_rcp(a2, aw, ra);
+            }
+            if (fgl) { f0 = m0; f1 = m1; f2 = m2; fv = mv; }
+            else { b0 = m0; b1 = m1; b2 = m2; bv = mv; }
+            vmask = 0;
+            if (DBG && inimg) {
+                const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
+                if (p.dbg.merged_color) {
+                    p.dbg.merged_color[o * 3 + 0] = m0;
+                    p.dbg.merged_color[o * 3 + 1] = m1;
+                    p.dbg.merged_color[o * 3 + 2] = m2;
+                }
+                if (p.dbg.merged_depth) p.dbg.merged_depth[o] = mv ? ddiv(ad, aw) : 0.0;
+                if (p.dbg.merged_valid) p.dbg.merged_valid[o] = mv ? 1 : 0;
+            }
+        }
+    }
+    // -- composite (synthesis.py:295-318): hole, then BG, then FG; rint, clip
+    if (inimg) {
+        double o0, o1, o2;
+        if (fv) { o0 = f0; o1 = f1; o2 = f2; }
+        else if (bv) { o0 = b0; o1 = b1; o2 = b2; }
+        else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
+        if (p.rgb_out) {
+            uint8_t *o = p.rgb_out + pix * 3;
+            o[0] = (uint8_t)fmin(fmax(rint(o0), 0.0), 255.0);
+            o[1] = (uint8_t)fmin(fmax(rint(o1), 0.0), 255.0);
+            o[2] = (uint8_t)fmin(fmax(rint(o2), 0.0), 255.0);
+        }
+        if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
+    }
+}
+
+template <int MAXR>
+static size_t fast_smem() {
+    return 2 * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(double) +
+           (size_t)MAXR * 4 * NT * sizeof(double) + 2 * FCELLS * sizeof(int) + 2 * FCELLS;
+}
+
+template <typename K>
+static void raise_smem(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     dim3 grid((p.dst.W + TX - 1) / TX, (p.dst.H + TY - 1) / TY);
     const int maxn = p.n_fg > p.n_bg ? p.n_fg : p.n_bg;
+    const bool dbg = p.dbg.contrib_color || p.dbg.contrib_depth || p.dbg.contrib_valid ||
+                     p.dbg.contrib_winner || p.dbg.contrib_stage || p.dbg.merged_color ||
+                     p.dbg.merged_depth || p.dbg.merged_valid;
+    if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0) {
+        static bool init = false;
+        if (!init) {
+            raise_smem(k_resolve_fast<4, false>, fast_smem<4>());
+            raise_smem(k_resolve_fast<4, true>, fast_smem<4>());
+            raise_smem(k_resolve_fast<FVV_MAX_REFS, false>, fast_smem<FVV_MAX_REFS>());
+            raise_smem(k_resolve_fast<FVV_MAX_REFS, true>, fast_smem<FVV_MAX_REFS>());
+            init = true;
+        }
+        if (maxn <= 4) {
+            if (dbg) k_resolve_fast<4, true><<<grid, NT, fast_smem<4>(), s>>>(p);
+            else k_resolve_fast<4, false><<<grid, NT, fast_smem<4>(), s>>>(p);
+        } else {
+            if (dbg) k_resolve_fast<FVV_MAX_REFS, true><<<grid, NT, fast_smem<FVV_MAX_REFS>(), s>>>(p);
+            else k_resolve_fast<FVV_MAX_REFS, false><<<grid, NT, fast_smem<FVV_MAX_REFS>(), s>>>(p);
+        }
+        return cudaGetLastError();
+    }
     if (maxn <= 4) {
-        k_resolve<4><<<grid, NT, resolve_smem_bytes(4), s>>>(p);
+        k_resolve_generic<4><<<grid, NT, resolve_smem_bytes(4), s>>>(p);
     } else {
         static bool attr_set = false;
         if (!attr_set) {
-            cudaFuncSetAttribute(k_resolve<FVV_MAX_REFS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)resolve_smem_bytes(FVV_MAX_REFS));
+            raise_smem(k_resolve_generic<FVV_MAX_REFS>, resolve_smem_bytes(FVV_MAX_REFS));
             attr_set = true;
         }
-        k_resolve<FVV_MAX_REFS><<<grid, NT, resolve_smem_bytes(FVV_MAX_REFS), s>>>(p);
+        k_resolve_generic<FVV_MAX_REFS><<<grid, NT, resolve_smem_bytes(FVV_MAX_REFS), s>>>(p);
     }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// numerics self-test: div_rcp / proj_rint against the correctly rounded path
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ double unit(uint64_t r) { return (double)(r >> 11) * 0x1.0p-53; }
+
+__global__ void k_selftest_div(long long n, uint64_t seed, int mode,
+                               unsigned long long *mism) {
+    unsigned long long bad = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint64_t r1 = splitmix(seed ^ (uint64_t)i * 2 + 1), r2 = splitmix(r1), r3 = splitmix(r2);
+        double a, b;
+        if (mode == 0) {        // bilinear normalisation: sum(w*c) / sum(w)
+            b = 1e-12 + unit(r2) * (1.0 - 1e-12);
+            a = unit(r1) * 255.0 * b;
+        } else if (mode == 1) { // projection: (f*x) / z
+            a = (unit(r1) * 2.0 - 1.0) * 1e7;
+            b = exp(log(1e-3) + unit(r2) * log(1e6));
+        } else if (mode == 2) { // mix: sum(w*c) / sum(w)
+            b = 0.01 + unit(r2) * 1600.0;
+            a = unit(r1) * 255.0 * b;
+        } else {                // wide log-uniform magnitudes, both signs
+            a = exp((unit(r1) * 2.0 - 1.0) * 69.0) * ((r3 & 1) ? -1.0 : 1.0);
+            b = exp((unit(r2) * 2.0 - 1.0) * 69.0) * ((r3 & 2) ? -1.0 : 1.0);
+        }
+        if (mode <= 3) {
+            const double q = div_rcp(a, b, rcp_nr(b));
+            const double t = __ddiv_rn(a, b);
+            bad += (__double_as_longlong(q) != __double_as_longlong(t)) && !(q == 0.0 && t == 0.0);
+        } else {                // K2's filtered rint(f*x/z + c), incl. near-half quotients
+            const double f = 500.0 + unit(r1) * 3000.0, z = 0.3 + unit(r2) * 20.0;
+            const double c = 100.0 + unit(r3) * 2000.0;
+            double u = floor(unit(splitmix(r3)) * 4000.0) - 100.0 + 0.5;  // a half-integer target
+            const double jitter = (unit(splitmix(r2 ^ 7)) - 0.5) * ((r3 & 4) ? 1e-9 : 1e-3);
+            const double x = ((u + jitter - c) * z) / f;
+            const double a1 = proj_rint(f, x, z, c);
+            const double a2 = rint(dadd(ddiv(dmul(f, x), z), c));
+            // compared as values: rint(-0.3) is -0.0 where the fast path gives
+            // +0.0; both convert to the same integer target
+            bad += !(a1 == a2);
+        }
+    }
+    if (bad) atomicAdd(mism, bad);
+}
+
+cudaError_t launch_selftest_div(long long n, uint64_t seed, int mode, unsigned long long *mism,
+                                cudaStream_t s) {
+    k_selftest_div<<<148 * 8, 256, 0, s>>>(n, seed, mode, mism);
     return cudaGetLastError();
 }
 

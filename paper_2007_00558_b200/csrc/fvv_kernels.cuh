@@ -62,6 +62,7 @@ struct ResolveContrib {
     int b;
     uint32_t flag;           // texel flag bit that marks colour-valid source pixels
     int layer_fg;
+    float inv_w;             // 1.0f / src.W (index -> (u, v) split)
 };
 
 struct ResolveParams {
@@ -97,6 +98,8 @@ cudaError_t launch_mix(const MixParams &p, cudaStream_t s);
 cudaError_t launch_composite(const double *fg_c, const uint8_t *fg_v, const double *bg_c,
                              const uint8_t *bg_v, int W, int H, const double hole[3],
                              uint8_t *rgb, uint8_t *prov, cudaStream_t s);
+cudaError_t launch_selftest_div(long long n, uint64_t seed, int mode, unsigned long long *mism,
+                                cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
 size_t resolve_smem_bytes(int maxr);
 

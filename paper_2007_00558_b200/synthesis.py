@@ -246,7 +246,8 @@ def synthesize_view_debug(virtual, inputs: Mapping[int, CameraStreamInputs],
     dbg = _native.FvvDebug(*[t.data_ptr() for t in (cc, cd, cv, cw, cs, mc, md, mv)])
     ctx.call("fvv_synthesize_view", C.byref(_native.camera(virtual)), frames, n,
              C.byref(_native.synth_cfg(cfg)), rgb.data_ptr(), prov.data_ptr(), C.byref(dbg))
-    cc, cd, cv, cw, cs, mc, md, mv = [_dev.host(t) for t in (cc, cd, cv, cw, cs, mc, md, mv)]
+    rgb, prov, cc, cd, cv, cw, cs, mc, md, mv = [
+        _dev.host(t) for t in (rgb, prov, cc, cd, cv, cw, cs, mc, md, mv)]
     contribs = []
     for k in range(2 * n):
         rid = refs[k % n]
