@@ -80,7 +80,8 @@ def build_workload(args):
     elif name in ("c2", "c4"):
         wl = scenes.make_workload(name, seed=args.seed, n_views=args.views, cameras="all")
     else:
-        wl = scenes.make_workload("c3", seed=args.seed, n_frames=max(args.frames, 1))
+        ws = int(os.environ.get("WORLD_SIZE", 1))
+        wl = scenes.make_workload("c3", seed=args.seed, n_frames=max(args.frames, ws))
     return wl
 
 
@@ -177,40 +178,56 @@ class Clocks:
 
 # ----------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
+#
+# The timed CPU path is the C restatement of the oracle (oracle/c/fvv_oracle.c,
+# bit-identical to the numpy oracle, tests/test_oracle.py): one view per host
+# thread, GIL released in the foreign calls. The numpy oracle (the reference's
+# own numpy formulation) is timed once beside it for context.
 
 _POOL_JOB = {}
 
 
-def _oracle_view(i):
+def _numpy_view(i):
     from oracle import fvv_oracle as O
 
-    job = _POOL_JOB
-    t = time.perf_counter()
-    O.es_view(job["virtual"], job["frames"])
-    return time.perf_counter() - t
+    O.es_view(_POOL_JOB["virtual"], _POOL_JOB["frames"])
+    return i
 
 
 def oracle_jobs(wl, view=0):
     caps = wl.frames[0]
     frames = [dict(calib=caps[r].calib, rgb=caps[r].rgb, mm=caps[r].mm, validity=caps[r].validity,
                    bg_depth=caps[r].bg_depth, bg_validity=caps[r].bg_validity)
-                  for r in wl.refs[view]]
+              for r in wl.refs[view]]
     return {"virtual": wl.virtuals[view], "frames": frames}
 
 
-def cpu_pool_run(wl, workers: int, rounds: int):
-    """``rounds`` rounds of one oracle view per worker; returns per-round wall s."""
+def c_oracle_rounds(wl, threads: int, rounds: int):
+    """``rounds`` rounds of one C-oracle view per host thread; wall s per round."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import c_oracle as CO
+
+    job = oracle_jobs(wl)
+    CO.lib()
+    walls = []
+    with ThreadPoolExecutor(threads) as ex:
+        for _ in range(rounds):
+            t = time.perf_counter()
+            list(ex.map(lambda _i: CO.es_view(job["virtual"], job["frames"]), range(threads)))
+            walls.append(time.perf_counter() - t)
+    return walls
+
+
+def numpy_oracle_round(wl, workers: int):
+    """One round of one numpy-oracle view per worker process (fork)."""
     import multiprocessing as mp
 
     _POOL_JOB.update(oracle_jobs(wl))
-    ctx = mp.get_context("fork")
-    walls = []
-    with ctx.Pool(workers) as pool:
-        for _ in range(rounds):
-            t = time.perf_counter()
-            pool.map(_oracle_view, range(workers))
-            walls.append(time.perf_counter() - t)
-    return walls
+    t = time.perf_counter()
+    with mp.get_context("fork").Pool(workers) as pool:
+        pool.map(_numpy_view, range(workers))
+    return time.perf_counter() - t
 
 
 def cpu_model() -> str:
@@ -228,19 +245,19 @@ def run_reference(args):
     if rank != 0:
         return 0
     wl = build_workload(args)
-    workers = args.cpu_workers or os.cpu_count()
-    walls = cpu_pool_run(wl, workers, args.warmup + args.steps)[args.warmup:]
+    threads = args.cpu_workers or os.cpu_count()
+    walls = c_oracle_rounds(wl, threads, args.warmup + args.steps)[args.warmup:]
     total = sum(walls)
-    views = workers * len(walls)
-    value = views / total
-    sample = (f"oracle port (numpy) es_view: mm decode + bilateral x{len(wl.refs[0])} + "
-              f"synthesize_view, {wl.description}; one view per worker per step")
+    value = threads * len(walls) / total
+    sample = (f"C oracle port (oracle/c/fvv_oracle.c) es_view = mm decode + bilateral x"
+              f"{len(wl.refs[0])} + synthesize_view, {wl.description}; each step = one view "
+              f"per host thread ({threads} threads)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / len(walls), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.description, "views_per_step": workers},
-            "cpu_baseline": {"value": value, "unit": "views/s", "cores": workers,
+            "config": {"workload": wl.description, "views_per_step": threads},
+            "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads,
                              "kind": "port", "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -265,30 +282,43 @@ def run_ours(args):
     # CPU baseline first (fork pool before any CUDA context exists)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        workers = args.cpu_workers or os.cpu_count()
-        walls = cpu_pool_run(wl, workers, 1)
-        cpu = {"value": workers / walls[0], "unit": "views/s", "cores": workers, "kind": "port",
-               "sample": f"{workers} views ({wl.description}, view 0) by the numpy oracle "
-                         f"es_view, one per worker process, {walls[0]:.1f} s wall",
-               "cpu": cpu_model()}
+        threads = args.cpu_workers or os.cpu_count()
+        walls = c_oracle_rounds(wl, threads, 3)
+        wall = min(walls)
+        np_wall = numpy_oracle_round(wl, threads)
+        cpu = {"value": threads / wall, "unit": "views/s", "cores": threads, "kind": "port",
+               "sample": f"{threads} views ({wl.description}, view 0), one per host thread, "
+                         f"by the C oracle port es_view (mm decode + bilateral + synthesis); "
+                         f"best of 3 rounds, {wall:.2f} s wall",
+               "cpu": cpu_model(),
+               "numpy_port": {"value": threads / np_wall, "unit": "views/s",
+                              "sample": f"{threads} views by the numpy oracle (the reference's "
+                                        f"numpy formulation), one per process, "
+                                        f"{np_wall:.1f} s wall"}}
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
     if args.config == "c3":
-        frames = wl.frames
-        views = [[i] for i in range(len(wl.virtuals))]
+        # frames sharded round-robin over ranks; view f is rendered from frame f
+        mine = D.shard(len(wl.frames), ws, rank, "cyclic")
+        frames = [wl.frames[f] for f in mine]
+        views = [[f] for f in mine]
     else:
         frames = frame_variants(wl, args.frames, args.seed + 1)
         nv = len(wl.virtuals)
         views = [D.shard(nv, ws, rank)] if args.config in ("c2", "c4") else [[0]]
     cams = sorted(frames[0])
     eng = EdgeRenderer(wl.rig)
-    for cid in cams:
-        c = frames[0][cid]
-        eng.set_bg_model(cid, c.bg_depth, c.bg_validity)
-    # pre-stage every frame's live inputs in HBM
+    bg_done = set()
+    for fr in frames:
+        for cid, c in fr.items():
+            if cid not in bg_done:
+                eng.set_bg_model(cid, c.bg_depth, c.bg_validity)
+                bg_done.add(cid)
+    # pre-stage every frame's live inputs in HBM (c2/c4 multi-GPU: only rank
+    # 0's copy is meaningful, the others receive it by broadcast each step)
     staged = []
     for fr in frames:
         staged.append({cid: (torch.from_numpy(fr[cid].rgb).to(dev),
@@ -299,10 +329,16 @@ def run_ours(args):
     vmax = max(len(v) for v in views)
     out = torch.empty((max(vmax, 1), H, W, 3), dtype=torch.uint8, device=dev)
 
+    bcast = ws > 1 and args.config in ("c2", "c4")
+
     def step(s):
         fi = s % len(staged)
         vi = views[s % len(views)] if args.config == "c3" else views[0]
         fr = staged[fi]
+        if bcast:
+            # the live MVD frame arrives at rank 0; one NCCL broadcast per
+            # tensor replicates it over NVLink (the path's only exchange)
+            D.broadcast_frame([t for cid in cams for t in fr[cid]])
         need = sorted({c for v in vi for c in wl.refs[v]})
         for cid in need:
             rgb, mm, val = fr[cid]
@@ -418,7 +454,8 @@ def run_ours(args):
         # 30 ms max synthesis time, 1080p, 3 refs
         "vs_baseline": (value / ws) / (1000.0 / 30.0) if args.config == "c1" else None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.description, "parallelism": f"replicas x{ws}" if args.config
-                   in ("c0", "c1") else f"views sharded x{ws}",
+                   in ("c0", "c1") else (f"frames sharded x{ws}" if args.config == "c3" else
+                                         f"views sharded x{ws} + NCCL frame broadcast"),
                    "views_per_step": views_per_step, "frames_rotating": len(staged),
                    "l2": f"inputs rotate over {len(staged)} pre-staged frames; per-step "
                          f"footprint (live inputs + BG models + 2R z canvases) exceeds the "

@@ -206,21 +206,14 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ P
             sg[si] = gg;
         }
         __syncthreads();
-        // Invalid pixels with >= min_valid Valid neighbours go to a work queue,
-        // drained by all 256 threads (dense instead of divergent per-lane loops)
+        // Every Invalid pixel goes to a work queue drained by all 256 threads
+        // (dense, instead of divergent per-lane loops over 4 pixels)
         unsigned qmask = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (val[q] != FVV_INVALID) continue;
-            const int c0 = (ty + R) * SC + lane * 4 + q + R;
-            int cnt = 0;
-            for (int dy = -R; dy <= R; ++dy)
-                for (int dx = -R; dx <= R; ++dx)
-                    cnt += (dy || dx) && sv[c0 + dy * SC + dx] == FVV_VALID;
-            if (cnt >= p.min_valid) {
-                s_queue[atomicAdd(&s_nq, 1)] = (uint16_t)(ty * PX + lane * 4 + q);
-                qmask |= 1u << q;
-            }
+            s_queue[atomicAdd(&s_nq, 1)] = (uint16_t)(ty * PX + lane * 4 + q);
+            qmask |= 1u << q;
         }
         __syncthreads();
         const int nq = s_nq;
@@ -228,10 +221,12 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ P
             const int lp = s_queue[e];
             const int c0 = (lp / PX + R) * SC + (lp % PX) + R;
             // depthproc.py:196-222: taps in dy-major order, centre skipped;
-            // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps
+            // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps;
+            // fill iff >= min_valid Valid taps and den > 0
             const uchar4 gc = sg[c0];
             const double g0 = gc.x, g1 = gc.y, g2 = gc.z;
             double num = 0.0, den = 0.0;
+            int cnt = 0;
             for (int dy = -R; dy <= R; ++dy) {
                 for (int dx = -R; dx <= R; ++dx) {
                     if (dy == 0 && dx == 0) continue;
@@ -244,9 +239,11 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ P
                     const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
                     num = dadd(num, dmul(w, (double)sz[ni]));
                     den = dadd(den, w);
+                    ++cnt;
                 }
             }
-            s_fill[lp] = den > 0.0 ? __double2float_rn(ddiv(num, den)) : -1.0f;
+            s_fill[lp] = (cnt >= p.min_valid && den > 0.0) ? __double2float_rn(ddiv(num, den))
+                                                           : -1.0f;
         }
         __syncthreads();
 #pragma unroll

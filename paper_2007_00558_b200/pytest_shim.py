@@ -1,0 +1,68 @@
+"""pytest plugin / import hook: route the reference's seams to the B200 backend.
+
+    PYTHONPATH=<fvv src>:<this repo> python -m pytest -p paper_2007_00558_b200.pytest_shim \
+        <fvv>/tests/test_synthesis.py <fvv>/tests/test_acceptance.py
+
+Plugins load before rootdir conftests, so ``from fvv import synthesis`` in the
+reference's conftest (tests/conftest.py:6) already receives the GPU module.
+What is rebound:
+
+* ``fvv.synthesis`` — every public name of :mod:`paper_2007_00558_b200.synthesis`
+  (synthesize_view, synthesize_view_debug, warp_layer, mix_layer, composite,
+  view_psnr, border_mask, the config/contribution types); the reference's
+  ``write_debug_bundle`` (disk I/O, out of scope) is kept;
+* ``fvv.pipeline.synthesis`` — the module global ``EdgeServer.render_tick``
+  reaches through ``synthesize_with_config`` (pipeline.py:546, 569-570);
+* ``fvv.depthproc.bilateral_close_holes`` (called at pipeline.py:518-519);
+* with ``FVV_SHIM_CODEC=1`` also ``fvv.depthcodec.unpack_yuv420`` /
+  ``dequantize12`` (pipeline.py:469-472).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import types
+
+_OVERRIDE = ("SynthesisConfig", "LayerContribution", "MergedLayer", "CameraStreamInputs",
+             "DebugBundle", "warp_layer", "mix_layer", "composite", "synthesize_view",
+             "synthesize_view_debug", "view_psnr", "border_mask", "LAYER_FG", "LAYER_BG")
+installed = {}
+
+
+def install() -> types.ModuleType:
+    """Replace the reference seams in ``sys.modules``; idempotent."""
+    if "synthesis" in installed:
+        return installed["synthesis"]
+    import fvv
+    from fvv import synthesis as ref_syn
+
+    from . import depthproc as ours_dp
+    from . import synthesis as ours
+
+    mod = types.ModuleType("fvv.synthesis", ours.__doc__)
+    mod.__dict__.update({k: v for k, v in ref_syn.__dict__.items() if not k.startswith("__")})
+    for name in _OVERRIDE:
+        setattr(mod, name, getattr(ours, name))
+    mod.__file__ = ours.__file__
+    mod.B200_BACKEND = True
+    sys.modules["fvv.synthesis"] = mod
+    fvv.synthesis = mod
+    if "fvv.pipeline" in sys.modules:
+        sys.modules["fvv.pipeline"].synthesis = mod
+    import fvv.depthproc as ref_dp
+
+    ref_dp.bilateral_close_holes = ours_dp.bilateral_close_holes
+    if os.environ.get("FVV_SHIM_CODEC") == "1":
+        import fvv.depthcodec as ref_codec
+
+        from . import depthcodec as ours_codec
+
+        ref_codec.unpack_yuv420 = ours_codec.unpack_yuv420
+        ref_codec.dequantize12 = ours_codec.dequantize12
+    installed["synthesis"] = mod
+    return mod
+
+
+def pytest_configure(config):  # pragma: no cover - exercised through pytest -p
+    install()

@@ -165,3 +165,31 @@ def test_oracle_rejects_empty_reference_list():
         O.synthesize_view(None, [])
     with pytest.raises(ValueError):
         O.mix_layer([], O.DEFAULT_CFG)
+
+
+@pytest.mark.parametrize("name", SYN + REFSCENE)
+def test_c_oracle_bit_identical_to_numpy_oracle(name):
+    from oracle import c_oracle as CO
+
+    g = golden(name)
+    case = syn_case(g) if name.startswith("syn_") else refscene_case(g)
+    a, pa = O.synthesize_view(case.virtual, case.oracle_refs())
+    b, pb = CO.synthesize_view(case.virtual, case.oracle_refs())
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(pa, pb)
+
+
+@pytest.mark.parametrize("name", ES)
+def test_c_oracle_preprocessing_matches_reference(name):
+    from oracle import c_oracle as CO
+
+    g = golden(name)
+    wl = workload(str(g["config"]), int(g["scale"]), int(g["seed"]))
+    c = wl.frames[0][int(g["cam"])]
+    d, v = CO.decode_mm(c.mm, c.validity)
+    np.testing.assert_array_equal(d, g["dec_depth"])
+    np.testing.assert_array_equal(v, g["dec_validity"])
+    fd, fv = CO.bilateral_close_holes(d, v, c.rgb)
+    np.testing.assert_array_equal(fv, g["fill_validity"])
+    diff = np.abs(fd.astype(np.float64) - g["fill_depth"].astype(np.float64))
+    assert (diff <= np.spacing(np.abs(g["fill_depth"]))).all()
