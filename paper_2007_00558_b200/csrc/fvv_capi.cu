@@ -186,9 +186,13 @@ void bilateral_params(PreprocParams &p, int radius, double sigma_s, double sigma
             p.sw[dy + radius][dx + radius] = std::exp((double)(-(dy * dy + dx * dx)) * inv_2ss);
 }
 
+int canvas_pitch(int W, int r) { return (W + 2 * r + 2) & ~1; }  // even, >= W+2r+1
+
+size_t canvas_per(int W, int H, int r) { return (size_t)canvas_pitch(W, r) * (H + 2 * r); }
+
 int ensure_canvas(fvv_ctx *ctx, int n, int W, int H, int r) {
-    const size_t per = (size_t)(W + 2 * r) * (H + 2 * r);
-    const size_t need = per * (size_t)n;
+    const size_t per = canvas_per(W, H, r);
+    const size_t need = per * (size_t)n + 2;  // +1 leading offset, +1 slack
     if (need > ctx->canvas_cap) {
         CK(cudaFree(ctx->canvas));
         ctx->canvas = nullptr;
@@ -203,7 +207,8 @@ int ensure_canvas(fvv_ctx *ctx, int n, int W, int H, int r) {
     // generation tags: keys of this view carry gen; anything else is empty.
     // One fill per 127 views instead of a clear per view.
     if (ctx->gen <= 0) {
-        LAUNCH_K(FVV_K_FILL, launch_fill_u64(ctx->canvas, per * (size_t)ctx->cn, kEmpty, ctx->stream));
+        LAUNCH_K(FVV_K_FILL, launch_fill_u64(ctx->canvas, per * (size_t)ctx->cn + 2, kEmpty,
+                                             ctx->stream));
         ctx->gen = 126;
     } else {
         ctx->gen -= 1;
@@ -223,12 +228,14 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     const int r = cfg.splat_radius;
     int rc = ensure_canvas(ctx, 2 * n, virt.width, virt.height, r);
     if (rc) return rc;
-    const size_t per = (size_t)(virt.width + 2 * r) * (virt.height + 2 * r);
+    const size_t per = canvas_per(virt.width, virt.height, r);
     const DevCam dst = to_dev(virt);
+    uint64_t *cbase = ctx->canvas + 1;
 
     WarpParams wp{};
     wp.dst = dst;
     wp.r = r;
+    wp.pitch = canvas_pitch(virt.width, r);
     wp.n = 2 * n;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
     ResolveParams rp{};
@@ -236,6 +243,7 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     rp.r = r;
     rp.window = cfg.crack_fill_window;
     rp.need = cfg.crack_fill_window * cfg.crack_fill_window / 2 + 1;
+    rp.pitch = wp.pitch;
     rp.gen = (uint64_t)ctx->gen;
     rp.n_fg = n;
     rp.n_bg = n;
@@ -254,8 +262,8 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         for (int L = 0; L < 2; ++L) {
             const int k = L * n + j;
             const float *d = L == 0 ? s.fgd : s.bgd;
-            wp.c[k] = WarpContrib{s.dev, d, rx, ry, ctx->canvas + per * k, b};
-            rp.c[k] = ResolveContrib{s.dev, s.texel, d, rx, ry, ctx->canvas + per * k, w, b,
+            wp.c[k] = WarpContrib{s.dev, d, rx, ry, cbase + per * k, b};
+            rp.c[k] = ResolveContrib{s.dev, s.texel, d, rx, ry, cbase + per * k, w, b,
                                      L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0,
                                      1.0f / (float)s.cam.width};
         }
@@ -665,15 +673,17 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     WarpParams wp{};
     wp.dst = dd;
     wp.r = r;
+    wp.pitch = canvas_pitch(dst->width, r);
     wp.n = 1;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
-    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas, b};
+    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas + 1, b};
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, (long long)src->width * src->height, ctx->stream));
     ResolveParams rp{};
     rp.dst = dd;
     rp.r = r;
     rp.window = cfg->crack_fill_window;
     rp.need = cfg->crack_fill_window * cfg->crack_fill_window / 2 + 1;
+    rp.pitch = wp.pitch;
     rp.gen = (uint64_t)ctx->gen;
     rp.n_fg = layer_fg ? 1 : 0;
     rp.n_bg = layer_fg ? 0 : 1;
@@ -683,7 +693,7 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.dbg.contrib_valid = valid_out;
     rp.dbg.contrib_winner = winner_out;
     rp.dbg.contrib_stage = stage_out;
-    rp.c[0] = ResolveContrib{s.dev, s.texel, s.fgd, rx, ry, ctx->canvas,
+    rp.c[0] = ResolveContrib{s.dev, s.texel, s.fgd, rx, ry, ctx->canvas + 1,
                              host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
                              layer_fg ? 1 : 0, 1.0f / (float)src->width};
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));

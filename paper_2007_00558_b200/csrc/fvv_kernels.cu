@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
         for (int q = 0; q < K2_PX; ++q) d[q] = (u0 + q < Ws) ? c.depth[row + u0 + q] : 0.0f;
     }
     const int r = p.r;
-    const int Wd = p.dst.W, Hd = p.dst.H, Wc = Wd + 2 * r;
+    const int Wd = p.dst.W, Hd = p.dst.H, P = p.pitch;
     const double lo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
     const double ry = __ldg(c.ry + sv);
 #pragma unroll
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
         if (!(ur >= lo && ur < uhi)) continue;
         const double vr = proj_rint(p.dst.fy, y, z, p.dst.cy);
         if (!(vr >= lo && vr < vhi)) continue;
-        const size_t cell = (size_t)((int)vr + r) * Wc + (size_t)((int)ur + r);
+        const size_t cell = (size_t)((int)vr + r) * P + (size_t)((int)ur + r);
         atomicMin((unsigned long long *)(c.canvas + cell),
                   (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
     }
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
                 const int cy = y0 - Hh + ky + r, cx = x0 - Hh + kx + r;
                 uint64_t key = kEmpty;
                 if (cy >= 0 && cy < Hc && cx >= 0 && cx < Wc) {
-                    const uint64_t v = c.canvas[(size_t)cy * Wc + cx];
+                    const uint64_t v = c.canvas[(size_t)cy * p.pitch + cx];
                     if ((v >> kGenShift) == p.gen) { key = v; any = 1; }
                 }
                 sk[i] = key;
@@ -690,23 +690,30 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 
 constexpr int FKR = TY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36
 constexpr int FBR = TY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
 
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int bytes) {
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// 12 x 36 keys (tile + 2-px halo) as 216 16-byte chunks, one per thread.
+// Tile column x0-2 is canvas column x0-1 (r = 1), which the +1 allocation
+// offset puts on an even element: every chunk is 16-byte aligned. Chunks
+// outside the canvas rows / pitch are zero-filled; they only ever feed
+// out-of-image cells, which are never resolved.
 __device__ __forceinline__ void stage_keys(uint64_t *dst, const uint64_t *canvas, int x0, int y0,
-                                           int Wc, int Hc, int tid) {
-    // tile origin in canvas coords: image (x0-2, y0-2) + r(=1)
-    for (int i = tid; i < FKEYS; i += NT) {
-        const int ky = i / FKC, kx = i - ky * FKC;
-        const int cy = y0 - 1 + ky, cx = x0 - 1 + kx;
-        const bool ok = cy >= 0 && cy < Hc && cx >= 0 && cx < Wc;
-        cp_async8(dst + i, ok ? canvas + (size_t)cy * Wc + cx : canvas, ok ? 8 : 0);
+                                           int P, int Hc, int tid) {
+    if (tid < FCHUNKS) {
+        const int ky = tid / (FKC / 2), kq = tid - ky * (FKC / 2);
+        const int cy = y0 - 1 + ky, cx = x0 - 1 + 2 * kq;
+        const bool ok = cy >= 0 && cy < Hc && cx >= -1 && cx + 1 <= P - 2;
+        cp_async16(dst + ky * FKC + 2 * kq, ok ? canvas + (ptrdiff_t)cy * P + cx : canvas,
+                   ok ? 16 : 0);
     }
 }
 
@@ -721,19 +728,22 @@ __device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam
     return transfer_z(c.src, dst, dmul(__ldg(c.rx + su), d), dmul(__ldg(c.ry + sv), d), d);
 }
 
+__device__ __forceinline__ double key_z(const ResolveContrib &c, const DevCam &dst, uint64_t w) {
+    return w == kEmpty ? INFINITY : winner_z(c, dst, (uint32_t)(w & ((1ull << c.b) - 1)));
+}
+
 __device__ __forceinline__ void cswap(double &a, double &b) {
     const double lo = fmin(a, b), hi = fmax(a, b);
     a = lo;
     b = hi;
 }
 
-// Phase "cells" of contribution k: splat policy + FG cull (synthesis.py:207-219)
-// for the 10x34 cells around the tile; writes f64 z (inf = uncovered).
+// Phase "cells" of one contribution: splat policy + FG cull (synthesis.py:
+// 207-219) for the 10x34 cells around the tile -> winner key (kEmpty = none).
 template <bool DBG>
-__device__ __forceinline__ int resolve_cells(const ResolveContrib &c, const DevCam &dst,
-                                             const uint64_t *K, double *szk, int *swin,
-                                             uint8_t *sst, uint64_t gen, int x0, int y0, int tid) {
-    const int Wd = dst.W, Hd = dst.H;
+__device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, int Hd,
+                                             const uint64_t *K, uint64_t *swk, uint8_t *sst,
+                                             uint64_t gen, int x0, int y0, int tid) {
     int any = 0;
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep) {
@@ -741,12 +751,11 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, const DevC
         if (i >= FCELLS) break;
         const int by = i / FBC, bx = i - by * FBC;
         const int qy = y0 - 1 + by, qx = x0 - 1 + bx;
-        double zq = INFINITY;
-        int wq = -1;
+        uint64_t w = kEmpty;
         uint8_t sq = kStageNone;
         if (qy >= 0 && qy < Hd && qx >= 0 && qx < Wd) {
             const int kc = (by + 1) * FKC + bx + 1;
-            uint64_t w = K[kc];
+            w = K[kc];
             if ((w >> kGenShift) == gen) {
                 sq = kStageCenter;
             } else {
@@ -780,15 +789,10 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, const DevC
                     }
                 }
             }
-            if (w != kEmpty) {
-                const uint32_t idx = (uint32_t)(w & ((1ull << c.b) - 1));
-                zq = winner_z(c, dst, idx);
-                wq = (int)idx;
-                any = 1;
-            }
+            any |= w != kEmpty;
         }
-        szk[i] = zq;
-        if (DBG) { swin[i] = wq; sst[i] = sq; }
+        swk[i] = w;
+        if (DBG) sst[i] = sq;
     }
     return any;
 }
@@ -797,10 +801,9 @@ template <int MAXR, bool DBG>
 __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ ResolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [2][FKEYS]
-    double *sz = reinterpret_cast<double *>(sk + 2 * FKEYS);     // [2][FCELLS]
-    double *sres = sz + 2 * FCELLS;                              // [MAXR][4][NT]
-    int *swin = reinterpret_cast<int *>(sres + MAXR * 4 * NT);   // [2][FCELLS] (DBG)
-    uint8_t *sst = reinterpret_cast<uint8_t *>(swin + 2 * FCELLS);  // [2][FCELLS] (DBG)
+    uint64_t *swk = sk + 2 * FKEYS;                              // [2][FCELLS] winner keys
+    double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
+    uint8_t *sst = reinterpret_cast<uint8_t *>(sres + MAXR * 4 * NT);  // [2][FCELLS] (DBG)
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
     const int ix = x0 + tx, iy = y0 + ty;
     const bool inimg = ix < Wd && iy < Hd;
     const size_t pix = (size_t)iy * Wd + ix;
-    const int Wc = Wd + 2, Hc = Hd + 2;
+    const int P = p.pitch, Hc = Hd + 2;
     const size_t plane = (size_t)Wd * Hd;
     const uint64_t gen = p.gen;
     const int ntot = p.n_fg + p.n_bg;
@@ -818,17 +821,17 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
     const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
 
     // prologue: keys of contributions 0 (and 1) in flight, cells of 0 resolved
-    stage_keys(sk, p.c[0].canvas, x0, y0, Wc, Hc, tid);
+    stage_keys(sk, p.c[0].canvas, x0, y0, P, Hc, tid);
     cp_async_commit();
     if (ntot > 1) {
-        stage_keys(sk + FKEYS, p.c[1].canvas, x0, y0, Wc, Hc, tid);
+        stage_keys(sk + FKEYS, p.c[1].canvas, x0, y0, P, Hc, tid);
         cp_async_commit();
         cp_async_wait<1>();
     } else {
         cp_async_wait<0>();
     }
     __syncthreads();
-    int any_next = resolve_cells<DBG>(p.c[0], dst, sk, sz, swin, sst, gen, x0, y0, tid);
+    int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
     double f0 = 0.0, f1 = 0.0, f2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
     bool fv = false, bv = false;
@@ -842,17 +845,17 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
         const int any = __syncthreads_or(any_next);
         // keys of k+2 into the buffer cells(k) just finished reading
         if (k + 2 < ntot) {
-            stage_keys(sk + (k & 1) * FKEYS, p.c[k + 2].canvas, x0, y0, Wc, Hc, tid);
+            stage_keys(sk + (k & 1) * FKEYS, p.c[k + 2].canvas, x0, y0, P, Hc, tid);
             cp_async_commit();
         }
-        // cells of k+1 (overlaps with the per-pixel work of k below)
+        // cells of k+1 (other warps' per-pixel work of k overlaps it)
         any_next = 0;
         if (k + 1 < ntot)
-            any_next = resolve_cells<DBG>(p.c[k + 1], dst, sk + ((k + 1) & 1) * FKEYS,
-                                          sz + ((k + 1) & 1) * FCELLS, swin + ((k + 1) & 1) * FCELLS,
+            any_next = resolve_cells<DBG>(p.c[k + 1], Wd, Hd, sk + ((k + 1) & 1) * FKEYS,
+                                          swk + ((k + 1) & 1) * FCELLS,
                                           sst + ((k + 1) & 1) * FCELLS, gen, x0, y0, tid);
         const ResolveContrib &c = p.c[k];
-        const double *szk = sz + (k & 1) * FCELLS;
+        const uint64_t *W = swk + (k & 1) * FCELLS;
         double z = INFINITY;
         int win = -1;
         uint8_t st = kStageNone;
@@ -860,17 +863,25 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
         double c0 = 0.0, c1 = 0.0, c2 = 0.0;
         if (any && inimg) {
             const int bi = (ty + 1) * FBC + tx + 1;
-            z = szk[bi];
-            if (DBG) { win = swin[(k & 1) * FCELLS + bi]; st = sst[(k & 1) * FCELLS + bi]; }
-            if (!(z < INFINITY)) {
-                // crack median (synthesis.py:90-125): >= 5 of 8 finite neighbours
-                double v0 = szk[bi - FBC - 1], v1 = szk[bi - FBC], v2 = szk[bi - FBC + 1],
-                       v3 = szk[bi - 1], v4 = szk[bi + 1], v5 = szk[bi + FBC - 1],
-                       v6 = szk[bi + FBC], v7 = szk[bi + FBC + 1];
-                const int cnt = (v0 < INFINITY) + (v1 < INFINITY) + (v2 < INFINITY) +
-                                (v3 < INFINITY) + (v4 < INFINITY) + (v5 < INFINITY) +
-                                (v6 < INFINITY) + (v7 < INFINITY);
+            const uint64_t wk = W[bi];
+            if (DBG) st = sst[(k & 1) * FCELLS + bi];
+            if (wk != kEmpty) {
+                const uint32_t idx = (uint32_t)(wk & ((1ull << c.b) - 1));
+                z = winner_z(c, dst, idx);
+                win = (int)idx;
+            } else {
+                // crack median (synthesis.py:90-125): >= 5 of 8 covered neighbours;
+                // their exact z is recomputed only here (rare)
+                const uint64_t k0 = W[bi - FBC - 1], k1 = W[bi - FBC], k2 = W[bi - FBC + 1],
+                               k3 = W[bi - 1], k4 = W[bi + 1], k5 = W[bi + FBC - 1],
+                               k6 = W[bi + FBC], k7 = W[bi + FBC + 1];
+                const int cnt = (k0 != kEmpty) + (k1 != kEmpty) + (k2 != kEmpty) +
+                                (k3 != kEmpty) + (k4 != kEmpty) + (k5 != kEmpty) +
+                                (k6 != kEmpty) + (k7 != kEmpty);
                 if (cnt >= 5) {
+                    double v0 = key_z(c, dst, k0), v1 = key_z(c, dst, k1), v2 = key_z(c, dst, k2),
+                           v3 = key_z(c, dst, k3), v4 = key_z(c, dst, k4), v5 = key_z(c, dst, k5),
+                           v6 = key_z(c, dst, k6), v7 = key_z(c, dst, k7);
                     // Batcher odd-even merge sort of 8 (inf sorts last)
                     cswap(v0, v1); cswap(v2, v3); cswap(v4, v5); cswap(v6, v7);
                     cswap(v0, v2); cswap(v1, v3); cswap(v4, v6); cswap(v5, v7);
@@ -883,7 +894,6 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
                     if (cnt & 1) z = lo;
                     else z = ddiv(dadd(lo, cnt == 6 ? v3 : v4), 2.0);
                     st = kStageCrack;
-                    win = -1;
                 }
             }
             // backward colour fetch (synthesis.py:224-247, _bilinear_fetch :128-159)
@@ -1024,8 +1034,8 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
 
 template <int MAXR>
 static size_t fast_smem() {
-    return 2 * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(double) +
-           (size_t)MAXR * 4 * NT * sizeof(double) + 2 * FCELLS * sizeof(int) + 2 * FCELLS;
+    return 2 * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
+           (size_t)MAXR * 4 * NT * sizeof(double) + 2 * FCELLS;
 }
 
 template <typename K>

@@ -44,9 +44,14 @@ struct WarpContrib {
     int b;                   // index bits
 };
 
+// Canvas layout: element (cy, cx) of a (Hd+2r) x (Wd+2r) canvas lives at
+// ptr[cy * pitch + cx], where ptr = allocation + 1 + k * per and pitch is even
+// and >= Wd+2r+1, so that tile rows starting at image column x0 (a multiple
+// of 32) are 16-byte aligned for cp.async staging.
 struct WarpParams {
     DevCam dst;
     int r;
+    int pitch;
     int n;
     uint64_t gen_hi;         // generation code << 57
     WarpContrib c[2 * FVV_MAX_REFS];
@@ -68,6 +73,7 @@ struct ResolveContrib {
 struct ResolveParams {
     DevCam dst;
     int r, window, need;
+    int pitch;
     uint64_t gen;            // generation code (0..127)
     int n_fg, n_bg;
     double band_rel;

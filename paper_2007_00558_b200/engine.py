@@ -152,3 +152,92 @@ def synthesize(virtual_camera, mvd_frame: Mapping, refs=None, cfg: Optional[Synt
     ``refs=None`` selects ``cfg.reference_count`` nearest cameras."""
     r = EdgeRenderer(rig, bg_models, cfg)
     return r.synthesize(virtual_camera, mvd_frame, refs, hole_closing=hole_closing)
+
+
+class FrameUploader:
+    """Double-buffered host->device staging of live frames on a copy stream.
+
+    ``put(frame)`` enqueues the pinned-host -> HBM copies of one frame
+    (``{cam_id: (rgb u8 HxWx3, mm int16/uint16 HxW, validity u8 HxW)}``) on a
+    dedicated stream and returns a ticket; ``get(ticket)`` makes the current
+    (compute) stream wait for those copies and returns the device tensors.
+    With ``depth`` >= 2 the upload of frame t+1 overlaps the synthesis of
+    frame t, so a PCIe-fed edge server is bounded by the link, not by
+    copy + compute in series.
+    """
+
+    def __init__(self, example_frame: Mapping, depth: int = 2, device=None):
+        self.dev = _dev.device() if device is None else torch.device(device)
+        self.stream = torch.cuda.Stream(self.dev)
+        self.depth = depth
+        self.bufs = [{cid: tuple(torch.empty(tuple(t.shape), dtype=t.dtype, device=self.dev)
+                                 for t in ts) for cid, ts in example_frame.items()}
+                     for _ in range(depth)]
+        self.done = [None] * depth        # copy-finished events
+        self.free = [None] * depth        # consumer-finished events
+        self.n = 0
+        self.bytes = 0
+
+    def put(self, frame: Mapping) -> int:
+        slot = self.n % self.depth
+        with torch.cuda.stream(self.stream):
+            if self.free[slot] is not None:
+                self.stream.wait_event(self.free[slot])
+            for cid, ts in frame.items():
+                for dst, src in zip(self.bufs[slot][cid], ts):
+                    dst.copy_(src, non_blocking=True)
+                    self.bytes += src.numel() * src.element_size()
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.done[slot] = ev
+        self.n += 1
+        return self.n - 1
+
+    def get(self, ticket: int) -> Mapping:
+        slot = ticket % self.depth
+        torch.cuda.current_stream(self.dev).wait_event(self.done[slot])
+        return self.bufs[slot]
+
+    def release(self, ticket: int) -> None:
+        """The current stream is done reading this ticket's buffers."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self.free[ticket % self.depth] = ev
+
+
+class ResultDownloader:
+    """Device -> pinned-host copies of rendered views on a separate stream."""
+
+    def __init__(self, shape, depth: int = 2, device=None):
+        self.dev = _dev.device() if device is None else torch.device(device)
+        self.stream = torch.cuda.Stream(self.dev)
+        self.host = [torch.empty(tuple(shape), dtype=torch.uint8).pin_memory()
+                     for _ in range(depth)]
+        self.depth = depth
+        self.n = 0
+        self.bytes = 0
+        self.events = [None] * depth
+
+    def put(self, views: torch.Tensor) -> torch.Tensor:
+        """Queue the copy of ``views`` (after the current stream's work);
+        returns the pinned host tensor it lands in (valid after ``sync``)."""
+        slot = self.n % self.depth
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(self.stream):
+            if self.events[slot] is not None:
+                self.events[slot].synchronize()
+            self.stream.wait_event(ready)
+            dst = self.host[slot][:views.shape[0]]
+            dst.copy_(views, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.events[slot] = ev
+        self.bytes += views.numel()
+        self.n += 1
+        return dst
+
+    def wait_into(self, stream) -> None:
+        for ev in self.events:
+            if ev is not None:
+                stream.wait_event(ev)
