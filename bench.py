@@ -479,11 +479,18 @@ def run_ours(args):
         kern[name]["share"] = prof[name][0] / tot_ms if tot_ms else None
     dom = max(kern, key=lambda n: prof[n][0])
     dom_bytes = per_kernel.get(dom)
+    # ncu DRAM bytes per launch of the same kernel, from the committed capture
+    traffic = None
+    tfile = ROOT / "profiles" / "r01_traffic.json"
+    if tfile.exists():
+        kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
+              "resolve": "k_resolve_fast"}.get(dom)
+        traffic = json.loads(tfile.read_text()).get(kn)
     roof = None
     if dom_bytes:
         ach = dom_bytes / (kern[dom]["avg_ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "algorithmic_bytes_per_launch": dom_bytes,
+                "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": peak_src}
     pipe = value / ws * b_view / 1e9
     line = {
