@@ -16,7 +16,10 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).with_name("libfvvb200.so")
+import os
+
+# FVV_B200_LIB overrides the library path (kernel-variant experiments only)
+LIB_PATH = Path(os.environ.get("FVV_B200_LIB") or Path(__file__).with_name("libfvvb200.so"))
 
 FVV_OK, FVV_EINVAL, FVV_ECUDA = 0, 1, 2
 MAX_REFS = 16

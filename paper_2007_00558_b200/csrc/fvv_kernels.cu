@@ -15,6 +15,7 @@
 
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "fvv_kernels.cuh"
 
@@ -688,6 +689,9 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 //          masked bilinear fetch; per-contribution result kept in smem.
 // then mix_layer x2 and composite per pixel.
 
+#ifndef FVV_K3_MINB
+#define FVV_K3_MINB 4
+#endif
 constexpr int FKR = TY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36
 constexpr int FBR = TY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
 constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
@@ -797,18 +801,114 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
     return any;
 }
 
+// crack median of a hole pixel from its 8 neighbours' winner keys (rare path,
+// kept out of line so the unrolled kernel stays small)
+#ifndef FVV_K3_CRACK_NOINLINE
+#define FVV_K3_CRACK_NOINLINE 0
+#endif
+#if FVV_K3_CRACK_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+double crack_z(const ResolveContrib &c, const DevCam &dst,
+                                       const uint64_t *W, int bi, int *stage) {
+    const uint64_t k0 = W[bi - FBC - 1], k1 = W[bi - FBC], k2 = W[bi - FBC + 1], k3 = W[bi - 1],
+                   k4 = W[bi + 1], k5 = W[bi + FBC - 1], k6 = W[bi + FBC], k7 = W[bi + FBC + 1];
+    const int cnt = (k0 != kEmpty) + (k1 != kEmpty) + (k2 != kEmpty) + (k3 != kEmpty) +
+                    (k4 != kEmpty) + (k5 != kEmpty) + (k6 != kEmpty) + (k7 != kEmpty);
+    if (cnt < 5) return INFINITY;
+    double v0 = key_z(c, dst, k0), v1 = key_z(c, dst, k1), v2 = key_z(c, dst, k2),
+           v3 = key_z(c, dst, k3), v4 = key_z(c, dst, k4), v5 = key_z(c, dst, k5),
+           v6 = key_z(c, dst, k6), v7 = key_z(c, dst, k7);
+    cswap(v0, v1); cswap(v2, v3); cswap(v4, v5); cswap(v6, v7);
+    cswap(v0, v2); cswap(v1, v3); cswap(v4, v6); cswap(v5, v7);
+    cswap(v1, v2); cswap(v5, v6);
+    cswap(v0, v4); cswap(v1, v5); cswap(v2, v6); cswap(v3, v7);
+    cswap(v2, v4); cswap(v3, v5);
+    cswap(v1, v2); cswap(v3, v4); cswap(v5, v6);
+    *stage = kStageCrack;
+    const double lo = cnt <= 6 ? v2 : v3;
+    return (cnt & 1) ? lo : ddiv(dadd(lo, cnt == 6 ? v3 : v4), 2.0);
+}
+
+// backward projection + masked bilinear fetch of one covered pixel
+// (synthesis.py:224-247, _bilinear_fetch :128-159)
+__device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst, double rxd,
+                                      double ryd, double z, double &c0, double &c1, double &c2) {
+    double xs, ys, zs;
+    transfer(dst, c.src, dmul(rxd, z), dmul(ryd, z), z, xs, ys, zs);
+    if (!(zs > 0.0)) return false;
+    const int Ws = c.src.W, Hs = c.src.H;
+    double us, vs;
+    if (zs > 1e-100) {
+        const double rz = rcp_nr(zs);
+        us = dadd(div_rcp(dmul(c.src.fx, xs), zs, rz), c.src.cx);
+        vs = dadd(div_rcp(dmul(c.src.fy, ys), zs, rz), c.src.cy);
+    } else {
+        us = proj(c.src.fx, xs, zs, c.src.cx);
+        vs = proj(c.src.fy, ys, zs, c.src.cy);
+    }
+    if (!(us >= -0.5 && us <= (double)Ws - 0.5 && vs >= -0.5 && vs <= (double)Hs - 0.5))
+        return false;
+    const double uc = fmin(fmax(us, 0.0), (double)(Ws - 1));
+    const double vc = fmin(fmax(vs, 0.0), (double)(Hs - 1));
+    const double u0 = floor(uc), v0 = floor(vc);
+    const int iu = (int)u0, iv = (int)v0;
+    const double fu = dsub(uc, u0), fv = dsub(vc, v0);
+    const double omu = dsub(1.0, fu), omv = dsub(1.0, fv);
+    const bool inu = iu + 1 < Ws, inv = iv + 1 < Hs;
+    const uint32_t *row0 = c.texel + (size_t)iv * Ws + iu;
+    const uint32_t fl = c.flag << 24;
+    const uint32_t t0 = __ldg(row0);
+    const uint32_t t1 = inu ? __ldg(row0 + 1) : 0u;
+    const uint32_t t2 = inv ? __ldg(row0 + Ws) : 0u;
+    const uint32_t t3 = (inu && inv) ? __ldg(row0 + Ws + 1) : 0u;
+    // a masked tap weight of +0.0 adds exactly nothing (synthesis.py:154)
+    const double w0 = (t0 & fl) ? dmul(omu, omv) : 0.0;
+    const double w1 = (t1 & fl) ? dmul(fu, omv) : 0.0;
+    const double w2 = (t2 & fl) ? dmul(omu, fv) : 0.0;
+    const double w3 = (t3 & fl) ? dmul(fu, fv) : 0.0;
+#define FVV_CH(T, SH) (double)(((T) >> (SH)) & 0xFFu)
+    c0 = dadd(dadd(dadd(dmul(w0, FVV_CH(t0, 0)), dmul(w1, FVV_CH(t1, 0))), dmul(w2, FVV_CH(t2, 0))),
+              dmul(w3, FVV_CH(t3, 0)));
+    c1 = dadd(dadd(dadd(dmul(w0, FVV_CH(t0, 8)), dmul(w1, FVV_CH(t1, 8))), dmul(w2, FVV_CH(t2, 8))),
+              dmul(w3, FVV_CH(t3, 8)));
+    c2 = dadd(dadd(dadd(dmul(w0, FVV_CH(t0, 16)), dmul(w1, FVV_CH(t1, 16))),
+                   dmul(w2, FVV_CH(t2, 16))), dmul(w3, FVV_CH(t3, 16)));
+#undef FVV_CH
+    const double s = dadd(dadd(dadd(w0, w1), w2), w3);
+    if (!(s > 1e-12)) return false;
+    const double rs = rcp_nr(s);
+    c0 = div_rcp(c0, s, rs);
+    c1 = div_rcp(c1, s, rs);
+    c2 = div_rcp(c2, s, rs);
+    return true;
+}
+
+#ifndef FVV_K3_NBUF
+#define FVV_K3_NBUF 2
+#endif
+constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of the one shaded)
+
+// One 32x8 tile per CTA; the 12x36 key tiles of the next three contributions
+// are in flight (cp.async groups) while the current one is shaded, and the
+// cells phase of contribution q+1 runs in the same barrier interval as the
+// per-pixel work of contribution q.
 template <int MAXR, bool DBG>
-__global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ ResolveParams p) {
+__global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [2][FKEYS]
-    uint64_t *swk = sk + 2 * FKEYS;                              // [2][FCELLS] winner keys
+    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
+    uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
-    uint8_t *sst = reinterpret_cast<uint8_t *>(sres + MAXR * 4 * NT);  // [2][FCELLS] (DBG)
+    double *sfg = sres + MAXR * 4 * NT;                          // [3][NT] merged FG colour
+    uint8_t *sst = reinterpret_cast<uint8_t *>(sfg + 3 * NT);    // [2][FCELLS] (DBG)
+    __shared__ int s_fresh[3];
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const DevCam &dst = p.dst;
     const int Wd = dst.W, Hd = dst.H;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const int ix = x0 + tx, iy = y0 + ty;
     const bool inimg = ix < Wd && iy < Hd;
     const size_t pix = (size_t)iy * Wd + ix;
@@ -816,46 +916,57 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
     const size_t plane = (size_t)Wd * Hd;
     const uint64_t gen = p.gen;
     const int ntot = p.n_fg + p.n_bg;
+    const int nitems = ntot;
+    // this thread's own staged chunk (visible to it after cp.async.wait_group)
+    const int my_chunk = tid < FCHUNKS ? (tid / (FKC / 2)) * FKC + 2 * (tid % (FKC / 2)) : -1;
     // virtual-camera ray of this pixel (pixel_rays, core.py:224-227)
     const double rxd = ddiv(dsub((double)ix, dst.cx), dst.fx);
     const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
 
-    // prologue: keys of contributions 0 (and 1) in flight, cells of 0 resolved
-    stage_keys(sk, p.c[0].canvas, x0, y0, P, Hc, tid);
-    cp_async_commit();
-    if (ntot > 1) {
-        stage_keys(sk + FKEYS, p.c[1].canvas, x0, y0, P, Hc, tid);
-        cp_async_commit();
-        cp_async_wait<1>();
-    } else {
-        cp_async_wait<0>();
-    }
+    auto stage = [&](int q) {
+        if (q < nitems) stage_keys(sk + (q % NBUF) * FKEYS, p.c[q].canvas, x0, y0, P, Hc, tid);
+        cp_async_commit();  // (possibly empty) group per item keeps the accounting uniform
+    };
+
+#pragma unroll
+    for (int q = 0; q < NBUF; ++q) stage(q);
+    cp_async_wait<NBUF - 1>();
+    if (tid < 3) s_fresh[tid] = 0;
     __syncthreads();
     int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
-    double f0 = 0.0, f1 = 0.0, f2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
     bool fv = false, bv = false;
     uint32_t vmask = 0;
 #pragma unroll 1
-    for (int k = 0; k < ntot; ++k) {
+    for (int q = 0; q < nitems; ++q) {
+        const int k = q;
         const bool fgl = k < p.n_fg;
         const int j = fgl ? k : k - p.n_fg;
-        // keys of k+1 must have landed; cells of k must be complete
-        cp_async_wait<0>();
-        const int any = __syncthreads_or(any_next);
-        // keys of k+2 into the buffer cells(k) just finished reading
-        if (k + 2 < ntot) {
-            stage_keys(sk + (k & 1) * FKEYS, p.c[k + 2].canvas, x0, y0, P, Hc, tid);
-            cp_async_commit();
+        // keys of q+1 must have landed (groups q+1 done, q+2 may pend); cells of q
+        // complete. Key tiles of q+1 with no fresh key skip their cells phase.
+        cp_async_wait<NBUF - 2>();
+        if (q + 1 < nitems && my_chunk >= 0) {
+            const uint64_t *Kn = sk + ((q + 1) % NBUF) * FKEYS + my_chunk;
+            if ((Kn[0] >> kGenShift) == gen || (Kn[1] >> kGenShift) == gen) s_fresh[q % 3] = 1;
         }
-        // cells of k+1 (other warps' per-pixel work of k overlaps it)
+        const int any = __syncthreads_or(any_next);
+        const int fresh_next = s_fresh[q % 3];
+        if (tid == 0) s_fresh[(q + 2) % 3] = 0;
+        // keys of q+NBUF into the buffer item q's cells phase (iteration q-1) used
+        stage(q + NBUF);
+        // cells of q+1 (other warps' per-pixel work of q overlaps it)
         any_next = 0;
-        if (k + 1 < ntot)
-            any_next = resolve_cells<DBG>(p.c[k + 1], Wd, Hd, sk + ((k + 1) & 1) * FKEYS,
-                                          swk + ((k + 1) & 1) * FCELLS,
-                                          sst + ((k + 1) & 1) * FCELLS, gen, x0, y0, tid);
+#ifdef FVV_EXP_NO_CELLS
+        if (false)
+#else
+        if (q + 1 < nitems && fresh_next)
+#endif
+            any_next = resolve_cells<DBG>(p.c[q + 1], Wd, Hd, sk + ((q + 1) % NBUF) * FKEYS,
+                                          swk + ((q + 1) & 1) * FCELLS,
+                                          sst + ((q + 1) & 1) * FCELLS, gen, x0, y0, tid);
         const ResolveContrib &c = p.c[k];
-        const uint64_t *W = swk + (k & 1) * FCELLS;
+        const uint64_t *W = swk + (q & 1) * FCELLS;
         double z = INFINITY;
         int win = -1;
         uint8_t st = kStageNone;
@@ -864,92 +975,21 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
         if (any && inimg) {
             const int bi = (ty + 1) * FBC + tx + 1;
             const uint64_t wk = W[bi];
-            if (DBG) st = sst[(k & 1) * FCELLS + bi];
+            if (DBG) st = sst[(q & 1) * FCELLS + bi];
             if (wk != kEmpty) {
                 const uint32_t idx = (uint32_t)(wk & ((1ull << c.b) - 1));
                 z = winner_z(c, dst, idx);
                 win = (int)idx;
             } else {
-                // crack median (synthesis.py:90-125): >= 5 of 8 covered neighbours;
-                // their exact z is recomputed only here (rare)
-                const uint64_t k0 = W[bi - FBC - 1], k1 = W[bi - FBC], k2 = W[bi - FBC + 1],
-                               k3 = W[bi - 1], k4 = W[bi + 1], k5 = W[bi + FBC - 1],
-                               k6 = W[bi + FBC], k7 = W[bi + FBC + 1];
-                const int cnt = (k0 != kEmpty) + (k1 != kEmpty) + (k2 != kEmpty) +
-                                (k3 != kEmpty) + (k4 != kEmpty) + (k5 != kEmpty) +
-                                (k6 != kEmpty) + (k7 != kEmpty);
-                if (cnt >= 5) {
-                    double v0 = key_z(c, dst, k0), v1 = key_z(c, dst, k1), v2 = key_z(c, dst, k2),
-                           v3 = key_z(c, dst, k3), v4 = key_z(c, dst, k4), v5 = key_z(c, dst, k5),
-                           v6 = key_z(c, dst, k6), v7 = key_z(c, dst, k7);
-                    // Batcher odd-even merge sort of 8 (inf sorts last)
-                    cswap(v0, v1); cswap(v2, v3); cswap(v4, v5); cswap(v6, v7);
-                    cswap(v0, v2); cswap(v1, v3); cswap(v4, v6); cswap(v5, v7);
-                    cswap(v1, v2); cswap(v5, v6);
-                    cswap(v0, v4); cswap(v1, v5); cswap(v2, v6); cswap(v3, v7);
-                    cswap(v2, v4); cswap(v3, v5);
-                    cswap(v1, v2); cswap(v3, v4); cswap(v5, v6);
-                    // cnt in 5..8: lower middle v2 (5,6) or v3 (7,8); upper v3 (6) / v4 (8)
-                    const double lo = cnt <= 6 ? v2 : v3;
-                    if (cnt & 1) z = lo;
-                    else z = ddiv(dadd(lo, cnt == 6 ? v3 : v4), 2.0);
-                    st = kStageCrack;
-                }
+                // crack median (synthesis.py:90-125), rare: out of line
+                int stc = st;
+                z = crack_z(c, dst, W, bi, &stc);
+                st = (uint8_t)stc;
             }
-            // backward colour fetch (synthesis.py:224-247, _bilinear_fetch :128-159)
-            if (z < INFINITY) {
-                double xs, ys, zs;
-                transfer(dst, c.src, dmul(rxd, z), dmul(ryd, z), z, xs, ys, zs);
-                if (zs > 0.0) {
-                    const int Ws = c.src.W, Hs = c.src.H;
-                    double us, vs;
-                    if (zs > 1e-100) {
-                        const double rz = rcp_nr(zs);
-                        us = dadd(div_rcp(dmul(c.src.fx, xs), zs, rz), c.src.cx);
-                        vs = dadd(div_rcp(dmul(c.src.fy, ys), zs, rz), c.src.cy);
-                    } else {
-                        us = proj(c.src.fx, xs, zs, c.src.cx);
-                        vs = proj(c.src.fy, ys, zs, c.src.cy);
-                    }
-                    if (us >= -0.5 && us <= (double)Ws - 0.5 && vs >= -0.5 &&
-                        vs <= (double)Hs - 0.5) {
-                        const double uc = fmin(fmax(us, 0.0), (double)(Ws - 1));
-                        const double vc = fmin(fmax(vs, 0.0), (double)(Hs - 1));
-                        const double u0 = floor(uc), v0 = floor(vc);
-                        const int iu = (int)u0, iv = (int)v0;
-                        const double fu = dsub(uc, u0), fv_ = dsub(vc, v0);
-                        const double omu = dsub(1.0, fu), omv = dsub(1.0, fv_);
-                        const bool inu = iu + 1 < Ws, inv = iv + 1 < Hs;
-                        const uint32_t *row0 = c.texel + (size_t)iv * Ws + iu;
-                        const uint32_t fl = c.flag << 24;
-                        const uint32_t t0 = __ldg(row0);
-                        const uint32_t t1 = inu ? __ldg(row0 + 1) : 0u;
-                        const uint32_t t2 = inv ? __ldg(row0 + Ws) : 0u;
-                        const uint32_t t3 = (inu && inv) ? __ldg(row0 + Ws + 1) : 0u;
-                        double s = 0.0;
-#define FVV_TAP(T, WT)                                                          \
-    if ((T) & fl) {                                                             \
-        const double w_ = (WT);                                                 \
-        c0 = dadd(c0, dmul(w_, (double)((T) & 0xFFu)));                         \
-        c1 = dadd(c1, dmul(w_, (double)(((T) >> 8) & 0xFFu)));                  \
-        c2 = dadd(c2, dmul(w_, (double)(((T) >> 16) & 0xFFu)));                 \
-        s = dadd(s, w_);                                                        \
-    }
-                        FVV_TAP(t0, dmul(omu, omv))
-                        FVV_TAP(t1, dmul(fu, omv))
-                        FVV_TAP(t2, dmul(omu, fv_))
-                        FVV_TAP(t3, dmul(fu, fv_))
-#undef FVV_TAP
-                        if (s > 1e-12) {
-                            ok = true;
-                            const double rs = rcp_nr(s);
-                            c0 = div_rcp(c0, s, rs);
-                            c1 = div_rcp(c1, s, rs);
-                            c2 = div_rcp(c2, s, rs);
-                        }
-                    }
-                }
-            }
+#ifdef FVV_EXP_NO_BACKWARD
+            if (z < INFINITY) { ok = true; c0 = z; c1 = z; c2 = z; z = INFINITY; }
+#endif
+            if (z < INFINITY) ok = fetch(c, dst, rxd, ryd, z, c0, c1, c2);
         }
         if (!ok) { c0 = c1 = c2 = 0.0; }
         const double zd = ok ? z : 0.0;
@@ -976,19 +1016,19 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
             const int n = j + 1;
             const int kb = k - j;
             double zmin = INFINITY;
-            for (int q = 0; q < n; ++q) {
-                const double zj = sres[(q * 4 + 3) * NT + tid];
-                if (((vmask >> q) & 1u) && zj < zmin) zmin = zj;
+            for (int qq = 0; qq < n; ++qq) {
+                const double zj = sres[(qq * 4 + 3) * NT + tid];
+                if (((vmask >> qq) & 1u) && zj < zmin) zmin = zj;
             }
             const double thr = dadd(zmin, dmul(p.band_rel, zmin));
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
-            for (int q = 0; q < n; ++q) {
-                const double zj = sres[(q * 4 + 3) * NT + tid];
-                if (((vmask >> q) & 1u) && zj <= thr) {
-                    const double w = p.c[kb + q].weight;
-                    a0 = dadd(a0, dmul(w, sres[(q * 4 + 0) * NT + tid]));
-                    a1 = dadd(a1, dmul(w, sres[(q * 4 + 1) * NT + tid]));
-                    a2 = dadd(a2, dmul(w, sres[(q * 4 + 2) * NT + tid]));
+            for (int qq = 0; qq < n; ++qq) {
+                const double zj = sres[(qq * 4 + 3) * NT + tid];
+                if (((vmask >> qq) & 1u) && zj <= thr) {
+                    const double w = p.c[kb + qq].weight;
+                    a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * NT + tid]));
+                    a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * NT + tid]));
+                    a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * NT + tid]));
                     if (DBG) ad = dadd(ad, dmul(w, zj));
                     aw = dadd(aw, w);
                 }
@@ -1001,8 +1041,14 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
                 m1 = div_rcp(a1, aw, ra);
                 m2 = div_rcp(a2, aw, ra);
             }
-            if (fgl) { f0 = m0; f1 = m1; f2 = m2; fv = mv; }
-            else { b0 = m0; b1 = m1; b2 = m2; bv = mv; }
+            if (fgl) {
+                sfg[tid] = m0;
+                sfg[NT + tid] = m1;
+                sfg[2 * NT + tid] = m2;
+                fv = mv;
+            } else {
+                b0 = m0; b1 = m1; b2 = m2; bv = mv;
+            }
             vmask = 0;
             if (DBG && inimg) {
                 const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
@@ -1015,27 +1061,28 @@ __global__ void __launch_bounds__(NT, 3) k_resolve_fast(const __grid_constant__ 
                 if (p.dbg.merged_valid) p.dbg.merged_valid[o] = mv ? 1 : 0;
             }
         }
-    }
-    // -- composite (synthesis.py:295-318): hole, then BG, then FG; rint, clip
-    if (inimg) {
-        double o0, o1, o2;
-        if (fv) { o0 = f0; o1 = f1; o2 = f2; }
-        else if (bv) { o0 = b0; o1 = b1; o2 = b2; }
-        else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
-        if (p.rgb_out) {
-            uint8_t *o = p.rgb_out + pix * 3;
-            o[0] = (uint8_t)fmin(fmax(rint(o0), 0.0), 255.0);
-            o[1] = (uint8_t)fmin(fmax(rint(o1), 0.0), 255.0);
-            o[2] = (uint8_t)fmin(fmax(rint(o2), 0.0), 255.0);
+        // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
+        if (k == ntot - 1 && inimg) {
+            double o0, o1, o2;
+            if (fv) { o0 = sfg[tid]; o1 = sfg[NT + tid]; o2 = sfg[2 * NT + tid]; }
+            else if (bv) { o0 = b0; o1 = b1; o2 = b2; }
+            else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
+            if (p.rgb_out) {
+                uint8_t *o = p.rgb_out + pix * 3;
+                o[0] = (uint8_t)fmin(fmax(rint(o0), 0.0), 255.0);
+                o[1] = (uint8_t)fmin(fmax(rint(o1), 0.0), 255.0);
+                o[2] = (uint8_t)fmin(fmax(rint(o2), 0.0), 255.0);
+            }
+            if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
         }
-        if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
     }
+    cp_async_wait<0>();
 }
 
 template <int MAXR>
 static size_t fast_smem() {
-    return 2 * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
-           (size_t)MAXR * 4 * NT * sizeof(double) + 2 * FCELLS;
+    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
+           (size_t)MAXR * 4 * NT * sizeof(double) + 3 * NT * sizeof(double) + 2 * FCELLS;
 }
 
 template <typename K>
@@ -1052,13 +1099,18 @@ cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0) {
         static bool init = false;
         if (!init) {
+            raise_smem(k_resolve_fast<3, false>, fast_smem<3>());
+            raise_smem(k_resolve_fast<3, true>, fast_smem<3>());
             raise_smem(k_resolve_fast<4, false>, fast_smem<4>());
             raise_smem(k_resolve_fast<4, true>, fast_smem<4>());
             raise_smem(k_resolve_fast<FVV_MAX_REFS, false>, fast_smem<FVV_MAX_REFS>());
             raise_smem(k_resolve_fast<FVV_MAX_REFS, true>, fast_smem<FVV_MAX_REFS>());
             init = true;
         }
-        if (maxn <= 4) {
+        if (maxn <= 3) {
+            if (dbg) k_resolve_fast<3, true><<<grid, NT, fast_smem<3>(), s>>>(p);
+            else k_resolve_fast<3, false><<<grid, NT, fast_smem<3>(), s>>>(p);
+        } else if (maxn <= 4) {
             if (dbg) k_resolve_fast<4, true><<<grid, NT, fast_smem<4>(), s>>>(p);
             else k_resolve_fast<4, false><<<grid, NT, fast_smem<4>(), s>>>(p);
         } else {
