@@ -113,7 +113,8 @@ int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t 
 /* Numerics self-test of the shared-reciprocal division and K2's filtered
  * rint(f*x/z + c) against the correctly rounded __ddiv_rn path, on n seeded
  * samples of operand class `mode` (0 bilinear, 1 projection, 2 mix, 3 wide
- * log-uniform, 4 near-half projections). Adds mismatches to *mismatches_dev. */
+ * log-uniform, 4 near-half projections, 5 all u16 mm -> m quotients).
+ * Adds mismatches to *mismatches_dev. */
 int fvv_selftest_division(fvv_ctx *ctx, int64_t n, uint64_t seed, int32_t mode,
                           uint64_t *mismatches_dev);
 

@@ -357,7 +357,7 @@ int fvv_selftest_division(fvv_ctx *ctx, int64_t n, uint64_t seed, int32_t mode,
                           uint64_t *mismatches_dev) {
     int rc = enter(ctx);
     if (rc) return rc;
-    if (n < 0 || mode < 0 || mode > 4 || !mismatches_dev)
+    if (n < 0 || mode < 0 || mode > 5 || !mismatches_dev)
         return fail(ctx, FVV_EINVAL, "selftest_division: bad arguments");
     LAUNCH(launch_selftest_div(n, seed, mode, (unsigned long long *)mismatches_dev, ctx->stream));
     return FVV_OK;

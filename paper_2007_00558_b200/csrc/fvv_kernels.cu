@@ -53,6 +53,9 @@ cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s)
 // ---------------------------------------------------------------------------
 // K0 + K1 + ingest
 
+#ifndef FVV_PRE_MINB
+#define FVV_PRE_MINB 4
+#endif
 constexpr int PX = 128, PY = 8, PMAXR = 4;  // tile: 8 rows x 128 px, 4 px per thread
 constexpr int PSC = PX + 2 * PMAXR, PSR = PY + 2 * PMAXR;
 
@@ -72,10 +75,20 @@ __device__ __forceinline__ uint32_t yuv_code(const PreprocParams &p, int iy, int
     return (msb << 8) | lsb;
 }
 
+// (float)mm / 1000.0f correctly rounded: product with the rounded reciprocal
+// and one FMA residual correction. Equal to the IEEE quotient for every u16
+// (verified exhaustively with exact rational arithmetic, and on the device by
+// fvv_selftest_division mode 5).
+__device__ __forceinline__ float mm_to_m(uint32_t mm) {
+    const float a = (float)mm, r = 1.0f / 1000.0f;
+    const float q = __fmul_rn(a, r);
+    return __fmaf_rn(__fmaf_rn(-1000.0f, q, a), r, q);
+}
+
 // core.depth_from_millimeters (core.py:260-269): fp32 TRUE division by 1000
 __device__ __forceinline__ void decode_mm(uint32_t mm, uint8_t &val, float &z) {
     if (val == FVV_VALID && mm == 0) val = FVV_INVALID;
-    z = (val == FVV_VALID) ? __fdiv_rn((float)mm, 1000.0f) : 0.0f;
+    z = (val == FVV_VALID) ? mm_to_m(mm) : 0.0f;
 }
 
 // depthcodec.dequantize12 / dequantize_codes (depthcodec.py:113-138)
@@ -119,20 +132,19 @@ __device__ __forceinline__ uchar4 load_rgb(const PreprocParams &p, size_t i) {
 // The 5x5 joint-bilateral fill (depthproc.py:171-224) only runs when the
 // tile holds an Invalid pixel: then the 2-px halo is staged in shared memory
 // (zero-padded like scenegen._shift2d: outside pixels are never Valid).
-__global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ PreprocParams p) {
+__global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_constant__ PreprocParams p) {
     __shared__ float sz[PSR * PSC];
     __shared__ uint8_t sv[PSR * PSC];
     __shared__ uchar4 sg[PSR * PSC];
     __shared__ float s_fill[PY * PX];
-    __shared__ uint16_t s_queue[PY * PX];
-    __shared__ int s_holes, s_nq;
+    __shared__ int s_holes;
 
     const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
     const int iy = y0 + ty, xb = x0 + lane * 4;
     const int R = p.radius;
     const int SC = PX + 2 * R;
-    if (tid == 0) { s_holes = 0; s_nq = 0; }
+    if (tid == 0) s_holes = 0;
 
     float z[4];
     uint8_t val[4];
@@ -207,51 +219,85 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ P
             sg[si] = gg;
         }
         __syncthreads();
-        // Every Invalid pixel goes to a work queue drained by all 256 threads
-        // (dense, instead of divergent per-lane loops over 4 pixels)
-        unsigned qmask = 0;
+        // Each warp drains the Invalid pixels of its own 128-px row segment:
+        // ballot + __fns compaction, so the 24-tap loops run on dense lanes
+        // without another block barrier.
+        // Invalid pixels with fewer than min_valid Valid neighbours can never
+        // fill: count them with SIMD byte compares on the staged validity
+        // (Valid == 0 bytes) and keep only the candidates (sky / miss regions
+        // drop out here instead of running 24-tap loops).
+        unsigned hm[4];
+        int nh_warp = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (val[q] != FVV_INVALID) continue;
-            s_queue[atomicAdd(&s_nq, 1)] = (uint16_t)(ty * PX + lane * 4 + q);
-            qmask |= 1u << q;
-        }
-        __syncthreads();
-        const int nq = s_nq;
-        for (int e = tid; e < nq; e += 256) {
-            const int lp = s_queue[e];
-            const int c0 = (lp / PX + R) * SC + (lp % PX) + R;
-            // depthproc.py:196-222: taps in dy-major order, centre skipped;
-            // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps;
-            // fill iff >= min_valid Valid taps and den > 0
-            const uchar4 gc = sg[c0];
-            const double g0 = gc.x, g1 = gc.y, g2 = gc.z;
-            double num = 0.0, den = 0.0;
-            int cnt = 0;
-            for (int dy = -R; dy <= R; ++dy) {
-                for (int dx = -R; dx <= R; ++dx) {
-                    if (dy == 0 && dx == 0) continue;
-                    const int ni = c0 + dy * SC + dx;
-                    if (sv[ni] != FVV_VALID) continue;
-                    const uchar4 n = sg[ni];
-                    const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
-                                 e2 = dsub(g2, (double)n.z);
-                    const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-                    const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
-                    num = dadd(num, dmul(w, (double)sz[ni]));
-                    den = dadd(den, w);
-                    ++cnt;
+            bool cand = false;
+            if (val[q] == FVV_INVALID) {
+                int cnt = 0;
+                const int x = lane * 4 + q;  // tile column; window columns x..x+2R in smem
+                if (R == 2) {
+                    // 5-byte window = 4 + 1 bytes out of two aligned words
+                    for (int dy = -2; dy <= 2; ++dy) {
+                        const int o = (ty + 2 + dy) * SC + x;
+                        const uint32_t *w = reinterpret_cast<const uint32_t *>(sv) + (o >> 2);
+                        const uint64_t span = (((uint64_t)w[1] << 32) | w[0]) >> (8 * (o & 3));
+                        cnt += __popc(__vcmpeq4((uint32_t)span, 0u)) / 8 +
+                               (((uint32_t)(span >> 32) & 0xFFu) == 0u);
+                    }
+                } else {
+                    for (int dy = -R; dy <= R; ++dy)
+                        for (int dx = -R; dx <= R; ++dx)
+                            cnt += sv[(ty + R + dy) * SC + x + R + dx] == FVV_VALID;
                 }
+                cand = cnt >= p.min_valid;
+                if (!cand) s_fill[ty * PX + x] = -1.0f;
             }
-            s_fill[lp] = (cnt >= p.min_valid && den > 0.0) ? __double2float_rn(ddiv(num, den))
-                                                           : -1.0f;
+            hm[q] = __ballot_sync(0xffffffffu, cand);
+            nh_warp += __popc(hm[q]);
         }
-        __syncthreads();
+        for (int base = 0; base < nh_warp; base += 32) {
+            int i = base + lane;
+            if (i < nh_warp) {
+                int qq = 0, src = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = __popc(hm[q]);
+                    if (i >= 0 && i < c) { qq = q; src = __fns(hm[q], 0, i + 1); }
+                    i -= c;
+                }
+                const int lp = ty * PX + src * 4 + qq;
+                const int c0 = (ty + R) * SC + src * 4 + qq + R;
+                // depthproc.py:196-222: taps in dy-major order, centre skipped;
+                // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps;
+                // fill iff >= min_valid Valid taps and den > 0
+                const uchar4 gc = sg[c0];
+                const double g0 = gc.x, g1 = gc.y, g2 = gc.z;
+                double num = 0.0, den = 0.0;
+                int cnt = 0;
+                for (int dy = -R; dy <= R; ++dy) {
+                    for (int dx = -R; dx <= R; ++dx) {
+                        if (dy == 0 && dx == 0) continue;
+                        const int ni = c0 + dy * SC + dx;
+                        if (sv[ni] != FVV_VALID) continue;
+                        const uchar4 n = sg[ni];
+                        const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
+                                     e2 = dsub(g2, (double)n.z);
+                        const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
+                        const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
+                        num = dadd(num, dmul(w, (double)sz[ni]));
+                        den = dadd(den, w);
+                        ++cnt;
+                    }
+                }
+                s_fill[lp] = (cnt >= p.min_valid && den > 0.0)
+                                 ? __double2float_rn(ddiv(num, den)) : -1.0f;
+            }
+        }
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            // a fill is a positive depth; -1 marks den == 0 (no fill)
+            // a fill is a positive depth; -1 marks "not filled"
             const int lp = ty * PX + lane * 4 + q;
-            if (((qmask >> q) & 1u) && s_fill[lp] >= 0.0f) {
+            if (val[q] == FVV_INVALID && s_fill[lp] >= 0.0f) {
                 z[q] = s_fill[lp];
                 val[q] = FVV_VALID;
             }
@@ -1163,6 +1209,13 @@ __global__ void k_selftest_div(long long n, uint64_t seed, int mode,
         } else {                // wide log-uniform magnitudes, both signs
             a = exp((unit(r1) * 2.0 - 1.0) * 69.0) * ((r3 & 1) ? -1.0 : 1.0);
             b = exp((unit(r2) * 2.0 - 1.0) * 69.0) * ((r3 & 2) ? -1.0 : 1.0);
+        }
+        if (mode == 5) {
+            if (i < 65536) {
+                const float t = __fdiv_rn((float)(uint32_t)i, 1000.0f);
+                bad += __float_as_uint(mm_to_m((uint32_t)i)) != __float_as_uint(t);
+            }
+            continue;
         }
         if (mode <= 3) {
             const double q = div_rcp(a, b, rcp_nr(b));
