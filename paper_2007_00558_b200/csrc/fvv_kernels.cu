@@ -365,23 +365,32 @@ cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
 // the ring min in K3 (verified equivalent).
 
 // rint((f*x)/z + c) — the target pixel of np.round(uv) (synthesis.py:193-194).
-// The quotient is first formed with a Newton-refined reciprocal (relative
-// error ~1e-15); only when the result lies within 1e-6 of a rounding boundary
-// (k + 0.5) is the correctly rounded __ddiv_rn path taken, so the rounded
-// target is always the one the exact float64 expression gives.
-__device__ __forceinline__ double proj_rint(double f, double x, double z, double c) {
+// The quotient is first formed with a Newton-refined reciprocal r of z
+// (shared by u and v, relative error ~1e-16); only when the result lies within
+// 1e-6 of a rounding boundary (k + 0.5) is the correctly rounded __ddiv_rn
+// path taken, so the rounded target is always the one the exact float64
+// expression gives (tests/test_gpu_numerics.py, mode 4).
+__device__ __forceinline__ double proj_rint_r(double f, double x, double z, double r, double c) {
     const double num = dmul(f, x);
+    const double ua = fma(num, r, c);
+    const double fl = floor(ua);
+    const double fr = ua - fl;
+    if (fabs(fr - 0.5) > 1e-6 && fabs(ua) < 1e8) return fr > 0.5 ? fl + 1.0 : fl;
+    return rint(dadd(ddiv(num, z), c));
+}
+
+__device__ __forceinline__ double rcp_approx2(double z) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
     double e = fma(-z, r, 1.0);
     r = fma(r, e, r);
     e = fma(-z, r, 1.0);
-    r = fma(r, e, r);
-    const double ua = fma(num, r, c);
-    const double fl = floor(ua);
-    const double fr = ua - fl;
-    if (fabs(fr - 0.5) > 1e-6 && fabs(ua) < 1e8 && z > 1e-200) return fr > 0.5 ? fl + 1.0 : fl;
-    return rint(dadd(ddiv(num, z), c));
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ double proj_rint(double f, double x, double z, double c) {
+    if (!(z > 1e-200)) return rint(dadd(ddiv(dmul(f, x), z), c));
+    return proj_rint_r(f, x, z, rcp_approx2(z), c);
 }
 
 constexpr int K2_THREADS = 128, K2_PX = 4;
@@ -413,13 +422,24 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
         double x, y, z;
         transfer(c.src, p.dst, dmul(__ldg(c.rx + su), dd), dmul(ry, dd), dd, x, y, z);
         if (!(z > 0.0)) continue;
-        const double ur = proj_rint(p.dst.fx, x, z, p.dst.cx);
-        if (!(ur >= lo && ur < uhi)) continue;
-        const double vr = proj_rint(p.dst.fy, y, z, p.dst.cy);
-        if (!(vr >= lo && vr < vhi)) continue;
+        double ur, vr;
+        if (z > 1e-200) {
+            const double rz = rcp_approx2(z);
+            ur = proj_rint_r(p.dst.fx, x, z, rz, p.dst.cx);
+            vr = proj_rint_r(p.dst.fy, y, z, rz, p.dst.cy);
+        } else {
+            ur = rint(dadd(ddiv(dmul(p.dst.fx, x), z), p.dst.cx));
+            vr = rint(dadd(ddiv(dmul(p.dst.fy, y), z), p.dst.cy));
+        }
+        if (!(ur >= lo && ur < uhi && vr >= lo && vr < vhi)) continue;
         const size_t cell = (size_t)((int)vr + r) * P + (size_t)((int)ur + r);
+#ifdef FVV_EXP_K2_NOATOMIC
+        const unsigned long long kk = p.gen_hi | zkey(z, (uint32_t)(row + su), c.b);
+        if (kk == 0x1234ull) c.canvas[cell] = kk;
+#else
         atomicMin((unsigned long long *)(c.canvas + cell),
                   (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
+#endif
     }
 }
 
@@ -1018,7 +1038,10 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         uint8_t st = kStageNone;
         bool ok = false;
         double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-        if (any && inimg) {
+        // BG contributions cannot change a pixel whose merged FG layer is valid
+        // (composite = FG over BG, synthesis.py:309-311): skip their fetch
+        // there unless every intermediate raster is requested (DBG)
+        if (any && inimg && (DBG || fgl || !fv)) {
             const int bi = (ty + 1) * FBC + tx + 1;
             const uint64_t wk = W[bi];
             if (DBG) st = sst[(q & 1) * FCELLS + bi];
