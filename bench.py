@@ -54,8 +54,8 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", default="c1", choices=("c0", "c1", "c2", "c3", "c4"))
     ap.add_argument("--frames", type=int, default=4, help="pre-staged frames to rotate over")
@@ -149,7 +149,7 @@ class Clocks:
             self.path = tempfile.mktemp(suffix=".csv")
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv",
-                                          "-lms", "100", "-i", str(self.dev)], stdout=self.fh,
+                                          "-lms", "50", "-i", str(self.dev)], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None

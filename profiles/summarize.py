@@ -133,7 +133,7 @@ def main():
     rep = sys.argv[1]
     print(f"# ncu summary: `{rep}`\n")
     if len(sys.argv) > 2:
-        print("## Launch list (gpu__time_duration, cold-cache serialised replay)\n")
+        print("## Launch list (gpu__time_duration per launch, serialised; see file for cache mode)\n")
         print("\n".join(launches(sys.argv[2])) + "\n")
     for i, d in enumerate(raw_rows(rep)):
         name = d.get("Kernel Name", ("?", ""))[0]
