@@ -969,7 +969,6 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
     double *sfg = sres + MAXR * 4 * NT;                          // [3][NT] merged FG colour
     uint8_t *sst = reinterpret_cast<uint8_t *>(sfg + 3 * NT);    // [2][FCELLS] (DBG)
-    __shared__ int s_fresh[3];
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const DevCam &dst = p.dst;
@@ -983,8 +982,6 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     const uint64_t gen = p.gen;
     const int ntot = p.n_fg + p.n_bg;
     const int nitems = ntot;
-    // this thread's own staged chunk (visible to it after cp.async.wait_group)
-    const int my_chunk = tid < FCHUNKS ? (tid / (FKC / 2)) * FKC + 2 * (tid % (FKC / 2)) : -1;
     // virtual-camera ray of this pixel (pixel_rays, core.py:224-227)
     const double rxd = ddiv(dsub((double)ix, dst.cx), dst.fx);
     const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
@@ -997,7 +994,6 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
 #pragma unroll
     for (int q = 0; q < NBUF; ++q) stage(q);
     cp_async_wait<NBUF - 1>();
-    if (tid < 3) s_fresh[tid] = 0;
     __syncthreads();
     int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
@@ -1010,24 +1006,14 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         const bool fgl = k < p.n_fg;
         const int j = fgl ? k : k - p.n_fg;
         // keys of q+1 must have landed (groups q+1 done, q+2 may pend); cells of q
-        // complete. Key tiles of q+1 with no fresh key skip their cells phase.
+        // complete
         cp_async_wait<NBUF - 2>();
-        if (q + 1 < nitems && my_chunk >= 0) {
-            const uint64_t *Kn = sk + ((q + 1) % NBUF) * FKEYS + my_chunk;
-            if ((Kn[0] >> kGenShift) == gen || (Kn[1] >> kGenShift) == gen) s_fresh[q % 3] = 1;
-        }
         const int any = __syncthreads_or(any_next);
-        const int fresh_next = s_fresh[q % 3];
-        if (tid == 0) s_fresh[(q + 2) % 3] = 0;
         // keys of q+NBUF into the buffer item q's cells phase (iteration q-1) used
         stage(q + NBUF);
         // cells of q+1 (other warps' per-pixel work of q overlaps it)
         any_next = 0;
-#ifdef FVV_EXP_NO_CELLS
-        if (false)
-#else
-        if (q + 1 < nitems && fresh_next)
-#endif
+        if (q + 1 < nitems)
             any_next = resolve_cells<DBG>(p.c[q + 1], Wd, Hd, sk + ((q + 1) % NBUF) * FKEYS,
                                           swk + ((q + 1) & 1) * FCELLS,
                                           sst + ((q + 1) & 1) * FCELLS, gen, x0, y0, tid);
