@@ -172,6 +172,39 @@ int fvv_composite(fvv_ctx *ctx, const double *fg_color, const uint8_t *fg_valid,
                   int32_t height, const uint8_t hole_color[3], uint8_t *rgb_out,
                   uint8_t *provenance_out);
 
+/* ---- capture-server chain ------------------------
+ * The producer side of the MVD stream, CaptureServer.capture
+ * (pipeline.py:381-397). All rasters device pointers; mean/var are the
+ * GaussianBgModel's (H,W,3) float64 arrays (depthproc.py:91-118). */
+/* depthproc.correct_depth (depthproc.py:67-84) */
+int fvv_correct_depth(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                      int32_t height, double alpha, double beta, float *depth_out,
+                      uint8_t *validity_out);
+/* depthproc.bg_train (depthproc.py:121-136); first != 0 on the model's first frame */
+int fvv_bg_train(fvv_ctx *ctx, const uint8_t *rgb, int32_t width, int32_t height, double *mean,
+                 double *var, int32_t first, double learning_rate, double var_floor);
+/* depthproc.classify_fg (depthproc.py:139-149): mask 1 = FG */
+int fvv_classify_fg(fvv_ctx *ctx, const uint8_t *rgb, const double *mean, const double *var,
+                    int32_t width, int32_t height, double threshold, uint8_t *fg_mask_out);
+/* depthproc.remove_bg_depth (depthproc.py:152-164) */
+int fvv_remove_bg_depth(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                        const uint8_t *fg_mask, int32_t width, int32_t height, float *depth_out,
+                        uint8_t *validity_out);
+/* depthcodec.quantize12 (depthcodec.py:83-110) */
+int fvv_quantize12(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                   int32_t height, double z_near, double z_far, uint16_t *codes_out);
+/* depthcodec.pack_yuv420 (depthcodec.py:180-193) */
+int fvv_pack_yuv420(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t height,
+                    uint8_t *y_out, uint8_t *u_out, uint8_t *v_out);
+/* correct -> classify -> remove BG -> quantize12 -> pack_yuv420 in one pass.
+ * do_correct = 0 skips the correction; bg_mean = NULL skips BG removal.
+ * codes_out may be NULL. */
+int fvv_capture_encode(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                       const uint8_t *rgb, int32_t width, int32_t height, int32_t do_correct,
+                       double alpha, double beta, const double *bg_mean, const double *bg_var,
+                       double threshold, double z_near, double z_far, uint8_t *y_out,
+                       uint8_t *u_out, uint8_t *v_out, uint16_t *codes_out);
+
 /* ---- session path: resident camera slots, batched views ---------------------
  * The edge server keeps a slot per rig camera: its calibration, its static
  * BG model (uploaded once, pipeline.py:445) and its latest live frame. */

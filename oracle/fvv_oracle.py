@@ -19,6 +19,10 @@ What it restates, function by function (each cites the reference line):
 * ``mix_layer``            synthesis.mix_layer              synthesis.py:261-292
 * ``composite``            synthesis.composite              synthesis.py:295-318
 * ``synthesize_view``      synthesis.synthesize_view        synthesis.py:331-362
+* ``quantize12`` / ``pack_yuv420``  depthcodec encoder       depthcodec.py:83-110,141-193
+* ``correct_depth``        depthproc.correct_depth          depthproc.py:67-84
+* ``bg_train`` / ``classify_fg``  depthproc BG model         depthproc.py:121-149
+* ``remove_bg_depth``      depthproc.remove_bg_depth        depthproc.py:152-164
 
 Differences from the reference, all deliberate and mirrored by the kernels:
 
@@ -533,3 +537,46 @@ def es_view(virtual, frames, cfg=None, hole_closing=True, debug=False):
         refs.append(dict(calib=f["calib"], rgb=f["rgb"], live_depth=d, live_validity=v,
                          bg_depth=f["bg_depth"], bg_validity=f["bg_validity"]))
     return synthesize_view(virtual, refs, cfg, debug=debug)
+
+
+# ----------------------------------------------------------------------------
+# capture-server chain
+
+
+def correct_depth(depth, validity, alpha, beta):
+    """depthproc.correct_depth (depthproc.py:67-84)."""
+    d = depth.astype(np.float64).copy()
+    val = validity.copy()
+    ok = val == VALID
+    z = d[ok]
+    d[ok] = (alpha * z + beta) * z
+    val[ok & (d <= 0)] = INVALID
+    d[val != VALID] = 0.0
+    return d.astype(np.float32), val
+
+
+def bg_train(mean, var, rgb, first, rho=0.02, var_floor=4.0):
+    """depthproc.bg_train (depthproc.py:121-136), in place on mean/var."""
+    x = rgb.astype(np.float64)
+    if first:
+        mean[:] = x
+        var[:] = var_floor
+    else:
+        mean[:] = (1.0 - rho) * mean + rho * x
+        var[:] = np.maximum((1.0 - rho) * var + rho * (x - mean) ** 2, var_floor)
+
+
+def classify_fg(mean, var, rgb, threshold=3.5):
+    """depthproc.classify_fg (depthproc.py:139-149)."""
+    x = rgb.astype(np.float64)
+    return np.sum((x - mean) ** 2 / var, axis=-1) > threshold ** 2
+
+
+def remove_bg_depth(depth, validity, fg_mask):
+    """depthproc.remove_bg_depth (depthproc.py:152-164)."""
+    val = validity.copy()
+    d = depth.copy()
+    bg = ~np.asarray(fg_mask, dtype=bool)
+    val[bg] = BACKGROUND
+    d[bg] = 0.0
+    return d, val

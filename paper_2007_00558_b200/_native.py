@@ -33,6 +33,8 @@ EXPORTS = (
     "fvv_mix_layer", "fvv_composite", "fvv_slot_set_camera", "fvv_slot_set_bg",
     "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slot_ingest_yuv", "fvv_render_views",
     "fvv_profile_enable", "fvv_profile_read", "fvv_selftest_division",
+    "fvv_correct_depth", "fvv_bg_train", "fvv_classify_fg", "fvv_remove_bg_depth",
+    "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -94,6 +96,14 @@ _SIGS = {
     "fvv_profile_enable": ([_VP, _I32], C.c_int),
     "fvv_selftest_division": ([_VP, C.c_int64, C.c_uint64, _I32, _VP], C.c_int),
     "fvv_profile_read": ([_VP, _I32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+    "fvv_correct_depth": ([_VP, _VP, _VP, _I32, _I32, _D, _D, _VP, _VP], C.c_int),
+    "fvv_bg_train": ([_VP, _VP, _I32, _I32, _VP, _VP, _I32, _D, _D], C.c_int),
+    "fvv_classify_fg": ([_VP, _VP, _VP, _VP, _I32, _I32, _D, _VP], C.c_int),
+    "fvv_remove_bg_depth": ([_VP, _VP, _VP, _VP, _I32, _I32, _VP, _VP], C.c_int),
+    "fvv_quantize12": ([_VP, _VP, _VP, _I32, _I32, _D, _D, _VP], C.c_int),
+    "fvv_pack_yuv420": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP], C.c_int),
+    "fvv_capture_encode": ([_VP, _VP, _VP, _VP, _I32, _I32, _I32, _D, _D, _VP, _VP, _D, _D, _D,
+                            _VP, _VP, _VP, _VP], C.c_int),
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
                          C.c_int),

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "fvv_capture.cuh"
 #include "fvv_kernels.cuh"
 
 using namespace fvv;
@@ -473,6 +474,129 @@ int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *v
     p.n_holes = n_holes_dev;
     if (n_holes_dev) CK(cudaMemsetAsync(n_holes_dev, 0, sizeof(int32_t), ctx->stream));
     LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
+    return FVV_OK;
+}
+
+static QuantParams quant_params(double zn, double zf) {
+    QuantParams q;
+    q.zn = zn;
+    q.zf = zf;
+    q.lo = zn * (1.0 - 0.01);  // depthcodec.py:101-102 (GUARD_BAND = 0.01)
+    q.hi = zf * (1.0 + 0.01);
+    q.inv_zf = 1.0 / zf;
+    q.inv_span = 1.0 / zn - 1.0 / zf;
+    return q;
+}
+
+#define NEED(cond, msg) \
+    do {                \
+        if (!(cond)) return fail(ctx, FVV_EINVAL, "%s", msg); \
+    } while (0)
+
+int fvv_correct_depth(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                      int32_t height, double alpha, double beta, float *depth_out,
+                      uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && depth && validity && depth_out && validity_out,
+         "correct_depth: bad arguments");
+    NEED(std::isfinite(alpha) && std::isfinite(beta), "correction model parameters must be finite");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_correct_depth(depth, validity, (size_t)width * height, alpha, beta,
+                                               depth_out, validity_out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_bg_train(fvv_ctx *ctx, const uint8_t *rgb, int32_t width, int32_t height, double *mean,
+                 double *var, int32_t first, double learning_rate, double var_floor) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && rgb && mean && var, "bg_train: bad arguments");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_bg_train(rgb, (size_t)width * height, mean, var, first != 0,
+                                          learning_rate, var_floor, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_classify_fg(fvv_ctx *ctx, const uint8_t *rgb, const double *mean, const double *var,
+                    int32_t width, int32_t height, double threshold, uint8_t *fg_mask_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && rgb && mean && var && fg_mask_out,
+         "classify_fg: bad arguments");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_classify_fg(rgb, mean, var, (size_t)width * height,
+                                             threshold * threshold, fg_mask_out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_remove_bg_depth(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                        const uint8_t *fg_mask, int32_t width, int32_t height, float *depth_out,
+                        uint8_t *validity_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && depth && validity && fg_mask && depth_out && validity_out,
+         "remove_bg_depth: bad arguments");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_remove_bg(depth, validity, fg_mask, (size_t)width * height,
+                                           depth_out, validity_out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_quantize12(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                   int32_t height, double z_near, double z_far, uint16_t *codes_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && depth && validity && codes_out, "quantize12: bad arguments");
+    NEED(0 < z_near && z_near < z_far, "need 0 < z_near < z_far");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_quantize12(depth, validity, (size_t)width * height,
+                                            quant_params(z_near, z_far), codes_out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_pack_yuv420(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t height,
+                    uint8_t *y_out, uint8_t *u_out, uint8_t *v_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && codes && y_out && u_out && v_out, "pack_yuv420: bad arguments");
+    NEED(width % 2 == 0 && height % 2 == 0, "disparity map dimensions must be even");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_pack_yuv420(codes, width, height, y_out, u_out, v_out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_capture_encode(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
+                       const uint8_t *rgb, int32_t width, int32_t height, int32_t do_correct,
+                       double alpha, double beta, const double *bg_mean, const double *bg_var,
+                       double threshold, double z_near, double z_far, uint8_t *y_out,
+                       uint8_t *u_out, uint8_t *v_out, uint16_t *codes_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && depth && validity && y_out && u_out && v_out,
+         "capture_encode: bad arguments");
+    NEED(width % 2 == 0 && height % 2 == 0, "YUV420 dimensions must be even");
+    NEED(0 < z_near && z_near < z_far, "need 0 < z_near < z_far");
+    NEED(!bg_mean || (bg_var && rgb), "BG removal needs the colour frame and model variance");
+    if (!width || !height) return FVV_OK;
+    CaptureParams p{};
+    p.W = width;
+    p.H = height;
+    p.depth = depth;
+    p.validity = validity;
+    p.rgb = rgb;
+    p.correct = do_correct != 0;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.bg_mean = bg_mean;
+    p.bg_var = bg_var;
+    p.tau2 = threshold * threshold;
+    p.quant = quant_params(z_near, z_far);
+    p.y = y_out;
+    p.u = u_out;
+    p.v = v_out;
+    p.codes_out = codes_out;
+    LAUNCH_K(FVV_K_OTHER, launch_capture_encode(p, ctx->stream));
     return FVV_OK;
 }
 

@@ -5,9 +5,10 @@
 * ``decode_yuv420_depth`` -> both fused in one pass (kernel K0, the form the
   edge server runs, pipeline.py:469-472).
 
-The encoder (``quantize12``/``pack_yuv420``) and the MED+Rice entropy coder
-belong to the capture server / wire format and are not provided here
-(SURVEY.md §8f ranks them "next").
+The encoder half (``quantize12`` / ``pack_yuv420`` and the fused
+``capture_encode`` of the capture server's per-frame chain) is provided as
+SURVEY.md §8f's rank-1 widening. The MED+Rice entropy coder (a sequential
+bitstream) is not.
 """
 
 from __future__ import annotations
@@ -108,3 +109,66 @@ def decode_yuv420_depth(img: Yuv420Image, range_: DepthRange, timestamp_us: int 
     H, W = img.y.shape
     d, val, _ = _decode(img, range_)
     return DepthFrame(W, H, _dev.host(d), _dev.host(val), timestamp_us)
+
+
+# ---------------------------------------------------------------------------
+# encoder half: depthcodec.py:83-110, 180-193
+
+
+def quantize12(depth, range_: DepthRange) -> DisparityMap12:
+    """Metric depth -> 12-bit codes: 0 Background, 1 Invalid/out of band (depthcodec.py:83-110)."""
+    ctx = _native.context()
+    W, H = int(depth.width), int(depth.height)
+    d = _dev.upload(depth.depth, np.float32)
+    v = _dev.upload(depth.validity, np.uint8)
+    codes = _dev.empty((H, W), np.uint16)
+    ctx.call("fvv_quantize12", d.data_ptr(), v.data_ptr(), W, H, float(range_.z_near),
+             float(range_.z_far), codes.data_ptr())
+    return DisparityMap12(W, H, _dev.host(codes, np.uint16))
+
+
+def pack_yuv420(d: DisparityMap12) -> Yuv420Image:
+    """LSB fold + MSB nibble interleave into YUV420 (depthcodec.py:180-193)."""
+    if d.width % 2 or d.height % 2:
+        raise ValueError("disparity map dimensions must be even")
+    ctx = _native.context()
+    c = _dev.upload(d.values, np.uint16)
+    y = _dev.empty((d.height, d.width), np.uint8)
+    u = _dev.empty((d.height // 2, d.width // 2), np.uint8)
+    v = _dev.empty((d.height // 2, d.width // 2), np.uint8)
+    ctx.call("fvv_pack_yuv420", c.data_ptr(), d.width, d.height, y.data_ptr(), u.data_ptr(),
+             v.data_ptr())
+    return Yuv420Image(_dev.host(y), _dev.host(u), _dev.host(v))
+
+
+def capture_encode(depth, color, range_: DepthRange, correction=None, bg_model=None):
+    """CaptureServer.capture's chain (pipeline.py:384-397) in one kernel:
+    correct_depth -> classify_fg -> remove_bg_depth -> quantize12 -> pack_yuv420.
+
+    Returns (Yuv420Image, DisparityMap12)."""
+    ctx = _native.context()
+    W, H = int(depth.width), int(depth.height)
+    if W % 2 or H % 2:
+        raise ValueError("YUV420 dimensions must be even")
+    d = _dev.upload(depth.depth, np.float32)
+    v = _dev.upload(depth.validity, np.uint8)
+    rgb = _dev.upload(color.pixels, np.uint8) if color is not None else None
+    if bg_model is not None and not bg_model.trained:
+        from .depthproc import UntrainedModelError
+        raise UntrainedModelError("BG model warm-up incomplete")
+    mean = _dev.upload(bg_model.mean, np.float64) if bg_model is not None else None
+    var = _dev.upload(bg_model.var, np.float64) if bg_model is not None else None
+    y = _dev.empty((H, W), np.uint8)
+    u = _dev.empty((H // 2, W // 2), np.uint8)
+    vv = _dev.empty((H // 2, W // 2), np.uint8)
+    codes = _dev.empty((H, W), np.uint16)
+    ctx.call("fvv_capture_encode", d.data_ptr(), v.data_ptr(), _dev.ptr(rgb), W, H,
+             int(correction is not None),
+             float(correction.alpha) if correction is not None else 0.0,
+             float(correction.beta) if correction is not None else 0.0,
+             _dev.ptr(mean), _dev.ptr(var),
+             float(bg_model.threshold) if bg_model is not None else 0.0,
+             float(range_.z_near), float(range_.z_far), y.data_ptr(), u.data_ptr(),
+             vv.data_ptr(), codes.data_ptr())
+    return (Yuv420Image(_dev.host(y), _dev.host(u), _dev.host(vv)),
+            DisparityMap12(W, H, _dev.host(codes, np.uint16)))

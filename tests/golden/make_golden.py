@@ -195,7 +195,40 @@ def codec_case():
     print("codec ok")
 
 
+def capture_case():
+    """CaptureServer chain (pipeline.py:384-397) on a generated frame."""
+    wl = workload("c1", 8, 2007)
+    c = wl.frames[0][wl.refs[0][0]]
+    H, W = c.mm.shape
+    rng = np.random.default_rng(77)
+    # a degraded all-Valid depth (FG + BG surfaces), like degrade_depth's output
+    d = np.where(c.mm > 0, c.mm.astype(np.float32) / 1000.0,
+                 np.where(c.bg_validity == 0, c.bg_depth, 0.0)).astype(np.float32)
+    val = np.where(d > 0, 0, 1).astype(np.uint8)
+    depth = rc.DepthFrame(W, H, d, val)
+    corrected = rproc.correct_depth(depth, rproc.CorrectionModel(-0.004, 1.01))
+    model = rproc.GaussianBgModel(width=W, height=H, warmup_frames=6)
+    train = []
+    for i in range(6):
+        px = np.clip(c.rgb.astype(np.int16) + rng.integers(-6, 7, c.rgb.shape), 0, 255)
+        train.append(px.astype(np.uint8))
+        rproc.bg_train(model, rc.ColorFrame(W, H, train[-1]))
+    live = c.rgb.copy()
+    live[H // 3: H // 2, W // 3: W // 2] = (250, 20, 40)   # a foreground blob
+    fg = rproc.classify_fg(model, rc.ColorFrame(W, H, live))
+    stripped = rproc.remove_bg_depth(corrected, fg)
+    codes = rcodec.quantize12(stripped, rc.DepthRange(0.5, 6.5))
+    img = rcodec.pack_yuv420(codes)
+    np.savez_compressed(OUT / "capture.npz", depth=d, validity=val, train=np.stack(train),
+                        live=live, alpha=-0.004, beta=1.01, cor_depth=corrected.depth,
+                        cor_validity=corrected.validity, mean=model.mean, var=model.var,
+                        fg=fg, rm_depth=stripped.depth, rm_validity=stripped.validity,
+                        codes=codes.values, y=img.y, u=img.u, v=img.v)
+    print("capture ok: fg", int(fg.sum()), "codes", np.bincount(codes.values.ravel() > 1))
+
+
 if __name__ == "__main__":
+    capture_case()
     for args in SYN_CASES:
         syn_case(*args)
     refscene_case("identity_simple", "simple", 4, [4], 1.0, quality=True)
