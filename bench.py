@@ -340,9 +340,7 @@ def run_ours(args):
             # tensor replicates it over NVLink (the path's only exchange)
             D.broadcast_frame([t for cid in cams for t in fr[cid]])
         need = sorted({c for v in vi for c in wl.refs[v]})
-        for cid in need:
-            rgb, mm, val = fr[cid]
-            eng.ingest_mm(cid, rgb, mm, val, hole_closing=True)
+        eng.ingest_mm_many({cid: fr[cid] for cid in need}, hole_closing=True)
         eng.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=out)
         return len(vi)
 
@@ -423,9 +421,7 @@ def run_ours(args):
                 up = uploader_for(s)
                 fr = up.get(ticket)
                 vi = step_views(s)
-                for cid in step_cams(s):
-                    rgb, mm, val = fr[cid]
-                    eng.ingest_mm(cid, rgb, mm, val, hole_closing=True)
+                eng.ingest_mm_many({cid: fr[cid] for cid in step_cams(s)}, hole_closing=True)
                 eng.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=out)
                 up.release(ticket)
                 dl.put(out[:len(vi)])
@@ -454,8 +450,8 @@ def run_ours(args):
         e2e = {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
                "h2d_bytes_per_step": (b1 - b0) // args.steps,
                "d2h_bytes_per_step": (dl.bytes - d0) // args.steps,
-               "api": "FrameUploader (pinned H2D, copy stream) -> EdgeRenderer.ingest_mm + "
-                      "render (C ABI fvv_slot_ingest_mm, fvv_render_views) -> "
+               "api": "FrameUploader (pinned H2D, copy stream) -> EdgeRenderer.ingest_mm_many + "
+                      "render (C ABI fvv_slots_ingest_mm, fvv_render_views) -> "
                       "ResultDownloader (D2H, copy stream), double-buffered",
                "ms_per_step": ms2 / args.steps}
         del ups_all

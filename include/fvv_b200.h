@@ -221,6 +221,12 @@ int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float 
 int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint16_t *mm,
                        const uint8_t *validity, int32_t hole_closing, float *depth_out,
                        uint8_t *validity_out);
+/* Several slots' live frames from mm rasters in ONE launch (one CTA grid
+ * layer per camera): the form a render tick uses for its reference cameras.
+ * rgb / mm / validity are host arrays of n device pointers. */
+int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
+                        const uint8_t *const *rgb, const uint16_t *const *mm,
+                        const uint8_t *const *validity, int32_t hole_closing);
 /* Live frame from the 12-bit YUV420 depth raster (pipeline.py:469-472). */
 int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
                         const uint8_t *u, const uint8_t *v, double z_near, double z_far,

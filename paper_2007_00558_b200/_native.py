@@ -34,7 +34,7 @@ EXPORTS = (
     "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slot_ingest_yuv", "fvv_render_views",
     "fvv_profile_enable", "fvv_profile_read", "fvv_selftest_division",
     "fvv_correct_depth", "fvv_bg_train", "fvv_classify_fg", "fvv_remove_bg_depth",
-    "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode",
+    "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode", "fvv_slots_ingest_mm",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -104,6 +104,8 @@ _SIGS = {
     "fvv_pack_yuv420": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP], C.c_int),
     "fvv_capture_encode": ([_VP, _VP, _VP, _VP, _I32, _I32, _I32, _D, _D, _VP, _VP, _D, _D, _D,
                             _VP, _VP, _VP, _VP], C.c_int),
+    "fvv_slots_ingest_mm": ([_VP, _I32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                             C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _I32], C.c_int),
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
                          C.c_int),

@@ -670,6 +670,41 @@ int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uin
     return FVV_OK;
 }
 
+int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
+                        const uint8_t *const *rgb, const uint16_t *const *mm,
+                        const uint8_t *const *validity, int32_t hole_closing) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 0 || n > FVV_MAX_REFS || (n && (!slots || !rgb || !mm)))
+        return fail(ctx, FVV_EINVAL, "slots_ingest_mm: bad arguments");
+    PreprocBatch b{};
+    if (hole_closing) {
+        PreprocParams tmp{};
+        bilateral_params(tmp, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
+        b.bil = static_cast<const BilateralParams &>(tmp);
+    }
+    b.n = n;
+    for (int i = 0; i < n; ++i) {
+        const int sl = slots[i];
+        if (sl < 0 || sl >= FVV_MAX_SLOTS || !ctx->slots[sl].has_cam)
+            return fail(ctx, FVV_EINVAL, "slot %d has no camera", sl);
+        if (!rgb[i] || !mm[i]) return fail(ctx, FVV_EINVAL, "slots_ingest_mm: NULL buffer");
+        Slot &s = ctx->slots[sl];
+        PreprocCore &c = b.cam[i];
+        c.W = s.cam.width;
+        c.H = s.cam.height;
+        c.src = kSrcMM;
+        c.mm = mm[i];
+        c.validity = validity ? validity[i] : nullptr;
+        c.rgb = rgb[i];
+        c.texel = s.texel;
+        c.warp_depth = s.fgd;
+    }
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess_batch(b, ctx->stream));
+    for (int i = 0; i < n; ++i) ctx->slots[slots[i]].has_frame = true;
+    return FVV_OK;
+}
+
 int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
                         const uint8_t *u, const uint8_t *v, double z_near, double z_far,
                         int32_t hole_closing, float *depth_out, uint8_t *validity_out) {

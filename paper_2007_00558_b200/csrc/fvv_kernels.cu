@@ -63,7 +63,7 @@ constexpr int PSC = PX + 2 * PMAXR, PSR = PY + 2 * PMAXR;
 // (depthcodec.py:154-177, 213-222): MSB nibble from U (even rows) or V (odd
 // rows), A = odd bit positions for even columns, B = even positions for odd
 // columns; LSB mirrored when the MSB is odd.
-__device__ __forceinline__ uint32_t yuv_code(const PreprocParams &p, int iy, int ix) {
+__device__ __forceinline__ uint32_t yuv_code(const PreprocCore &p, int iy, int ix) {
     const uint8_t *plane = (iy & 1) ? p.v : p.u;
     const uint32_t c = plane[(size_t)(iy >> 1) * (p.W >> 1) + (ix >> 1)];
     const uint32_t sh = (ix & 1) ? 0u : 1u;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void decode_mm(uint32_t mm, uint8_t &val, float &z) {
 }
 
 // depthcodec.dequantize12 / dequantize_codes (depthcodec.py:113-138)
-__device__ __forceinline__ void decode_code(const PreprocParams &p, uint32_t c, uint8_t &val,
+__device__ __forceinline__ void decode_code(const PreprocCore &p, uint32_t c, uint8_t &val,
                                             float &z) {
     if (c < 2) {
         val = (c == 0) ? (uint8_t)FVV_BACKGROUND : (uint8_t)FVV_INVALID;
@@ -105,7 +105,7 @@ __device__ __forceinline__ void decode_code(const PreprocParams &p, uint32_t c, 
 }
 
 // Decoded (depth, validity) of one pixel, per source format.
-__device__ __forceinline__ void load_depth(const PreprocParams &p, int iy, int ix, float &z,
+__device__ __forceinline__ void load_depth(const PreprocCore &p, int iy, int ix, float &z,
                                            uint8_t &val, uint32_t *code) {
     const size_t i = (size_t)iy * p.W + ix;
     if (p.src == kSrcMM) {
@@ -121,7 +121,7 @@ __device__ __forceinline__ void load_depth(const PreprocParams &p, int iy, int i
     }
 }
 
-__device__ __forceinline__ uchar4 load_rgb(const PreprocParams &p, size_t i) {
+__device__ __forceinline__ uchar4 load_rgb(const PreprocCore &p, size_t i) {
     if (!p.rgb) return make_uchar4(0, 0, 0, 0);
     const uint8_t *c = p.rgb + i * 3;
     return make_uchar4(c[0], c[1], c[2], 0);
@@ -132,7 +132,9 @@ __device__ __forceinline__ uchar4 load_rgb(const PreprocParams &p, size_t i) {
 // The 5x5 joint-bilateral fill (depthproc.py:171-224) only runs when the
 // tile holds an Invalid pixel: then the 2-px halo is staged in shared memory
 // (zero-padded like scenegen._shift2d: outside pixels are never Valid).
-__global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_constant__ PreprocParams p) {
+__global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_constant__ PreprocBatch batch) {
+    const PreprocCore &p = batch.cam[blockIdx.z];
+    const BilateralParams &bl = batch.bil;
     __shared__ float sz[PSR * PSC];
     __shared__ uint8_t sv[PSR * PSC];
     __shared__ uchar4 sg[PSR * PSC];
@@ -141,8 +143,9 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
 
     const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
+    if (x0 >= p.W || y0 >= p.H) return;  // batch grids cover the largest camera
     const int iy = y0 + ty, xb = x0 + lane * 4;
-    const int R = p.radius;
+    const int R = bl.radius;
     const int SC = PX + 2 * R;
     if (tid == 0) s_holes = 0;
 
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                         for (int dx = -R; dx <= R; ++dx)
                             cnt += sv[(ty + R + dy) * SC + x + R + dx] == FVV_VALID;
                 }
-                cand = cnt >= p.min_valid;
+                cand = cnt >= bl.min_valid;
                 if (!cand) s_fill[ty * PX + x] = -1.0f;
             }
             hm[q] = __ballot_sync(0xffffffffu, cand);
@@ -282,13 +285,13 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                         const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
                                      e2 = dsub(g2, (double)n.z);
                         const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-                        const double w = dmul(p.sw[dy + R][dx + R], exp(dmul(-d2, p.inv_2sr)));
+                        const double w = dmul(bl.sw[dy + R][dx + R], exp(dmul(-d2, bl.inv_2sr)));
                         num = dadd(num, dmul(w, (double)sz[ni]));
                         den = dadd(den, w);
                         ++cnt;
                     }
                 }
-                s_fill[lp] = (cnt >= p.min_valid && den > 0.0)
+                s_fill[lp] = (cnt >= bl.min_valid && den > 0.0)
                                  ? __double2float_rn(ddiv(num, den)) : -1.0f;
             }
         }
@@ -350,10 +353,24 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     }
 }
 
-cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
-    dim3 grid((p.W + PX - 1) / PX, (p.H + PY - 1) / PY);
-    k_preprocess<<<grid, 256, 0, s>>>(p);
+cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
+    if (b.n <= 0) return cudaSuccess;
+    int W = 0, H = 0;
+    for (int i = 0; i < b.n; ++i) {
+        W = b.cam[i].W > W ? b.cam[i].W : W;
+        H = b.cam[i].H > H ? b.cam[i].H : H;
+    }
+    dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
+    k_preprocess<<<grid, 256, 0, s>>>(b);
     return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
+    PreprocBatch b{};
+    b.bil = static_cast<const BilateralParams &>(p);
+    b.n = 1;
+    b.cam[0] = static_cast<const PreprocCore &>(p);
+    return launch_preprocess_batch(b, s);
 }
 
 // ---------------------------------------------------------------------------

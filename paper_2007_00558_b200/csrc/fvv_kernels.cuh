@@ -12,7 +12,8 @@ constexpr uint32_t kFlagLiveBackground = 2u;  // live validity == BACKGROUND -> 
 // Where a per-camera live depth comes from.
 enum DepthSource : int { kSrcF32 = 0, kSrcMM = 1, kSrcYUV = 2, kSrcCodes = 3 };
 
-struct PreprocParams {
+// Per-camera buffers of one preprocessing pass (K0 decode + K1 fill + ingest).
+struct PreprocCore {
     int W, H;
     int src;                 // DepthSource
     const float *depth;      // kSrcF32
@@ -20,13 +21,9 @@ struct PreprocParams {
     const uint16_t *mm;      // kSrcMM
     const uint8_t *y, *u, *v;// kSrcYUV
     const uint16_t *codes;   // kSrcCodes
-    double inv_span, inv_zf; // kSrcYUV: 1/zn - 1/zf, 1/zf (host-evaluated like numpy)
+    double inv_span, inv_zf; // kSrcYUV/Codes: 1/zn - 1/zf, 1/zf (host-evaluated like numpy)
     const uint8_t *rgb;      // guide / colour (H*W*3)
     const uint8_t *color_valid; // optional explicit colour-valid mask -> flag bit 0
-    // joint bilateral (depthproc.py:171-224); radius 0 disables
-    int radius, min_valid;
-    double sw[9][9];         // spatial weights math.exp(-(dy^2+dx^2)/(2 s^2)), host evaluated
-    double inv_2sr;          // 1/(2 sigma_range^2)
     // outputs (any may be null)
     uint32_t *texel;         // packed RGB + flags
     float *warp_depth;       // depth where Valid else 0
@@ -34,6 +31,22 @@ struct PreprocParams {
     uint8_t *validity_out;   // decoded / filled DepthFrame validity
     uint16_t *codes_out;     // kSrcYUV 12-bit codes
     int *n_holes;            // count of Invalid pixels before filling
+};
+
+// joint bilateral parameters (depthproc.py:171-224); radius 0 disables
+struct BilateralParams {
+    int radius, min_valid;
+    double sw[9][9];         // spatial weights math.exp(-(dy^2+dx^2)/(2 s^2)), host evaluated
+    double inv_2sr;          // 1/(2 sigma_range^2)
+};
+
+struct PreprocParams : PreprocCore, BilateralParams {};
+
+// several cameras in one launch (blockIdx.z = camera), same bilateral params
+struct PreprocBatch {
+    BilateralParams bil;
+    int n;
+    PreprocCore cam[FVV_MAX_REFS];
 };
 
 struct WarpContrib {
@@ -97,6 +110,7 @@ struct MixParams {
 
 // host launchers; return cudaGetLastError()
 cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s);
+cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s);
 cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s);
 cudaError_t launch_forward_warp(const WarpParams &p, long long max_src_pixels, cudaStream_t s);
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s);

@@ -87,6 +87,27 @@ class EdgeRenderer:
                       _dev.ptr(validity_out))
         self.ingested.add(cid)
 
+    def ingest_mm_many(self, frames: Mapping, hole_closing: bool = True) -> None:
+        """``{cam_id: (rgb, mm, validity)}`` in one fused launch (one grid layer
+        per camera) — the form a render tick uses for its reference cameras."""
+        self._bind()
+        items = list(frames.items())
+        n = len(items)
+        if n > _native.MAX_REFS:
+            for i in range(0, n, _native.MAX_REFS):
+                self.ingest_mm_many(dict(items[i:i + _native.MAX_REFS]), hole_closing)
+            return
+        keep = []
+        for cid, (rgb, mm, val) in items:
+            keep.append((_dev.upload(rgb, np.uint8), _dev.upload(mm, np.uint16),
+                         None if val is None else _dev.upload(val, np.uint8)))
+        arr = C.c_void_p * n
+        slots = (C.c_int32 * n)(*[self._slot(cid) for cid, _ in items])
+        vals = None if any(k[2] is None for k in keep) else arr(*[k[2].data_ptr() for k in keep])
+        self.ctx.call("fvv_slots_ingest_mm", n, slots, arr(*[k[0].data_ptr() for k in keep]),
+                      arr(*[k[1].data_ptr() for k in keep]), vals, int(bool(hole_closing)))
+        self.ingested.update(cid for cid, _ in items)
+
     def ingest_yuv(self, cid, rgb, y, u, v, depth_range, hole_closing: bool = True) -> None:
         """Live frame as the 12-bit YUV420 depth raster (pipeline.py:469-472)."""
         self._bind()

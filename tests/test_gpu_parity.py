@@ -219,3 +219,27 @@ def test_identity_view_reproduces_inputs(cuda):
     keep &= ~S.border_mask(out.height, out.width, 2)
     same = (out.pixels == inputs[rid].live_color.pixels).all(-1)
     assert same[keep].mean() >= 0.99
+
+
+def test_batched_ingest_equals_per_camera_ingest(cuda):
+    """fvv_slots_ingest_mm (one launch for all reference cameras) produces the
+    same slots, hence the same view, as one fvv_slot_ingest_mm per camera."""
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    wl = workload("c1", 4, 2007)
+    outs = []
+    for batched in (False, True):
+        r = EdgeRenderer(wl.rig)
+        frames = {}
+        for cid, c in wl.frames[0].items():
+            r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+            frames[cid] = (c.rgb, c.mm, c.validity)
+        if batched:
+            r.ingest_mm_many(frames)
+        else:
+            for cid, (rgb, mm, val) in frames.items():
+                r.ingest_mm(cid, rgb, mm, val)
+        outs.append(r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    o_rgb, _ = O.es_view(wl.virtuals[0], _es_frames(wl))
+    assert (outs[1] == o_rgb).all(-1).mean() >= 0.9999
