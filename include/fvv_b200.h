@@ -145,6 +145,14 @@ int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *v
                               int32_t min_valid_neighbors, float *depth_out,
                               uint8_t *validity_out, int32_t *n_holes_dev);
 
+/* K1's range factor np.exp(-color_d2 / (2 sigma_range^2)) (depthproc.py:
+ * 200, 211-212) has an exact integer argument color_d2 in [0, 3*255^2], so
+ * K1 reads it from a resident table of 3*255^2+1 doubles. This call installs
+ * the caller's table for sigma_range (the Python host passes the np.exp values
+ * the reference computes, which differ from libm's in the last bit on ~5 % of
+ * entries); without it the library builds the table with libm exp. */
+int fvv_set_range_weights(fvv_ctx *ctx, double sigma_range, const double *table, int32_t n);
+
 /* ---- K2+K3: one synthesized view (synthesis.synthesize_view, synthesis.py:331-362) */
 int fvv_synthesize_view(fvv_ctx *ctx, const fvv_camera *virt, const fvv_ref_frame *refs,
                         int32_t n_refs, const fvv_synth_cfg *cfg, uint8_t *rgb_out,

@@ -62,9 +62,14 @@ void fo_decode_mm(const uint16_t *mm, const uint8_t *val_in, int W, int H, float
     }
 }
 
-/* returns the number of Invalid input pixels */
+/* returns the number of Invalid input pixels. range_w (may be NULL = libm
+ * exp) holds exp(-d2 * inv_2sr) for every integer d2 in [0, 3*255^2]: the
+ * Python wrapper passes the np.exp values the reference computes
+ * (depthproc.py:212), since numpy's SIMD exp and libm's differ in the last bit
+ * on some arguments. */
 long fo_bilateral(const float *d, const uint8_t *v, const uint8_t *rgb, int W, int H, int R,
-                  double sigma_s, double sigma_r, int min_valid, float *out_d, uint8_t *out_v) {
+                  double sigma_s, double sigma_r, int min_valid, float *out_d, uint8_t *out_v,
+                  const double *range_w) {
     const long n = (long)W * H;
     memcpy(out_d, d, n * sizeof(float));
     memcpy(out_v, v, n);
@@ -93,7 +98,8 @@ long fo_bilateral(const float *d, const uint8_t *v, const uint8_t *rgb, int W, i
                     const double e0 = g0 - rgb[j * 3], e1 = g1 - rgb[j * 3 + 1],
                                  e2 = g2 - rgb[j * 3 + 2];
                     const double d2 = (e0 * e0 + e1 * e1) + e2 * e2;
-                    const double w = sw[dy + R][dx + R] * exp(-d2 * inv_2sr);
+                    const double w = sw[dy + R][dx + R] *
+                                     (range_w ? range_w[(long)d2] : exp(-d2 * inv_2sr));
                     num += w * (double)d[j];
                     den += w;
                     ++cnt;

@@ -45,7 +45,7 @@ def lib():
                                       C.c_void_p]
         _lib.fo_bilateral.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                       C.c_int, C.c_double, C.c_double, C.c_int, C.c_void_p,
-                                      C.c_void_p]
+                                      C.c_void_p, C.c_void_p]
         _lib.fo_bilateral.restype = C.c_long
         _lib.fo_synthesize_view.argtypes = [C.POINTER(_Cam), C.POINTER(_Ref), C.c_int,
                                             C.POINTER(_Cfg), C.c_void_p, C.c_void_p]
@@ -74,6 +74,20 @@ def decode_mm(mm, validity):
     return d, v
 
 
+_range_tables: dict = {}
+
+
+def _range_table(sigma_range):
+    """np.exp(-color_d2 * inv_2sr) over every integer color_d2 (depthproc.py:
+    200,212), so the C restatement uses numpy's exp like the reference."""
+    t = _range_tables.get(sigma_range)
+    if t is None:
+        inv_2sr = 1.0 / (2.0 * sigma_range ** 2)
+        t = _range_tables[sigma_range] = np.exp(-np.arange(3 * 255 * 255 + 1, dtype=np.float64)
+                                                * inv_2sr)
+    return t
+
+
 def bilateral_close_holes(depth, validity, rgb, radius=2, sigma_spatial=2.0, sigma_range=10.0,
                           min_valid_neighbors=6):
     depth = np.ascontiguousarray(depth, np.float32)
@@ -83,7 +97,8 @@ def bilateral_close_holes(depth, validity, rgb, radius=2, sigma_spatial=2.0, sig
     od = np.empty_like(depth)
     ov = np.empty_like(validity)
     lib().fo_bilateral(_p(depth), _p(validity), _p(rgb), W, H, radius, sigma_spatial,
-                       sigma_range, min_valid_neighbors, _p(od), _p(ov))
+                       sigma_range, min_valid_neighbors, _p(od), _p(ov),
+                       _p(_range_table(sigma_range)))
     return od, ov
 
 

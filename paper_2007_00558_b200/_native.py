@@ -35,6 +35,7 @@ EXPORTS = (
     "fvv_profile_enable", "fvv_profile_read", "fvv_selftest_division",
     "fvv_correct_depth", "fvv_bg_train", "fvv_classify_fg", "fvv_remove_bg_depth",
     "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode", "fvv_slots_ingest_mm",
+    "fvv_set_range_weights",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -106,6 +107,7 @@ _SIGS = {
                             _VP, _VP, _VP, _VP], C.c_int),
     "fvv_slots_ingest_mm": ([_VP, _I32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
                              C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _I32], C.c_int),
+    "fvv_set_range_weights": ([_VP, _D, C.POINTER(C.c_double), _I32], C.c_int),
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
                          C.c_int),
@@ -113,6 +115,25 @@ _SIGS = {
 
 _lib = None
 _lock = threading.Lock()
+
+# K1's range factor np.exp(-color_d2 * inv_2sr) (depthproc.py:200,211-212) takes
+# its argument from a finite integer set (d2 = sum of three squared u8
+# differences), so the host evaluates it once per sigma with the very np.exp
+# the reference calls, and the kernel reads the table. numpy's SIMD exp and
+# libm's differ in the last bit on ~5 % of these arguments.
+RANGE_TABLE_LEN = 3 * 255 * 255 + 1
+_DEFAULT_SIGMA_RANGE = 10.0  # depthproc.py:176
+# entry points that run K1 with the reference defaults when hole_closing != 0
+_DEFAULT_HOLE_CLOSING = frozenset((
+    "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slots_ingest_mm", "fvv_slot_ingest_yuv"))
+
+
+def range_weight_table(sigma_range: float) -> np.ndarray:
+    """np.exp(-color_d2 * inv_2sr) for color_d2 = 0 .. 3*255^2, in the
+    reference's own expression (depthproc.py:200,212)."""
+    inv_2sr = 1.0 / (2.0 * float(sigma_range) ** 2)
+    color_d2 = np.arange(RANGE_TABLE_LEN, dtype=np.float64)
+    return np.ascontiguousarray(np.exp(-color_d2 * inv_2sr))
 
 
 def load() -> C.CDLL:
@@ -169,6 +190,19 @@ class Context:
                                "(no CUDA device?)")
         self.h = h
         self.device = int(device)
+        self._range_sigma = None
+        self.range_weights(_DEFAULT_SIGMA_RANGE)
+
+    def range_weights(self, sigma_range: float) -> None:
+        """Make K1's resident range-weight table the np.exp one for sigma_range."""
+        sigma_range = float(sigma_range)
+        if self._range_sigma == sigma_range:
+            return
+        t = range_weight_table(sigma_range)
+        self.check(self.lib.fvv_set_range_weights(
+            self.h, sigma_range, t.ctypes.data_as(C.POINTER(C.c_double)), RANGE_TABLE_LEN),
+            "fvv_set_range_weights")
+        self._range_sigma = sigma_range
 
     def check(self, rc: int, what: str = "") -> None:
         if rc == FVV_OK:
@@ -179,6 +213,8 @@ class Context:
         raise RuntimeError(f"{what}: {msg}")
 
     def call(self, name: str, *args) -> None:
+        if name in _DEFAULT_HOLE_CLOSING:
+            self.range_weights(_DEFAULT_SIGMA_RANGE)
         self.check(getattr(self.lib, name)(self.h, *args), name)
 
     def set_stream(self, stream_handle: int) -> None:

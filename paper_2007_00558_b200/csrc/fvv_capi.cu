@@ -50,6 +50,9 @@ struct fvv_ctx {
     size_t canvas_cap = 0;  // keys allocated
     int cW = -1, cH = -1, cr = -1, cn = 0;
     int gen = -1;  // generation of the last view; -1 = canvases need a fill
+    // K1 range-weight table for range_sigma (kRangeTableLen doubles)
+    double *range_w = nullptr;
+    double range_sigma = -1.0;
     // per-kernel event timing (fvv_profile_enable)
     bool prof = false;
     struct Rec { int kid; cudaEvent_t a, b; };
@@ -175,16 +178,49 @@ PreprocParams base_pre(const Slot &s) {
     return p;
 }
 
-void bilateral_params(PreprocParams &p, int radius, double sigma_s, double sigma_r, int min_valid) {
-    // depthproc.py:199-200, 212: spatial factor via libm exp on the host
-    // (Python's math.exp is the same libm call), range factor on device.
+// Install the range-weight table exp(-d2 * inv_2sr), d2 = 0 .. 3*255^2, for
+// sigma_r. `host` (kRangeTableLen doubles) comes from the caller; NULL builds
+// it with libm exp. A table already resident for sigma_r is kept, so the
+// Python host's np.exp table (installed first) is never replaced by libm's.
+int range_table(fvv_ctx *ctx, double sigma_r, const double *host) {
+    if (!host && ctx->range_w && ctx->range_sigma == sigma_r) return FVV_OK;
+    if (!ctx->range_w) CK(cudaMalloc(&ctx->range_w, kRangeTableLen * sizeof(double)));
+    std::vector<double> t;
+    if (!host) {
+        // depthproc.py:200,212: inv_2sr = 1/(2 sr^2); w = exp(-d2 * inv_2sr)
+        const double inv_2sr = 1.0 / (2.0 * (sigma_r * sigma_r));
+        t.resize(kRangeTableLen);
+        for (int d = 0; d < kRangeTableLen; ++d) t[d] = std::exp(-(double)d * inv_2sr);
+        host = t.data();
+    }
+    // synchronous: the table is rebuilt only when sigma_range changes
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(ctx->range_w, host, kRangeTableLen * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->range_sigma = sigma_r;
+    return FVV_OK;
+}
+
+int bilateral_params(fvv_ctx *ctx, BilateralParams &p, int radius, double sigma_s, double sigma_r,
+                     int min_valid) {
+    // depthproc.py:199-200, 211-212: spatial factor via libm exp on the host
+    // (Python's math.exp is the same libm call); range factor from the table
     p.radius = radius;
     p.min_valid = min_valid;
     const double inv_2ss = 1.0 / (2.0 * (sigma_s * sigma_s));
-    p.inv_2sr = 1.0 / (2.0 * (sigma_r * sigma_r));
     for (int dy = -radius; dy <= radius; ++dy)
         for (int dx = -radius; dx <= radius; ++dx)
             p.sw[dy + radius][dx + radius] = std::exp((double)(-(dy * dy + dx * dx)) * inv_2ss);
+    if (radius > 0) {
+        int rc = range_table(ctx, sigma_r, nullptr);
+        if (rc) return rc;
+    }
+    p.range_w = ctx->range_w;
+    return FVV_OK;
+}
+
+// reference defaults, depthproc.py:174-177
+int bilateral_defaults(fvv_ctx *ctx, BilateralParams &p) {
+    return bilateral_params(ctx, p, 2, 2.0, 10.0, 6);
 }
 
 int canvas_pitch(int W, int r) { return (W + 2 * r + 2) & ~1; }  // even, >= W+2r+1
@@ -317,6 +353,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->slots) s.release();
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
+    cudaFree(ctx->range_w);
     for (auto &r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);
     delete ctx;
@@ -450,6 +487,16 @@ int fvv_dequantize12(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t
     return FVV_OK;
 }
 
+int fvv_set_range_weights(fvv_ctx *ctx, double sigma_range, const double *table, int32_t n) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!table || n != kRangeTableLen)
+        return fail(ctx, FVV_EINVAL, "range-weight table must hold %d doubles", kRangeTableLen);
+    if (!(sigma_range != 0.0 && std::isfinite(sigma_range)))
+        return fail(ctx, FVV_EINVAL, "sigma_range must be finite and non-zero");
+    return range_table(ctx, sigma_range, table);
+}
+
 int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *validity,
                               const uint8_t *rgb, int32_t width, int32_t height, int32_t radius,
                               double sigma_spatial, double sigma_range, int32_t min_valid,
@@ -468,7 +515,7 @@ int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *v
     p.depth = depth;
     p.validity = validity;
     p.rgb = rgb;
-    bilateral_params(p, radius, sigma_spatial, sigma_range, min_valid);
+    if ((rc = bilateral_params(ctx, p, radius, sigma_spatial, sigma_range, min_valid))) return rc;
     p.depth_out = depth_out;
     p.validity_out = validity_out;
     p.n_holes = n_holes_dev;
@@ -638,7 +685,7 @@ int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float 
     p.depth = depth;
     p.validity = validity;
     p.rgb = rgb;
-    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
+    if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
@@ -660,7 +707,7 @@ int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uin
     p.mm = mm;
     p.validity = validity;
     p.rgb = rgb;
-    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
+    if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     p.depth_out = depth_out;
@@ -678,11 +725,7 @@ int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
     if (n < 0 || n > FVV_MAX_REFS || (n && (!slots || !rgb || !mm)))
         return fail(ctx, FVV_EINVAL, "slots_ingest_mm: bad arguments");
     PreprocBatch b{};
-    if (hole_closing) {
-        PreprocParams tmp{};
-        bilateral_params(tmp, 2, 2.0, 10.0, 6);  // depthproc.py:174-177 defaults
-        b.bil = static_cast<const BilateralParams &>(tmp);
-    }
+    if (hole_closing && (rc = bilateral_defaults(ctx, b.bil))) return rc;
     b.n = n;
     for (int i = 0; i < n; ++i) {
         const int sl = slots[i];
@@ -721,7 +764,7 @@ int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const ui
     p.inv_span = 1.0 / z_near - 1.0 / z_far;
     p.inv_zf = 1.0 / z_far;
     p.rgb = rgb;
-    if (hole_closing) bilateral_params(p, 2, 2.0, 10.0, 6);
+    if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     p.depth_out = depth_out;

@@ -272,8 +272,10 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                 // depthproc.py:196-222: taps in dy-major order, centre skipped;
                 // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps;
                 // fill iff >= min_valid Valid taps and den > 0
+                // The colour distance is an exact integer (u8 channels), so the
+                // range factor np.exp(-d2 * inv_2sr) is one table read.
                 const uchar4 gc = sg[c0];
-                const double g0 = gc.x, g1 = gc.y, g2 = gc.z;
+                const int g0 = gc.x, g1 = gc.y, g2 = gc.z;
                 double num = 0.0, den = 0.0;
                 int cnt = 0;
                 for (int dy = -R; dy <= R; ++dy) {
@@ -282,10 +284,9 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                         const int ni = c0 + dy * SC + dx;
                         if (sv[ni] != FVV_VALID) continue;
                         const uchar4 n = sg[ni];
-                        const double e0 = dsub(g0, (double)n.x), e1 = dsub(g1, (double)n.y),
-                                     e2 = dsub(g2, (double)n.z);
-                        const double d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-                        const double w = dmul(bl.sw[dy + R][dx + R], exp(dmul(-d2, bl.inv_2sr)));
+                        const int e0 = g0 - n.x, e1 = g1 - n.y, e2 = g2 - n.z;
+                        const int d2 = e0 * e0 + e1 * e1 + e2 * e2;
+                        const double w = dmul(bl.sw[dy + R][dx + R], __ldg(bl.range_w + d2));
                         num = dadd(num, dmul(w, (double)sz[ni]));
                         den = dadd(den, w);
                         ++cnt;

@@ -37,8 +37,13 @@ struct PreprocCore {
 struct BilateralParams {
     int radius, min_valid;
     double sw[9][9];         // spatial weights math.exp(-(dy^2+dx^2)/(2 s^2)), host evaluated
-    double inv_2sr;          // 1/(2 sigma_range^2)
+    // range weights exp(-d2 / (2 sigma_range^2)) for every integer colour
+    // distance d2 in [0, 3*255^2], evaluated on the host by the same exp the
+    // reference calls (np.exp, installed by the Python host; libm otherwise)
+    const double *range_w;
 };
+
+constexpr int kRangeTableLen = 3 * 255 * 255 + 1;
 
 struct PreprocParams : PreprocCore, BilateralParams {};
 

@@ -45,6 +45,8 @@ def bilateral_close_holes(depth, guide, radius: int = 2, sigma_spatial: float = 
     out_d = _dev.empty((H, W), np.float32)
     out_v = _dev.empty((H, W), np.uint8)
     holes = _dev.zeros((1,), np.int32)
+    if int(radius) > 0:
+        ctx.range_weights(sigma_range)
     ctx.call("fvv_bilateral_close_holes", d.data_ptr(), v.data_ptr(), g.data_ptr(), W, H,
              int(radius), float(sigma_spatial), float(sigma_range), int(min_valid_neighbors),
              out_d.data_ptr(), out_v.data_ptr(), holes.data_ptr())

@@ -397,8 +397,16 @@ def test_bilateral_matches_oracle_on_random_holes(P, T):
     out = P.bilateral_close_holes(T.DepthFrame(W, H, d, v), T.ColorFrame(W, H, rgb))
     od, ov, _ = O.bilateral_close_holes(d, v, rgb)
     np.testing.assert_array_equal(out.validity, ov)
-    diff = np.abs(out.depth.astype(np.float64) - od)
-    assert (diff <= np.spacing(np.abs(od))).all()
+    np.testing.assert_array_equal(out.depth, od)
+    # a non-default sigma_range installs its own np.exp table; the default
+    # table comes back for the next default call
+    out5 = P.bilateral_close_holes(T.DepthFrame(W, H, d, v), T.ColorFrame(W, H, rgb),
+                                   sigma_range=5.0)
+    od5, ov5, _ = O.bilateral_close_holes(d, v, rgb, sigma_range=5.0)
+    np.testing.assert_array_equal(out5.validity, ov5)
+    np.testing.assert_array_equal(out5.depth, od5)
+    again = P.bilateral_close_holes(T.DepthFrame(W, H, d, v), T.ColorFrame(W, H, rgb))
+    np.testing.assert_array_equal(again.depth, od)
 
 
 # ---------------------------------------------------------------- engine

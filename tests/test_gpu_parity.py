@@ -120,14 +120,19 @@ def test_edge_server_preprocessing_vs_reference(cuda, name):
     np.testing.assert_array_equal(df.validity, g["dec_validity"])
     H, W = c.mm.shape
     out = P.bilateral_close_holes(df, ColorFrame(W, H, c.rgb))
-    # fill mask bit-exact; filled depth is an f64 exp-weighted mean cast to f32:
-    # equal to the reference's except where CUDA's and numpy's exp differ by an
-    # ulp and the f32 rounding flips (tolerance: 1 f32 ulp)
+    # K1 reads the range weights np.exp computes on this host, so it is
+    # bit-exact against the reference formula evaluated here (the numpy oracle)
+    od, ov, _ = O.bilateral_close_holes(df.depth, df.validity, c.rgb)
+    np.testing.assert_array_equal(out.validity, ov)
+    np.testing.assert_array_equal(out.depth, od)
     np.testing.assert_array_equal(out.validity, g["fill_validity"])
-    diff = np.abs(out.depth.astype(np.float64) - g["fill_depth"].astype(np.float64))
-    ulp = np.spacing(np.abs(g["fill_depth"])).astype(np.float64)
-    assert (diff <= ulp).all()
-    assert (diff == 0).mean() >= 0.999
+    if np.array_equal(od, g["fill_depth"]):
+        # this host's np.exp equals the golden generator's: bit-exact
+        np.testing.assert_array_equal(out.depth, g["fill_depth"])
+    else:
+        # another CPU's numpy SIMD exp may differ by an ulp (tolerance: 1 f32 ulp)
+        diff = np.abs(out.depth.astype(np.float64) - g["fill_depth"].astype(np.float64))
+        assert (diff <= np.spacing(np.abs(g["fill_depth"])).astype(np.float64)).all()
 
 
 def test_codec_decode_vs_reference(cuda):
@@ -178,12 +183,8 @@ def test_full_size_edge_server_path_vs_oracle(cuda, cfg_name, scale):
     r = _renderer(wl)
     img = r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy()
     o_rgb, _ = O.es_view(wl.virtuals[0], _es_frames(wl))
-    same = (img == o_rgb).all(-1)
-    # bilateral depths may differ by one f32 ulp (exp), which can move a
-    # handful of warped targets; everything else is bit-exact
-    assert same.mean() >= 0.9999, same.mean()
-    assert within_1lsb_frac(img, o_rgb) >= 0.999
-    assert psnr(img, o_rgb) >= 50.0
+    # K1 uses np.exp's range weights like the C oracle: bit-exact end to end
+    np.testing.assert_array_equal(img, o_rgb)
 
 
 def test_batch_equals_single_and_generation_rollover(cuda):
@@ -242,4 +243,4 @@ def test_batched_ingest_equals_per_camera_ingest(cuda):
         outs.append(r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
     o_rgb, _ = O.es_view(wl.virtuals[0], _es_frames(wl))
-    assert (outs[1] == o_rgb).all(-1).mean() >= 0.9999
+    np.testing.assert_array_equal(outs[1], o_rgb)
