@@ -50,6 +50,9 @@ struct fvv_ctx {
     size_t canvas_cap = 0;  // keys allocated
     int cW = -1, cH = -1, cr = -1, cn = 0;
     int gen = -1;  // generation of the last view; -1 = canvases need a fill
+    // per contribution: K2's exact z of every source pixel (zcap doubles each)
+    double *zsrc = nullptr;
+    size_t zcap = 0, zn = 0;
     // K1 range-weight table for range_sigma (kRangeTableLen doubles)
     double *range_w = nullptr;
     double range_sigma = -1.0;
@@ -253,6 +256,21 @@ int ensure_canvas(fvv_ctx *ctx, int n, int W, int H, int r) {
     return FVV_OK;
 }
 
+// n per-contribution z planes of `px` source pixels each (never cleared: K3
+// reads only the entries of this view's winners, which K2 just wrote)
+int ensure_zsrc(fvv_ctx *ctx, int n, size_t px) {
+    if (px > ctx->zcap || (size_t)n > ctx->zn) {
+        const size_t cap = px > ctx->zcap ? px : ctx->zcap;
+        const size_t nn = (size_t)n > ctx->zn ? (size_t)n : ctx->zn;
+        CK(cudaFree(ctx->zsrc));
+        ctx->zsrc = nullptr;
+        CK(cudaMalloc(&ctx->zsrc, cap * nn * sizeof(double)));
+        ctx->zcap = cap;
+        ctx->zn = nn;
+    }
+    return FVV_OK;
+}
+
 double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
     const double dx = a.C[0] - b.C[0], dy = a.C[1] - b.C[1], dz = a.C[2] - b.C[2];
     return 1.0 / (std::sqrt((dx * dx + dy * dy) + dz * dz) + eps);
@@ -291,6 +309,11 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     if (dbg) rp.dbg = *dbg;
     long long maxpx = 0;
     for (int j = 0; j < n; ++j) {
+        const long long np = (long long)refs[j]->cam.width * refs[j]->cam.height;
+        maxpx = np > maxpx ? np : maxpx;
+    }
+    if ((rc = ensure_zsrc(ctx, 2 * n, (size_t)maxpx))) return rc;
+    for (int j = 0; j < n; ++j) {
         const Slot &s = *refs[j];
         const double w = (weights && weights[j] > 0) ? weights[j]
                                                      : host_weight(s.cam, virt, cfg.mixing_epsilon);
@@ -299,13 +322,11 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         for (int L = 0; L < 2; ++L) {
             const int k = L * n + j;
             const float *d = L == 0 ? s.fgd : s.bgd;
-            wp.c[k] = WarpContrib{s.dev, d, rx, ry, cbase + per * k, b};
-            rp.c[k] = ResolveContrib{s.dev, s.texel, d, rx, ry, cbase + per * k, w, b,
-                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0,
-                                     1.0f / (float)s.cam.width};
+            double *zs = ctx->zsrc + ctx->zcap * k;
+            wp.c[k] = WarpContrib{s.dev, d, rx, ry, cbase + per * k, zs, b};
+            rp.c[k] = ResolveContrib{s.dev, s.texel, zs, cbase + per * k, w, b,
+                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
         }
-        const long long np = (long long)s.cam.width * s.cam.height;
-        maxpx = np > maxpx ? np : maxpx;
     }
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
@@ -353,6 +374,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->slots) s.release();
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
+    cudaFree(ctx->zsrc);
     cudaFree(ctx->range_w);
     for (auto &r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);
@@ -878,7 +900,8 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     wp.pitch = canvas_pitch(dst->width, r);
     wp.n = 1;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
-    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas + 1, b};
+    if ((rc = ensure_zsrc(ctx, 1, (size_t)src->width * src->height))) return rc;
+    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas + 1, ctx->zsrc, b};
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, (long long)src->width * src->height, ctx->stream));
     ResolveParams rp{};
     rp.dst = dd;
@@ -895,9 +918,9 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.dbg.contrib_valid = valid_out;
     rp.dbg.contrib_winner = winner_out;
     rp.dbg.contrib_stage = stage_out;
-    rp.c[0] = ResolveContrib{s.dev, s.texel, s.fgd, rx, ry, ctx->canvas + 1,
+    rp.c[0] = ResolveContrib{s.dev, s.texel, ctx->zsrc, ctx->canvas + 1,
                              host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
-                             layer_fg ? 1 : 0, 1.0f / (float)src->width};
+                             layer_fg ? 1 : 0};
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
     return FVV_OK;
 }

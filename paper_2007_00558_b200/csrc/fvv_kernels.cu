@@ -432,8 +432,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
     const int Wd = p.dst.W, Hd = p.dst.H, P = p.pitch;
     const double lo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
     const double ry = __ldg(c.ry + sv);
+    double zq[K2_PX];
+    unsigned stored = 0;
 #pragma unroll
     for (int q = 0; q < K2_PX; ++q) {
+        zq[q] = 0.0;
         if (!(d[q] > 0.0f)) continue;
         const int su = u0 + q;
         const double dd = (double)d[q];
@@ -451,13 +454,24 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
         }
         if (!(ur >= lo && ur < uhi && vr >= lo && vr < vhi)) continue;
         const size_t cell = (size_t)((int)vr + r) * P + (size_t)((int)ur + r);
-#ifdef FVV_EXP_K2_NOATOMIC
-        const unsigned long long kk = p.gen_hi | zkey(z, (uint32_t)(row + su), c.b);
-        if (kk == 0x1234ull) c.canvas[cell] = kk;
-#else
         atomicMin((unsigned long long *)(c.canvas + cell),
                   (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
-#endif
+        zq[q] = z;
+        stored |= 1u << q;
+    }
+    // the exact z of every scattering source, so K3 reads a winner's depth
+    // instead of re-deriving it: one 32-byte run per thread where all four
+    // pixels scattered (dense BG layers), single stores otherwise
+    if (c.zsrc && stored) {
+        double *o = c.zsrc + row + u0;
+        if (stored == 0xFu && (Ws & 1) == 0) {
+            reinterpret_cast<double2 *>(o)[0] = make_double2(zq[0], zq[1]);
+            reinterpret_cast<double2 *>(o)[1] = make_double2(zq[2], zq[3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < K2_PX; ++q)
+                if (stored & (1u << q)) o[q] = zq[q];
+        }
     }
 }
 
@@ -605,13 +619,9 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
                             }
                         }
                         if (w != kEmpty) {
-                            // exact f64 z of the winner, recomputed from its index
+                            // exact f64 z of the winner, as K2 computed it
                             const uint32_t idx = (uint32_t)(w & ((1ull << c.b) - 1));
-                            const int sv = (int)(idx / (uint32_t)c.src.W);
-                            const int su = (int)(idx - (uint32_t)sv * c.src.W);
-                            const double d = (double)__ldg(c.depth + idx);
-                            zq = transfer_z(c.src, dst, dmul(__ldg(c.rx + su), d),
-                                            dmul(__ldg(c.ry + sv), d), d);
+                            zq = __ldg(c.zsrc + idx);
                             wq = (int)idx;
                         }
                     }
@@ -805,15 +815,10 @@ __device__ __forceinline__ void stage_keys(uint64_t *dst, const uint64_t *canvas
     }
 }
 
-// exact f64 z of a winner index (same operations as K2, so bit-identical)
-__device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &dst,
+// exact f64 z of a winner index: the value K2 computed and stored for it
+__device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &,
                                            uint32_t idx) {
-    const int W = c.src.W;
-    int sv = (int)((float)idx * c.inv_w);
-    int su = (int)idx - sv * W;
-    if (su < 0) { --sv; su += W; } else if (su >= W) { ++sv; su -= W; }
-    const double d = (double)__ldg(c.depth + idx);
-    return transfer_z(c.src, dst, dmul(__ldg(c.rx + su), d), dmul(__ldg(c.ry + sv), d), d);
+    return __ldg(c.zsrc + idx);
 }
 
 __device__ __forceinline__ double key_z(const ResolveContrib &c, const DevCam &dst, uint64_t w) {

@@ -59,6 +59,9 @@ struct WarpContrib {
     const float *depth;      // > 0 marks a source pixel (Valid), else 0
     const double *rx, *ry;   // src ray slope tables (core.py:224-227)
     uint64_t *canvas;        // (Hd+2r) x (Wd+2r) keys
+    double *zsrc;            // [Hs*Ws] exact f64 target-camera z of every source
+                             // pixel that scattered a key (read back by K3 for
+                             // the winners); may be null
     int b;                   // index bits
 };
 
@@ -78,14 +81,12 @@ struct WarpParams {
 struct ResolveContrib {
     DevCam src;
     const uint32_t *texel;
-    const float *depth;
-    const double *rx, *ry;
+    const double *zsrc;      // K2's exact z per source pixel (WarpContrib::zsrc)
     const uint64_t *canvas;
     double weight;
     int b;
     uint32_t flag;           // texel flag bit that marks colour-valid source pixels
     int layer_fg;
-    float inv_w;             // 1.0f / src.W (index -> (u, v) split)
 };
 
 struct ResolveParams {
