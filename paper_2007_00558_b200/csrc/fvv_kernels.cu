@@ -991,7 +991,9 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
     double *sfg = sres + MAXR * 4 * NT;                          // [3][NT] merged FG colour
-    uint8_t *sst = reinterpret_cast<uint8_t *>(sfg + 3 * NT);    // [2][FCELLS] (DBG)
+    double *sbg = sfg + 3 * NT;                                  // [3][NT] merged BG colour
+    double *sray = sbg + 3 * NT;                                 // [TX] rx, [TY] ry
+    uint8_t *sst = reinterpret_cast<uint8_t *>(sray + TX + TY);  // [2][FCELLS] (DBG)
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const DevCam &dst = p.dst;
@@ -1005,9 +1007,10 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     const uint64_t gen = p.gen;
     const int ntot = p.n_fg + p.n_bg;
     const int nitems = ntot;
-    // virtual-camera ray of this pixel (pixel_rays, core.py:224-227)
-    const double rxd = ddiv(dsub((double)ix, dst.cx), dst.fx);
-    const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
+    // virtual-camera rays of the tile's columns and rows (pixel_rays,
+    // core.py:224-227), once per CTA
+    if (tid < TX) sray[tid] = ddiv(dsub((double)(x0 + tid), dst.cx), dst.fx);
+    else if (tid < TX + TY) sray[tid] = ddiv(dsub((double)(y0 + tid - TX), dst.cy), dst.fy);
 
     auto stage = [&](int q) {
         if (q < nitems) stage_keys(sk + (q % NBUF) * FKEYS, p.c[q].canvas, x0, y0, P, Hc, tid);
@@ -1020,7 +1023,6 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     __syncthreads();
     int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
-    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
     bool fv = false, bv = false;
     uint32_t vmask = 0;
 #pragma unroll 1
@@ -1067,7 +1069,7 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
 #ifdef FVV_EXP_NO_BACKWARD
             if (z < INFINITY) { ok = true; c0 = z; c1 = z; c2 = z; z = INFINITY; }
 #endif
-            if (z < INFINITY) ok = fetch(c, dst, rxd, ryd, z, c0, c1, c2);
+            if (z < INFINITY) ok = fetch(c, dst, sray[tx], sray[TX + ty], z, c0, c1, c2);
         }
         if (!ok) { c0 = c1 = c2 = 0.0; }
         const double zd = ok ? z : 0.0;
@@ -1125,7 +1127,10 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
                 sfg[2 * NT + tid] = m2;
                 fv = mv;
             } else {
-                b0 = m0; b1 = m1; b2 = m2; bv = mv;
+                sbg[tid] = m0;
+                sbg[NT + tid] = m1;
+                sbg[2 * NT + tid] = m2;
+                bv = mv;
             }
             vmask = 0;
             if (DBG && inimg) {
@@ -1143,7 +1148,7 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         if (k == ntot - 1 && inimg) {
             double o0, o1, o2;
             if (fv) { o0 = sfg[tid]; o1 = sfg[NT + tid]; o2 = sfg[2 * NT + tid]; }
-            else if (bv) { o0 = b0; o1 = b1; o2 = b2; }
+            else if (bv) { o0 = sbg[tid]; o1 = sbg[NT + tid]; o2 = sbg[2 * NT + tid]; }
             else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
             if (p.rgb_out) {
                 uint8_t *o = p.rgb_out + pix * 3;
@@ -1160,7 +1165,8 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
 template <int MAXR>
 static size_t fast_smem() {
     return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
-           (size_t)MAXR * 4 * NT * sizeof(double) + 3 * NT * sizeof(double) + 2 * FCELLS;
+           (size_t)MAXR * 4 * NT * sizeof(double) + (6 * NT + TX + TY) * sizeof(double) +
+           2 * FCELLS;
 }
 
 template <typename K>
