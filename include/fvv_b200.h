@@ -57,9 +57,18 @@ typedef struct fvv_synth_cfg {
     double mixing_epsilon;     /* synthesis.py:41 */
     double depth_band_rel;     /* synthesis.py:42 */
     uint8_t hole_color[3];     /* synthesis.py:43 */
-    uint8_t angular_weight;    /* extension (not in reference); must be 0 */
-    uint8_t inpaint;           /* extension (not in reference); must be 0 */
+    /* Extensions outside the reference. All 0 in
+     * parity mode, which is what the reference computes. */
+    uint8_t angular_weight;    /* 1: blend weight 1/(dist+eps) is multiplied per pixel
+                                  by 1/(theta + angular_epsilon), theta the angle at
+                                  the surface point between the reference and the
+                                  virtual camera rays */
+    uint8_t inpaint;           /* 1: K4 fills holes from the background side;
+                                  provenance 3 marks inpainted pixels */
     uint8_t reserved[3];
+    double angular_epsilon;    /* rad, > 0 (default 0.0175 = 1 degree) */
+    int32_t inpaint_radius;    /* max march distance in pixels, 1..4096 (default 64) */
+    int32_t reserved2;
 } fvv_synth_cfg;
 
 /* synthesis.CameraStreamInputs (synthesis.py:321-328), device pointers. */

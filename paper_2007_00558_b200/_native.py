@@ -24,6 +24,8 @@ LIB_PATH = Path(os.environ.get("FVV_B200_LIB") or Path(__file__).with_name("libf
 FVV_OK, FVV_EINVAL, FVV_ECUDA = 0, 1, 2
 MAX_REFS = 16
 MAX_SLOTS = 64
+ANGULAR_EPSILON = 0.017453292519943295  # 1 degree (extension default)
+INPAINT_RADIUS = 64                     # pixels (extension default)
 
 # every entry point declared in include/fvv_b200.h
 EXPORTS = (
@@ -51,7 +53,9 @@ class FvvSynthCfg(C.Structure):
     _fields_ = [("splat_radius", C.c_int32), ("crack_fill_window", C.c_int32),
                 ("mixing_epsilon", C.c_double), ("depth_band_rel", C.c_double),
                 ("hole_color", C.c_uint8 * 3), ("angular_weight", C.c_uint8),
-                ("inpaint", C.c_uint8), ("reserved", C.c_uint8 * 3)]
+                ("inpaint", C.c_uint8), ("reserved", C.c_uint8 * 3),
+                ("angular_epsilon", C.c_double), ("inpaint_radius", C.c_int32),
+                ("reserved2", C.c_int32)]
 
 
 class FvvRefFrame(C.Structure):
@@ -173,8 +177,11 @@ def synth_cfg(cfg) -> FvvSynthCfg:
     s.mixing_epsilon = float(cfg.mixing_epsilon)
     s.depth_band_rel = float(cfg.depth_band_rel)
     s.hole_color[:] = [int(x) for x in cfg.hole_color]
+    # extensions (absent from the reference's SynthesisConfig -> parity mode)
     s.angular_weight = int(bool(getattr(cfg, "angular_weight", False)))
     s.inpaint = int(bool(getattr(cfg, "inpaint", False)))
+    s.angular_epsilon = float(getattr(cfg, "angular_epsilon", ANGULAR_EPSILON))
+    s.inpaint_radius = int(getattr(cfg, "inpaint_radius", INPAINT_RADIUS))
     return s
 
 

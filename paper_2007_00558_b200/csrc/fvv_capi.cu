@@ -53,6 +53,11 @@ struct fvv_ctx {
     // per contribution: K2's exact z of every source pixel (zcap doubles each)
     double *zsrc = nullptr;
     size_t zcap = 0, zn = 0;
+    // inpainting scratch (provenance + composite depth) when the caller
+    // passes no provenance buffer
+    uint8_t *iprov = nullptr;
+    float *idepth = nullptr;
+    size_t icap = 0;
     // K1 range-weight table for range_sigma (kRangeTableLen doubles)
     double *range_w = nullptr;
     double range_sigma = -1.0;
@@ -136,9 +141,10 @@ int check_cfg(fvv_ctx *ctx, const fvv_synth_cfg *cfg) {
         return fail(ctx, FVV_EINVAL, "bad splat/crack parameters");
     if (cfg->splat_radius > 3 || cfg->crack_fill_window > 5)
         return fail(ctx, FVV_EINVAL, "splat_radius > 3 or crack_fill_window > 5 not supported");
-    if (cfg->angular_weight || cfg->inpaint)
-        return fail(ctx, FVV_EINVAL, "angular weighting / inpainting are extensions outside "
-                                     "the reference and are not enabled in this build");
+    if (cfg->angular_weight && !(cfg->angular_epsilon > 0 && std::isfinite(cfg->angular_epsilon)))
+        return fail(ctx, FVV_EINVAL, "angular_epsilon must be positive and finite");
+    if (cfg->inpaint && (cfg->inpaint_radius < 1 || cfg->inpaint_radius > 4096))
+        return fail(ctx, FVV_EINVAL, "inpaint_radius must be in [1, 4096]");
     return FVV_OK;
 }
 
@@ -328,8 +334,33 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
                                      L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
         }
     }
+    rp.ang = cfg.angular_weight ? 1 : 0;
+    rp.ang_eps = cfg.angular_epsilon;
+    InpaintParams ip{};
+    if (cfg.inpaint && rgb_out) {
+        const size_t px = (size_t)virt.width * virt.height;
+        if (px > ctx->icap) {
+            CK(cudaFree(ctx->iprov));
+            CK(cudaFree(ctx->idepth));
+            ctx->iprov = nullptr;
+            ctx->idepth = nullptr;
+            CK(cudaMalloc(&ctx->iprov, px));
+            CK(cudaMalloc(&ctx->idepth, px * sizeof(float)));
+            ctx->icap = px;
+        }
+        if (!rp.prov_out) rp.prov_out = ctx->iprov;
+        rp.depth_out = ctx->idepth;
+        ip.W = virt.width;
+        ip.H = virt.height;
+        ip.radius = cfg.inpaint_radius;
+        ip.bg_band = 0.05;
+        ip.rgb = rgb_out;
+        ip.prov = rp.prov_out;
+        ip.depth = ctx->idepth;
+    }
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
+    if (ip.rgb) LAUNCH(launch_inpaint(ip, ctx->stream));
     return FVV_OK;
 }
 
@@ -375,6 +406,8 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
+    cudaFree(ctx->iprov);
+    cudaFree(ctx->idepth);
     cudaFree(ctx->range_w);
     for (auto &r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);

@@ -498,7 +498,7 @@ constexpr int MAXRC = 2;  // window/2
 constexpr int KMAX = (TY + 2 * MAXH) * (TX + 2 * MAXH);
 constexpr int BMAX = (TY + 2 * MAXRC) * (TX + 2 * MAXRC);
 
-size_t resolve_smem_bytes(int maxr) { return (size_t)maxr * 4 * NT * sizeof(double); }
+size_t resolve_smem_bytes(int maxr) { return (size_t)maxr * 5 * NT * sizeof(double); }
 
 // Median of the valid (finite) ring values around `center` (np.nanmedian,
 // synthesis.py:123): odd count -> middle, even -> (lo + hi) / 2.
@@ -529,13 +529,31 @@ __device__ __forceinline__ double ring_median(const double *sz, int BC, int cent
     return (cnt & 1) ? lo : ddiv(dadd(lo, hi), 2.0);
 }
 
+// Extension (not in the reference): angular factor of a blend weight,
+// 1 / (theta + eps), theta = angle at the surface point X (the virtual pixel's
+// ray at depth z) between the rays to the reference and to the virtual camera
+// centres. Free-order f64: this path has no reference to match.
+__device__ __forceinline__ double angular_factor(const DevCam &dst, const DevCam &src, double rxd,
+                                                 double ryd, double z, double eps) {
+    const double px = rxd * z, py = ryd * z, pz = z;
+    const double wx = px * dst.R[0] + py * dst.R[3] + pz * dst.R[6] + dst.C[0];
+    const double wy = px * dst.R[1] + py * dst.R[4] + pz * dst.R[7] + dst.C[1];
+    const double wz = px * dst.R[2] + py * dst.R[5] + pz * dst.R[8] + dst.C[2];
+    const double ax = wx - src.C[0], ay = wy - src.C[1], az = wz - src.C[2];
+    const double bx = wx - dst.C[0], by = wy - dst.C[1], bz = wz - dst.C[2];
+    const double den = sqrt((ax * ax + ay * ay + az * az) * (bx * bx + by * by + bz * bz));
+    double cs = den > 0.0 ? (ax * bx + ay * by + az * bz) / den : 1.0;
+    cs = fmin(fmax(cs, -1.0), 1.0);
+    return 1.0 / (acos(cs) + eps);
+}
+
 template <int MAXR>
 __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ ResolveParams p) {
     __shared__ uint64_t sk[KMAX];
     __shared__ double sz[BMAX];
     __shared__ int swin[BMAX];
     __shared__ uint8_t sst[BMAX];
-    extern __shared__ double sres[];  // [MAXR][4][NT]: colour rgb, depth
+    extern __shared__ double sres[];  // [MAXR][5][NT]: colour rgb, depth, weight
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -555,6 +573,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
     const double ryd = ddiv(dsub((double)iy, dst.cy), dst.fy);
 
     double lc[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    double ld[2] = {0.0, 0.0};
     bool lv[2] = {false, false};
 
     for (int L = 0; L < 2; ++L) {
@@ -698,10 +717,13 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
             if (!ok) { c0 = c1 = c2 = 0.0; }
             const double zd = ok ? z : 0.0;
             if (j < MAXR) {
-                sres[(j * 4 + 0) * NT + tid] = c0;
-                sres[(j * 4 + 1) * NT + tid] = c1;
-                sres[(j * 4 + 2) * NT + tid] = c2;
-                sres[(j * 4 + 3) * NT + tid] = zd;
+                sres[(j * 5 + 0) * NT + tid] = c0;
+                sres[(j * 5 + 1) * NT + tid] = c1;
+                sres[(j * 5 + 2) * NT + tid] = c2;
+                sres[(j * 5 + 3) * NT + tid] = zd;
+                sres[(j * 5 + 4) * NT + tid] =
+                    (p.ang && ok) ? c.weight * angular_factor(dst, c.src, rxd, ryd, z, p.ang_eps)
+                                  : c.weight;
             }
             if (ok) vmask |= 1u << j;
             if (inimg) {
@@ -720,18 +742,18 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
         // -- mix_layer (synthesis.py:261-292)
         double zmin = INFINITY;
         for (int j = 0; j < n && j < MAXR; ++j) {
-            const double zj = sres[(j * 4 + 3) * NT + tid];
+            const double zj = sres[(j * 5 + 3) * NT + tid];
             if (((vmask >> j) & 1u) && zj < zmin) zmin = zj;
         }
         const double thr = dadd(zmin, dmul(p.band_rel, zmin));
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
         for (int j = 0; j < n && j < MAXR; ++j) {
-            const double zj = sres[(j * 4 + 3) * NT + tid];
+            const double zj = sres[(j * 5 + 3) * NT + tid];
             if (((vmask >> j) & 1u) && zj <= thr) {
-                const double w = p.c[k0 + j].weight;
-                a0 = dadd(a0, dmul(w, sres[(j * 4 + 0) * NT + tid]));
-                a1 = dadd(a1, dmul(w, sres[(j * 4 + 1) * NT + tid]));
-                a2 = dadd(a2, dmul(w, sres[(j * 4 + 2) * NT + tid]));
+                const double w = sres[(j * 5 + 4) * NT + tid];
+                a0 = dadd(a0, dmul(w, sres[(j * 5 + 0) * NT + tid]));
+                a1 = dadd(a1, dmul(w, sres[(j * 5 + 1) * NT + tid]));
+                a2 = dadd(a2, dmul(w, sres[(j * 5 + 2) * NT + tid]));
                 ad = dadd(ad, dmul(w, zj));
                 aw = dadd(aw, w);
             }
@@ -752,6 +774,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
             if (p.dbg.merged_depth) p.dbg.merged_depth[o] = lv[L] ? ddiv(ad, aw) : 0.0;
             if (p.dbg.merged_valid) p.dbg.merged_valid[o] = lv[L] ? 1 : 0;
         }
+        ld[L] = lv[L] ? ddiv(ad, aw) : 0.0;
     }
     // -- composite (synthesis.py:295-318): hole, then BG, then FG; rint, clip
     if (inimg) {
@@ -765,6 +788,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
             }
         }
         if (p.prov_out) p.prov_out[pix] = lv[0] ? 2 : (lv[1] ? 1 : 0);
+        if (p.depth_out) p.depth_out[pix] = (float)(src >= 0 ? ld[src] : 0.0);
     }
 }
 
@@ -984,16 +1008,17 @@ constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of
 // are in flight (cp.async groups) while the current one is shaded, and the
 // cells phase of contribution q+1 runs in the same barrier interval as the
 // per-pixel work of contribution q.
-template <int MAXR, bool DBG>
+template <int MAXR, bool DBG, bool ANG>
 __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
     uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
-    double *sfg = sres + MAXR * 4 * NT;                          // [3][NT] merged FG colour
-    double *sbg = sfg + 3 * NT;                                  // [3][NT] merged BG colour
-    double *sray = sbg + 3 * NT;                                 // [TX] rx, [TY] ry
-    uint8_t *sst = reinterpret_cast<uint8_t *>(sray + TX + TY);  // [2][FCELLS] (DBG)
+    double *sfg = sres + MAXR * 4 * NT;                          // [4][NT] merged FG colour, z
+    double *sbg = sfg + 4 * NT;                                  // [4][NT] merged BG colour, z
+    double *sray = sbg + 4 * NT;                                 // [TX] rx, [TY] ry
+    double *swt = sray + TX + TY;                                // [MAXR][NT] weights (ANG)
+    uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (ANG ? MAXR * NT : 0));  // [2][FCELLS] (DBG)
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const DevCam &dst = p.dst;
@@ -1077,6 +1102,10 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         sres[(j * 4 + 1) * NT + tid] = c1;
         sres[(j * 4 + 2) * NT + tid] = c2;
         sres[(j * 4 + 3) * NT + tid] = zd;
+        if (ANG)
+            swt[j * NT + tid] = ok ? c.weight * angular_factor(dst, c.src, sray[tx], sray[TX + ty],
+                                                               z, p.ang_eps)
+                                   : c.weight;
         if (ok) vmask |= 1u << j;
         if (DBG && inimg) {
             const size_t o = (size_t)k * plane + pix;
@@ -1105,11 +1134,11 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
             for (int qq = 0; qq < n; ++qq) {
                 const double zj = sres[(qq * 4 + 3) * NT + tid];
                 if (((vmask >> qq) & 1u) && zj <= thr) {
-                    const double w = p.c[kb + qq].weight;
+                    const double w = ANG ? swt[qq * NT + tid] : p.c[kb + qq].weight;
                     a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * NT + tid]));
                     a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * NT + tid]));
                     a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * NT + tid]));
-                    if (DBG) ad = dadd(ad, dmul(w, zj));
+                    if (DBG || p.depth_out) ad = dadd(ad, dmul(w, zj));
                     aw = dadd(aw, w);
                 }
             }
@@ -1121,17 +1150,13 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
                 m1 = div_rcp(a1, aw, ra);
                 m2 = div_rcp(a2, aw, ra);
             }
-            if (fgl) {
-                sfg[tid] = m0;
-                sfg[NT + tid] = m1;
-                sfg[2 * NT + tid] = m2;
-                fv = mv;
-            } else {
-                sbg[tid] = m0;
-                sbg[NT + tid] = m1;
-                sbg[2 * NT + tid] = m2;
-                bv = mv;
-            }
+            double *sl = fgl ? sfg : sbg;
+            sl[tid] = m0;
+            sl[NT + tid] = m1;
+            sl[2 * NT + tid] = m2;
+            if (p.depth_out) sl[3 * NT + tid] = mv ? ddiv(ad, aw) : 0.0;
+            if (fgl) fv = mv;
+            else bv = mv;
             vmask = 0;
             if (DBG && inimg) {
                 const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
@@ -1157,22 +1182,46 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
                 o[2] = (uint8_t)fmin(fmax(rint(o2), 0.0), 255.0);
             }
             if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
+            if (p.depth_out)
+                p.depth_out[pix] = (float)(fv ? sfg[3 * NT + tid] : (bv ? sbg[3 * NT + tid] : 0.0));
         }
     }
     cp_async_wait<0>();
-}
-
-template <int MAXR>
-static size_t fast_smem() {
-    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
-           (size_t)MAXR * 4 * NT * sizeof(double) + (6 * NT + TX + TY) * sizeof(double) +
-           2 * FCELLS;
 }
 
 template <typename K>
 static void raise_smem(K kernel, size_t bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
+
+template <int MAXR, bool ANG>
+static size_t fast_smem() {
+    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
+           (size_t)MAXR * 4 * NT * sizeof(double) + (8 * NT + TX + TY) * sizeof(double) +
+           (ANG ? (size_t)MAXR * NT * sizeof(double) : 0) + 2 * FCELLS;
+}
+
+template <int MAXR, bool DBG, bool ANG>
+static void launch_fast(const ResolveParams &p, dim3 grid, cudaStream_t s) {
+    static bool init = false;
+    if (!init) {
+        raise_smem(k_resolve_fast<MAXR, DBG, ANG>, fast_smem<MAXR, ANG>());
+        init = true;
+    }
+    k_resolve_fast<MAXR, DBG, ANG><<<grid, NT, fast_smem<MAXR, ANG>(), s>>>(p);
+}
+
+template <int MAXR>
+static void launch_fast_r(const ResolveParams &p, bool dbg, dim3 grid, cudaStream_t s) {
+    if (p.ang) {
+        if (dbg) launch_fast<MAXR, true, true>(p, grid, s);
+        else launch_fast<MAXR, false, true>(p, grid, s);
+    } else {
+        if (dbg) launch_fast<MAXR, true, false>(p, grid, s);
+        else launch_fast<MAXR, false, false>(p, grid, s);
+    }
+}
+
 
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     dim3 grid((p.dst.W + TX - 1) / TX, (p.dst.H + TY - 1) / TY);
@@ -1181,29 +1230,17 @@ cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
                      p.dbg.contrib_winner || p.dbg.contrib_stage || p.dbg.merged_color ||
                      p.dbg.merged_depth || p.dbg.merged_valid;
     if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0) {
-        static bool init = false;
-        if (!init) {
-            raise_smem(k_resolve_fast<3, false>, fast_smem<3>());
-            raise_smem(k_resolve_fast<3, true>, fast_smem<3>());
-            raise_smem(k_resolve_fast<4, false>, fast_smem<4>());
-            raise_smem(k_resolve_fast<4, true>, fast_smem<4>());
-            raise_smem(k_resolve_fast<FVV_MAX_REFS, false>, fast_smem<FVV_MAX_REFS>());
-            raise_smem(k_resolve_fast<FVV_MAX_REFS, true>, fast_smem<FVV_MAX_REFS>());
-            init = true;
-        }
-        if (maxn <= 3) {
-            if (dbg) k_resolve_fast<3, true><<<grid, NT, fast_smem<3>(), s>>>(p);
-            else k_resolve_fast<3, false><<<grid, NT, fast_smem<3>(), s>>>(p);
-        } else if (maxn <= 4) {
-            if (dbg) k_resolve_fast<4, true><<<grid, NT, fast_smem<4>(), s>>>(p);
-            else k_resolve_fast<4, false><<<grid, NT, fast_smem<4>(), s>>>(p);
-        } else {
-            if (dbg) k_resolve_fast<FVV_MAX_REFS, true><<<grid, NT, fast_smem<FVV_MAX_REFS>(), s>>>(p);
-            else k_resolve_fast<FVV_MAX_REFS, false><<<grid, NT, fast_smem<FVV_MAX_REFS>(), s>>>(p);
-        }
+        if (maxn <= 3) launch_fast_r<3>(p, dbg, grid, s);
+        else if (maxn <= 4) launch_fast_r<4>(p, dbg, grid, s);
+        else launch_fast_r<FVV_MAX_REFS>(p, dbg, grid, s);
         return cudaGetLastError();
     }
     if (maxn <= 4) {
+        static bool attr4 = false;
+        if (!attr4) {
+            raise_smem(k_resolve_generic<4>, resolve_smem_bytes(4));
+            attr4 = true;
+        }
         k_resolve_generic<4><<<grid, NT, resolve_smem_bytes(4), s>>>(p);
     } else {
         static bool attr_set = false;
@@ -1213,6 +1250,73 @@ cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
         }
         k_resolve_generic<FVV_MAX_REFS><<<grid, NT, resolve_smem_bytes(FVV_MAX_REFS), s>>>(p);
     }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K4 (extension, not in the reference: SPEC.md:548 leaves holes at hole_color)
+//
+// Background-biased disocclusion fill. A hole of a forward-warped view is
+// where the virtual camera sees past a foreground edge that no reference saw
+// behind, so the right colour is the background beside it. Each hole pixel
+// marches up to `radius` pixels in 8 directions to the first non-hole pixel,
+// keeps the candidates whose depth lies within bg_band of the farthest one,
+// and averages them with 1/distance weights. Filled pixels get provenance 3;
+// both 0 and 3 read as holes, so the result does not depend on the order in
+// which threads fill.
+
+__global__ void k_inpaint(const InpaintParams p) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= p.W || y >= p.H) return;
+    const size_t i = (size_t)y * p.W + x;
+    if (p.prov[i] != 0) return;
+    const int dxs[8] = {1, -1, 0, 0, 1, 1, -1, -1};
+    const int dys[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+    float cz[8], cd[8];
+    size_t ci[8];
+    int n = 0;
+    float zmax = 0.0f;
+    for (int d = 0; d < 8; ++d) {
+        int xx = x, yy = y;
+        for (int s = 1; s <= p.radius; ++s) {
+            xx += dxs[d];
+            yy += dys[d];
+            if (xx < 0 || xx >= p.W || yy < 0 || yy >= p.H) break;
+            const size_t j = (size_t)yy * p.W + xx;
+            const uint8_t pv = p.prov[j];
+            if (pv == 1 || pv == 2) {
+                const float z = p.depth[j];
+                cz[n] = z;
+                cd[n] = (dxs[d] && dys[d]) ? 1.41421356f * (float)s : (float)s;
+                ci[n] = j;
+                zmax = fmaxf(zmax, z);
+                ++n;
+                break;
+            }
+        }
+    }
+    if (n == 0) return;
+    const float zlo = zmax * (float)(1.0 - p.bg_band);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, aw = 0.f;
+    for (int k = 0; k < n; ++k) {
+        if (cz[k] < zlo) continue;
+        const float w = 1.0f / cd[k];
+        const uint8_t *c = p.rgb + ci[k] * 3;
+        a0 += w * c[0];
+        a1 += w * c[1];
+        a2 += w * c[2];
+        aw += w;
+    }
+    uint8_t *o = p.rgb + i * 3;
+    o[0] = (uint8_t)fminf(fmaxf(rintf(a0 / aw), 0.f), 255.f);
+    o[1] = (uint8_t)fminf(fmaxf(rintf(a1 / aw), 0.f), 255.f);
+    o[2] = (uint8_t)fminf(fmaxf(rintf(a2 / aw), 0.f), 255.f);
+    p.prov[i] = 3;
+}
+
+cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s) {
+    if (p.W <= 0 || p.H <= 0) return cudaSuccess;
+    k_inpaint<<<dim3((p.W + 127) / 128, p.H), 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -99,8 +99,23 @@ struct ResolveParams {
     double hole[3];
     uint8_t *rgb_out;        // H*W*3 (may be null)
     uint8_t *prov_out;       // H*W (may be null)
+    // extensions outside the reference (off in parity mode, fvv_synth_cfg):
+    int ang;                 // 1: per-pixel angular factor on the blend weights
+    double ang_eps;          // rad, factor = 1 / (theta + ang_eps)
+    float *depth_out;        // H*W composite depth (inpainting input; may be null)
     fvv_debug dbg;
     ResolveContrib c[2 * FVV_MAX_REFS];
+};
+
+// K4 (extension): background-biased disocclusion inpainting of the holes of
+// a composited view
+struct InpaintParams {
+    int W, H;
+    int radius;              // max march distance in pixels
+    double bg_band;          // candidates within (1 - bg_band) * z_max count as background
+    uint8_t *rgb;            // in/out: holes are filled in place
+    uint8_t *prov;           // in/out: 0 hole -> 3 inpainted
+    const float *depth;      // composite depth (0 at holes)
 };
 
 struct MixParams {
@@ -126,6 +141,7 @@ cudaError_t launch_composite(const double *fg_c, const uint8_t *fg_v, const doub
                              uint8_t *rgb, uint8_t *prov, cudaStream_t s);
 cudaError_t launch_selftest_div(long long n, uint64_t seed, int mode, unsigned long long *mism,
                                 cudaStream_t s);
+cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
 size_t resolve_smem_bytes(int maxr);
 

@@ -48,12 +48,27 @@ class SynthesisConfig:
     mixing_epsilon: float = 0.01
     depth_band_rel: float = 0.02
     hole_color: Tuple[int, int, int] = (0, 0, 0)
+    # Extensions outside the reference, off by
+    # default so the defaults compute exactly what the reference computes:
+    #   angular_weight: blend weight 1/(dist + eps) x 1/(theta + angular_epsilon)
+    #     per pixel, theta the angle at the surface point between the reference
+    #     and virtual camera rays;
+    #   inpaint: background-biased fill of disocclusion holes (kernel K4);
+    #     provenance 3 marks inpainted pixels.
+    angular_weight: bool = False
+    angular_epsilon: float = 0.017453292519943295
+    inpaint: bool = False
+    inpaint_radius: int = 64
 
     def __post_init__(self):
         if self.reference_count < 1:
             raise ValueError("reference count must be >= 1")
         if self.splat_radius < 0 or self.crack_fill_window < 1:
             raise ValueError("bad splat/crack parameters")
+        if self.angular_weight and not self.angular_epsilon > 0:
+            raise ValueError("angular_epsilon must be positive")
+        if self.inpaint and not 1 <= self.inpaint_radius <= 4096:
+            raise ValueError("inpaint_radius must be in [1, 4096]")
 
 
 @dataclass(frozen=True)

@@ -295,18 +295,24 @@ def test_debug_bundle_matches_plain_view(S):
     assert len(b.fg_contributions) == len(b.bg_contributions) == len(case.refs)
 
 
-def test_extensions_rejected_in_parity_build(S):
+def test_extension_parameters_validated(S):
     import ctypes as C
 
     from paper_2007_00558_b200 import _native
 
     case = refscene_case(golden("refscene_identity_simple.npz"))
-    cfg = _native.synth_cfg(S.SynthesisConfig())
-    cfg.inpaint = 1
     ctx = _native.context()
+    for field, bad in (("inpaint_radius", 0), ("angular_epsilon", 0.0)):
+        cfg = _native.synth_cfg(S.SynthesisConfig())
+        cfg.inpaint = cfg.angular_weight = 1
+        setattr(cfg, field, bad)
+        with pytest.raises(ValueError):
+            ctx.call("fvv_render_views", C.byref(_native.camera(case.virtual)), 1,
+                     (C.c_int32 * 1)(0), None, 1, C.byref(cfg), None, None)
     with pytest.raises(ValueError):
-        ctx.call("fvv_render_views", C.byref(_native.camera(case.virtual)), 1,
-                 (C.c_int32 * 1)(0), None, 1, C.byref(cfg), None, None)
+        S.SynthesisConfig(inpaint=True, inpaint_radius=0)
+    with pytest.raises(ValueError):
+        S.SynthesisConfig(angular_weight=True, angular_epsilon=-1.0)
 
 
 # ---------------------------------------------------------------- bilateral

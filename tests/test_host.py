@@ -190,7 +190,8 @@ def test_ctypes_struct_layout_matches_c(tmp_path):
     fields = {
         "fvv_camera": ("id", "width", "fx", "cy", "R", "C"),
         "fvv_synth_cfg": ("splat_radius", "crack_fill_window", "mixing_epsilon",
-                          "depth_band_rel", "hole_color", "angular_weight", "inpaint"),
+                          "depth_band_rel", "hole_color", "angular_weight", "inpaint",
+                          "angular_epsilon", "inpaint_radius"),
         "fvv_ref_frame": ("cam", "rgb", "live_depth", "live_validity", "bg_depth",
                           "bg_validity", "weight"),
         "fvv_debug": ("contrib_color", "contrib_stage", "merged_valid"),
