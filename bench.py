@@ -58,13 +58,23 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", default="c1", choices=("c0", "c1", "c2", "c3", "c4"))
-    ap.add_argument("--frames", type=int, default=4, help="pre-staged frames to rotate over")
+    ap.add_argument("--frames", type=int, default=None,
+                    help="pre-staged frames to rotate over (c3: frames of the stream, default "
+                         "300 as BASELINE.json's config; others: 4)")
     ap.add_argument("--views", type=int, default=None, help="views per step (c2/c4 batches)")
     ap.add_argument("--seed", type=int, default=2007)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--gen", default="auto", choices=("auto", "host", "gpu"),
+                    help="input generator: numpy ray caster on the host, or scenes_gpu in "
+                         "HBM (auto: gpu for c3/c4, whose host generation takes minutes)")
+    args = ap.parse_args()
+    if args.gen == "auto":
+        args.gen = "gpu" if args.config in ("c3", "c4") else "host"
+    if args.frames is None:
+        args.frames = 300 if args.config == "c3" else 4
+    return args
 
 
 # ----------------------------------------------------------------------------
@@ -73,6 +83,19 @@ def parse():
 
 def build_workload(args):
     name = args.config
+    if args.gen == "gpu":
+        import torch
+
+        from paper_2007_00558_b200 import scenes_gpu
+
+        dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+        if name == "c3":
+            ws = int(os.environ.get("WORLD_SIZE", 1))
+            return scenes_gpu.make_workload("c3", seed=args.seed, n_frames=max(args.frames, ws),
+                                            dev=dev)
+        return scenes_gpu.make_workload(name, seed=args.seed, n_views=args.views,
+                                        cameras="all" if name in ("c2", "c4") else "refs",
+                                        dev=dev)
     if name == "c1":
         wl = scenes.make_workload("c1", seed=args.seed)
     elif name == "c0":
@@ -85,11 +108,26 @@ def build_workload(args):
     return wl
 
 
+def host_array(a):
+    """numpy view of a capture raster (scenes_gpu keeps them as device tensors,
+    mm as the int16 bit pattern of uint16)."""
+    if isinstance(a, np.ndarray):
+        return a
+    return a.cpu().numpy()
+
+
+def host_capture(c):
+    return c.host() if hasattr(c, "host") else c
+
+
 def frame_variants(wl, n: int, seed: int):
     """``n`` distinct frames: frame 0 as captured, the others re-noised
     (depth noise N(0, (0.5% z)^2) in mm, fresh invalid pixels) so every step
-    reads different bytes."""
+    reads different bytes. Device-generated frames (scenes_gpu) are used as
+    they are: their per-step footprint already exceeds L2."""
     out = [wl.frames[0]]
+    if not isinstance(wl.frames[0][next(iter(wl.frames[0]))].rgb, np.ndarray):
+        return list(wl.frames[:max(n, 1)])
     rng = np.random.default_rng(seed)
     for f in range(1, n):
         if len(wl.frames) > f:
@@ -195,7 +233,7 @@ def _numpy_view(i):
 
 
 def oracle_jobs(wl, view=0):
-    caps = wl.frames[0]
+    caps = {cid: host_capture(c) for cid, c in wl.frames[0].items() if cid in wl.refs[view]}
     frames = [dict(calib=caps[r].calib, rgb=caps[r].rgb, mm=caps[r].mm, validity=caps[r].validity,
                    bg_depth=caps[r].bg_depth, bg_validity=caps[r].bg_validity)
               for r in wl.refs[view]]
@@ -285,16 +323,18 @@ def run_ours(args):
         threads = args.cpu_workers or os.cpu_count()
         walls = c_oracle_rounds(wl, threads, 3)
         wall = min(walls)
-        np_wall = numpy_oracle_round(wl, threads)
+        # the numpy oracle runs in a fork pool, which must not inherit a CUDA
+        # context (device-generated inputs create one): threads-only then
+        np_wall = numpy_oracle_round(wl, threads) if args.gen == "host" else None
         cpu = {"value": threads / wall, "unit": "views/s", "cores": threads, "kind": "port",
                "sample": f"{threads} views ({wl.description}, view 0), one per host thread, "
                          f"by the C oracle port es_view (mm decode + bilateral + synthesis); "
                          f"best of 3 rounds, {wall:.2f} s wall",
                "cpu": cpu_model(),
-               "numpy_port": {"value": threads / np_wall, "unit": "views/s",
-                              "sample": f"{threads} views by the numpy oracle (the reference's "
-                                        f"numpy formulation), one per process, "
-                                        f"{np_wall:.1f} s wall"}}
+               "numpy_port": None if np_wall is None else {
+                   "value": threads / np_wall, "unit": "views/s",
+                   "sample": f"{threads} views by the numpy oracle (the reference's numpy "
+                             f"formulation), one per process, {np_wall:.1f} s wall"}}
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -319,11 +359,15 @@ def run_ours(args):
                 bg_done.add(cid)
     # pre-stage every frame's live inputs in HBM (c2/c4 multi-GPU: only rank
     # 0's copy is meaningful, the others receive it by broadcast each step)
+    def on_dev(a):
+        if isinstance(a, np.ndarray):
+            return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).to(dev)
+        return a
+
     staged = []
     for fr in frames:
-        staged.append({cid: (torch.from_numpy(fr[cid].rgb).to(dev),
-                             torch.from_numpy(fr[cid].mm.view(np.int16)).to(dev),
-                             torch.from_numpy(fr[cid].validity).to(dev)) for cid in fr})
+        staged.append({cid: (on_dev(fr[cid].rgb), on_dev(fr[cid].mm), on_dev(fr[cid].validity))
+                       for cid in fr})
     k = wl.rig[0].intrinsics
     H, W = k.height, k.width
     vmax = max(len(v) for v in views)
@@ -385,15 +429,21 @@ def run_ours(args):
         from paper_2007_00558_b200.engine import FrameUploader, ResultDownloader
 
         def step_views(s):
-            return views[s % len(views)] if args.config == "c3" else views[0]
+            # c3: the e2e run cycles over the frames that have host copies
+            return views[s % len(host)] if args.config == "c3" else views[0]
 
         def step_cams(s):
             return sorted({c for v in step_views(s) for c in wl.refs[v]})
 
+        def pinned(a):
+            a = host_array(a)
+            return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory()
+
+        # at most 8 distinct host frames rotate (c3's 300 would pin 11 GB)
         host = []
-        for fr in frames:
-            host.append({cid: tuple(torch.from_numpy(a).pin_memory() for a in
-                                    (fr[cid].rgb, fr[cid].mm.view(np.int16), fr[cid].validity))
+        for fr in frames[:8]:
+            host.append({cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm,
+                                                        fr[cid].validity))
                          for cid in fr})
 
         def host_frame(s):

@@ -418,11 +418,8 @@ def _arc(n, radius, gap_deg, intr, first_id=0):
 CONFIGS = ("c0", "c1", "c2", "c3", "c4")
 
 
-def make_workload(name: str, seed: int = 2007, scale: int = 1, n_frames: Optional[int] = None,
-                  n_views: Optional[int] = None, cameras: str = "refs") -> Workload:
-    """Build config ``name`` (c0..c4). ``scale`` > 1 divides the resolution
-    (for CPU-sized parity cases); ``cameras='refs'`` renders only the cameras
-    some view references, ``'all'`` the whole rig."""
+def workload_params(name: str, seed: int = 2007) -> dict:
+    """Rig, scene and capture parameters of config ``name`` (c0..c4) at full size."""
     if name == "c0":
         w, h, f, n, radius, gap = 640, 360, 470.0, 2, 2.5, 15.0
         scene = make_scene(seed, 4, 3, (1.5, 4.0), (1.5, 3.0), (0.2, 0.5), radius,
@@ -440,21 +437,40 @@ def make_workload(name: str, seed: int = 2007, scale: int = 1, n_frames: Optiona
         if name == "c1":
             phis, nv, nf = [math.radians(5.0)], 1, 1
         elif name == "c2":
-            nv, nf = n_views or 64, 1
-            phis = None
+            nv, nf, phis = 64, 1, None
         else:
-            nf = n_frames or 300
-            nv = nf
-            phis = None
+            nv, nf, phis = 300, 300, None
     elif name == "c4":
         w, h, f, n, radius, gap = 3840, 2160, 2800.0, 16, 3.0, 8.0
         scene = make_scene(seed, 10, 40, (2.0, 8.0), (1.2, 6.0), (0.1, 0.45), radius,
                            ground_y=1.2, hspan=40, vspan=16)
         cap = dict(noise_rel=0.005, invalid_frac=0.05, invalid_mode="edges")
-        nv, nf, k = n_views or 32, 1, 4
+        nv, nf, k = 32, 1, 4
         phis = None
     else:
         raise ValueError(f"unknown config {name!r}; expected one of {CONFIGS}")
+    return dict(w=w, h=h, f=f, n=n, radius=radius, gap=gap, scene=scene, capture=cap, k=k,
+                n_views=nv, n_frames=nf, phis=phis)
+
+
+def make_workload(name: str, seed: int = 2007, scale: int = 1, n_frames: Optional[int] = None,
+                  n_views: Optional[int] = None, cameras: str = "refs",
+                  render_frames: bool = True) -> Workload:
+    """Build config ``name`` (c0..c4). ``scale`` > 1 divides the resolution
+    (for CPU-sized parity cases); ``cameras='refs'`` renders only the cameras
+    some view references, ``'all'`` the whole rig. ``n_frames`` overrides the
+    frame count of c3; ``render_frames=False`` returns rig, views and
+    references without ray-casting any frame (scenes_gpu renders them)."""
+    prm = workload_params(name, seed)
+    w, h, f, n = prm["w"], prm["h"], prm["f"], prm["n"]
+    radius, gap, scene, cap, k = prm["radius"], prm["gap"], prm["scene"], prm["capture"], prm["k"]
+    nv, nf, phis = prm["n_views"], prm["n_frames"], prm["phis"]
+    if name in ("c2", "c4") and n_views:
+        nv = n_views
+    if name == "c3" and n_frames:
+        nf = nv = n_frames
+    if not render_frames:
+        nf = 0
     if scale > 1:
         w, h, f = w // scale // 2 * 2, h // scale // 2 * 2, f / scale
     intr = _intr(w, h, f)

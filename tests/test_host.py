@@ -296,3 +296,36 @@ def test_two_rank_gloo_broadcast_shard_and_max(tmp_path):
     assert res[0][2] == res[1][2] == "32"    # 64 views split 32/32
     assert res[0][3] == res[1][3] == "64"
     assert float(res[0][4]) == float(res[1][4]) == 1.5
+
+
+def test_device_ray_caster_matches_host_generator():
+    """scenes_gpu (torch, run here on the CPU device) renders the host
+    generator's scenes: same depth rasters, RGB equal up to transcendental ulps."""
+    import torch
+
+    from paper_2007_00558_b200 import scenes, scenes_gpu
+
+    for name, scale in (("c0", 4), ("c4", 16)):
+        prm = scenes.workload_params(name, 2007)
+        wl = scenes.make_workload(name, scale=scale, render_frames=False)
+        cam = wl.rig[wl.refs[0][0]]
+        h = scenes.render(prm["scene"], cam, 0.0)
+        d = scenes_gpu.render(prm["scene"], cam, 0.0, dev="cpu")
+        np.testing.assert_array_equal(d["hit"].numpy(), h["hit"])
+        np.testing.assert_array_equal(d["fg"].numpy(), h["fg"])
+        np.testing.assert_allclose(d["depth"].numpy(), h["depth"], rtol=1e-12, atol=0)
+        np.testing.assert_array_equal(scenes_gpu.to_mm(d["depth"]).numpy().view(np.uint16),
+                                      scenes.to_mm(h["depth"]))
+        diff = np.abs(d["rgb"].numpy().astype(int) - h["rgb"].astype(int))
+        assert diff.max() <= 1 and (diff == 0).mean() >= 0.999
+        c = scenes_gpu.capture(prm["scene"], cam, 5, 0.0, dev="cpu", **prm["capture"])
+        hc = c.host()
+        assert hc.mm.dtype == np.uint16 and hc.rgb.shape == h["rgb"].shape
+        inv = (hc.validity == 1).mean()
+        assert 0 < inv < 0.2
+        assert ((hc.mm > 0) <= (hc.validity == 0)).all()      # layered: only FG carries mm
+        assert ((hc.bg_depth > 0) == (hc.bg_validity == 0)).all()
+    wl = scenes_gpu.make_workload("c3", n_frames=3, dev="cpu", scale=16)
+    assert len(wl.frames) == len(wl.virtuals) == 3
+    assert all(sorted(f) == sorted(r) for f, r in zip(wl.frames, wl.refs))
+    assert isinstance(wl.frames[0][wl.refs[0][0]].rgb, torch.Tensor)
