@@ -58,6 +58,10 @@ struct fvv_ctx {
     uint8_t *iprov = nullptr;
     float *idepth = nullptr;
     size_t icap = 0;
+    // K1 candidate list (camera << 26 | pixel) + its length
+    uint32_t *cand = nullptr;
+    int *ncand = nullptr;
+    size_t cand_cap = 0;
     // K1 range-weight table for range_sigma (kRangeTableLen doubles)
     double *range_w = nullptr;
     double range_sigma = -1.0;
@@ -113,7 +117,7 @@ cudaEvent_t prof_event(fvv_ctx *ctx) {
             CK(cudaEventRecord(b__, ctx->stream));                       \
             ctx->recs.push_back({kid, a__, b__});                        \
         }                                                                \
-        ++ctx->launches;                                                 \
+        ctx->launches += 1 + take_extra_launches();                      \
     } while (0)
 #define LAUNCH(expr) LAUNCH_K(FVV_K_OTHER, expr)
 
@@ -230,6 +234,25 @@ int bilateral_params(fvv_ctx *ctx, BilateralParams &p, int radius, double sigma_
 // reference defaults, depthproc.py:174-177
 int bilateral_defaults(fvv_ctx *ctx, BilateralParams &p) {
     return bilateral_params(ctx, p, 2, 2.0, 10.0, 6);
+}
+
+// room for `px` K1 candidates (a batch's pixel count bounds it)
+int fill_list(fvv_ctx *ctx, size_t px, uint32_t *&cand, int *&ncand) {
+    if (!ctx->ncand) CK(cudaMalloc(&ctx->ncand, sizeof(int)));
+    if (px > ctx->cand_cap) {
+        CK(cudaFree(ctx->cand));
+        ctx->cand = nullptr;
+        CK(cudaMalloc(&ctx->cand, px * sizeof(uint32_t)));
+        ctx->cand_cap = px;
+    }
+    cand = ctx->cand;
+    ncand = ctx->ncand;
+    return FVV_OK;
+}
+
+int with_fill(fvv_ctx *ctx, PreprocParams &p) {
+    if (p.radius <= 0) return FVV_OK;
+    return fill_list(ctx, (size_t)p.W * p.H, p.cand, p.ncand);
 }
 
 int canvas_pitch(int W, int r) { return (W + 2 * r + 2) & ~1; }  // even, >= W+2r+1
@@ -406,6 +429,8 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
+    cudaFree(ctx->cand);
+    cudaFree(ctx->ncand);
     cudaFree(ctx->iprov);
     cudaFree(ctx->idepth);
     cudaFree(ctx->range_w);
@@ -571,6 +596,7 @@ int fvv_bilateral_close_holes(fvv_ctx *ctx, const float *depth, const uint8_t *v
     p.validity = validity;
     p.rgb = rgb;
     if ((rc = bilateral_params(ctx, p, radius, sigma_spatial, sigma_range, min_valid))) return rc;
+    if ((rc = with_fill(ctx, p))) return rc;
     p.depth_out = depth_out;
     p.validity_out = validity_out;
     p.n_holes = n_holes_dev;
@@ -741,6 +767,7 @@ int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float 
     p.validity = validity;
     p.rgb = rgb;
     if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
+    if ((rc = with_fill(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
@@ -763,6 +790,7 @@ int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uin
     p.validity = validity;
     p.rgb = rgb;
     if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
+    if ((rc = with_fill(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     p.depth_out = depth_out;
@@ -798,6 +826,11 @@ int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
         c.texel = s.texel;
         c.warp_depth = s.fgd;
     }
+    if (hole_closing) {
+        size_t px = 0;
+        for (int i = 0; i < n; ++i) px += (size_t)b.cam[i].W * b.cam[i].H;
+        if ((rc = fill_list(ctx, px, b.cand, b.ncand))) return rc;
+    }
     LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess_batch(b, ctx->stream));
     for (int i = 0; i < n; ++i) ctx->slots[slots[i]].has_frame = true;
     return FVV_OK;
@@ -820,6 +853,7 @@ int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const ui
     p.inv_zf = 1.0 / z_far;
     p.rgb = rgb;
     if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
+    if ((rc = with_fill(ctx, p))) return rc;
     p.texel = s.texel;
     p.warp_depth = s.fgd;
     p.depth_out = depth_out;

@@ -135,10 +135,7 @@ __device__ __forceinline__ uchar4 load_rgb(const PreprocCore &p, size_t i) {
 __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_constant__ PreprocBatch batch) {
     const PreprocCore &p = batch.cam[blockIdx.z];
     const BilateralParams &bl = batch.bil;
-    __shared__ float sz[PSR * PSC];
-    __shared__ uint8_t sv[PSR * PSC];
-    __shared__ uchar4 sg[PSR * PSC];
-    __shared__ float s_fill[PY * PX];
+    __shared__ __align__(8) uint8_t sv[PSR * PSC + 8];
     __shared__ int s_holes;
 
     const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
@@ -191,16 +188,50 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     for (int q = 0; q < 4; ++q) nh += (val[q] == FVV_INVALID);
 
     if (R > 0 && __syncthreads_or(nh)) {
-        // interior from registers, halo ring from global memory
+        // K1 candidates: Invalid pixels with >= min_valid Valid pixels in
+        // their window (depthproc.py:218). Only the validity of the tile and
+        // its R-px ring is staged (zero-padded like scenegen._shift2d: outside
+        // pixels are never Valid); the candidates go to a global list that
+        // k_fill drains densely after this kernel (a tile holds a few dozen of
+        // them, so filling them here would idle most of its lanes).
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int si = (ty + R) * SC + lane * 4 + q + R;
-            sz[si] = z[q];
-            sv[si] = val[q];
-            sg[si] = g[q];
-        }
+        for (int q = 0; q < 4; ++q) sv[(ty + R) * SC + lane * 4 + q + R] = val[q];
         const int SR = PY + 2 * R;
-        const int ring = SR * SC - PY * PX;
+        const int ring = vec && R == 2 ? 0 : SR * SC - PY * PX;
+        if (vec && R == 2) {
+            // halo validity with 16-byte-group loads: rows y0-2, y0-1, y0+8,
+            // y0+9 as 34 aligned 4-px groups each (columns x0-4 .. x0+131),
+            // then the 2-px side columns of the 8 tile rows
+            if (tid < 4 * 34) {
+                const int hr = tid / 34, gq = tid - hr * 34;
+                const int ry = hr < 2 ? hr : PY + hr;  // smem row
+                const int qy = y0 - 2 + ry, gx = x0 - 4 + 4 * gq;
+                uint32_t v4 = 0xFFFFFFFFu;
+                if (qy >= 0 && qy < p.H && gx >= 0 && gx + 3 < p.W) {
+                    const size_t gi = (size_t)qy * p.W + gx;
+                    const uint2 m = __ldg(reinterpret_cast<const uint2 *>(p.mm + gi));
+                    v4 = __ldg(reinterpret_cast<const uint32_t *>(p.validity + gi));
+                    const uint32_t mm4[4] = {m.x & 0xFFFFu, m.x >> 16, m.y & 0xFFFFu, m.y >> 16};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (((v4 >> (8 * q)) & 0xFFu) == FVV_VALID && mm4[q] == 0)
+                            v4 = (v4 & ~(0xFFu << (8 * q))) | ((uint32_t)FVV_INVALID << (8 * q));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int sx = 4 * gq - 2 + q;  // smem column of pixel gx + q
+                    if (sx >= 0 && sx < SC) sv[ry * SC + sx] = (uint8_t)(v4 >> (8 * q));
+                }
+            } else if (tid < 4 * 34 + PY * 4) {
+                const int j = tid - 4 * 34, ry = 2 + (j >> 2), c = j & 3;
+                const int rx = c < 2 ? c : PX + c;  // smem columns 0,1 and PX+2, PX+3
+                const int qy = y0 - 2 + ry, qx = x0 - 2 + rx;
+                float zz;
+                uint8_t vv = 0xFF;
+                if (qy < p.H && qx >= 0 && qx < p.W) load_depth(p, qy, qx, zz, vv, nullptr);
+                sv[ry * SC + rx] = vv;
+            }
+        }
         for (int i = tid; i < ring; i += 256) {
             int ry, rx;
             const int top = R * SC;
@@ -211,34 +242,18 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
             const int qy = y0 - R + ry, qx = x0 - R + rx;
             float zz = 0.0f;
             uint8_t vv = 0xFF;
-            uchar4 gg = make_uchar4(0, 0, 0, 0);
-            if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) {
-                load_depth(p, qy, qx, zz, vv, nullptr);
-                gg = load_rgb(p, (size_t)qy * p.W + qx);
-            }
-            const int si = ry * SC + rx;
-            sz[si] = zz;
-            sv[si] = vv;
-            sg[si] = gg;
+            if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) load_depth(p, qy, qx, zz, vv, nullptr);
+            sv[ry * SC + rx] = vv;
         }
         __syncthreads();
-        // Each warp drains the Invalid pixels of its own 128-px row segment:
-        // ballot + __fns compaction, so the 24-tap loops run on dense lanes
-        // without another block barrier.
-        // Invalid pixels with fewer than min_valid Valid neighbours can never
-        // fill: count them with SIMD byte compares on the staged validity
-        // (Valid == 0 bytes) and keep only the candidates (sky / miss regions
-        // drop out here instead of running 24-tap loops).
-        unsigned hm[4];
-        int nh_warp = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             bool cand = false;
+            const int x = lane * 4 + q;  // tile column; window columns x..x+2R in smem
             if (val[q] == FVV_INVALID) {
                 int cnt = 0;
-                const int x = lane * 4 + q;  // tile column; window columns x..x+2R in smem
                 if (R == 2) {
-                    // 5-byte window = 4 + 1 bytes out of two aligned words
+                    // 5-byte window = 4 + 1 bytes out of two aligned words (Valid == 0)
                     for (int dy = -2; dy <= 2; ++dy) {
                         const int o = (ty + 2 + dy) * SC + x;
                         const uint32_t *w = reinterpret_cast<const uint32_t *>(sv) + (o >> 2);
@@ -252,59 +267,14 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                             cnt += sv[(ty + R + dy) * SC + x + R + dx] == FVV_VALID;
                 }
                 cand = cnt >= bl.min_valid;
-                if (!cand) s_fill[ty * PX + x] = -1.0f;
             }
-            hm[q] = __ballot_sync(0xffffffffu, cand);
-            nh_warp += __popc(hm[q]);
-        }
-        for (int base = 0; base < nh_warp; base += 32) {
-            int i = base + lane;
-            if (i < nh_warp) {
-                int qq = 0, src = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int c = __popc(hm[q]);
-                    if (i >= 0 && i < c) { qq = q; src = __fns(hm[q], 0, i + 1); }
-                    i -= c;
-                }
-                const int lp = ty * PX + src * 4 + qq;
-                const int c0 = (ty + R) * SC + src * 4 + qq + R;
-                // depthproc.py:196-222: taps in dy-major order, centre skipped;
-                // w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on Valid taps;
-                // fill iff >= min_valid Valid taps and den > 0
-                // The colour distance is an exact integer (u8 channels), so the
-                // range factor np.exp(-d2 * inv_2sr) is one table read.
-                const uchar4 gc = sg[c0];
-                const int g0 = gc.x, g1 = gc.y, g2 = gc.z;
-                double num = 0.0, den = 0.0;
-                int cnt = 0;
-                for (int dy = -R; dy <= R; ++dy) {
-                    for (int dx = -R; dx <= R; ++dx) {
-                        if (dy == 0 && dx == 0) continue;
-                        const int ni = c0 + dy * SC + dx;
-                        if (sv[ni] != FVV_VALID) continue;
-                        const uchar4 n = sg[ni];
-                        const int e0 = g0 - n.x, e1 = g1 - n.y, e2 = g2 - n.z;
-                        const int d2 = e0 * e0 + e1 * e1 + e2 * e2;
-                        const double w = dmul(bl.sw[dy + R][dx + R], __ldg(bl.range_w + d2));
-                        num = dadd(num, dmul(w, (double)sz[ni]));
-                        den = dadd(den, w);
-                        ++cnt;
-                    }
-                }
-                s_fill[lp] = (cnt >= bl.min_valid && den > 0.0)
-                                 ? __double2float_rn(ddiv(num, den)) : -1.0f;
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            // a fill is a positive depth; -1 marks "not filled"
-            const int lp = ty * PX + lane * 4 + q;
-            if (val[q] == FVV_INVALID && s_fill[lp] >= 0.0f) {
-                z[q] = s_fill[lp];
-                val[q] = FVV_VALID;
-            }
+            const unsigned m = __ballot_sync(0xffffffffu, cand);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(batch.ncand, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (cand)
+                batch.cand[base + __popc(m & ((1u << lane) - 1u))] =
+                    ((uint32_t)blockIdx.z << 26) | (uint32_t)(rowbase + xb + q);
         }
     }
 
@@ -354,6 +324,86 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     }
 }
 
+// K1 proper: the joint-bilateral fill (depthproc.py:196-222) of the
+// candidates k_preprocess listed, one thread per candidate, reading the
+// window straight from the (L2-resident) inputs. Taps in dy-major order with
+// the centre skipped; w = exp_s(dy,dx) * exp(-|g - g_nb|^2 / (2 sr^2)) on
+// Valid taps; the colour distance is an exact integer (u8 channels), so the
+// range factor np.exp(-d2 * inv_2sr) is one table read. A filled pixel's
+// outputs (depth, validity, texel flags, warp depth) are rewritten; k_preprocess
+// already wrote it as Invalid.
+__device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int dy, int dx,
+                                         float &z, bool &ok, uchar4 &g) {
+    const int qy = y + dy, qx = x + dx;
+    ok = false;
+    z = 0.0f;
+    g = make_uchar4(0, 0, 0, 0);
+    if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) {
+        uint8_t v;
+        load_depth(p, qy, qx, z, v, nullptr);
+        ok = v == FVV_VALID;
+        if (ok) g = load_rgb(p, (size_t)qy * p.W + qx);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_fill(const __grid_constant__ PreprocBatch batch) {
+    // one warp per candidate: lane k evaluates tap k (its loads and table read
+    // in parallel with the other taps'), then lane 0 accumulates the taps in
+    // the reference's order. A non-Valid tap contributes w = 0 exactly as in
+    // the reference (np.where(nb_valid, w, 0): adding +0.0 changes nothing).
+    const BilateralParams &bl = batch.bil;
+    const int n = *batch.ncand;
+    const int R = bl.radius, D = 2 * R + 1, ntaps = D * D - 1;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int e = warp; e < n; e += nwarps) {
+        const uint32_t ent = batch.cand[e];
+        const PreprocCore &p = batch.cam[ent >> 26];
+        const int i = (int)(ent & ((1u << 26) - 1));
+        const int y = i / p.W, x = i - y * p.W;
+        const uchar4 gc = load_rgb(p, (size_t)i);
+        double num = 0.0, den = 0.0;
+        int cnt = 0;
+        for (int c0 = 0; c0 < ntaps; c0 += 32) {
+            const int k = c0 + lane;
+            double w = 0.0, wz = 0.0;
+            bool ok = false;
+            if (k < ntaps) {
+                const int kk = k < ntaps / 2 ? k : k + 1;  // skip the centre
+                const int dy = kk / D - R, dx = kk % D - R;
+                float zn;
+                uchar4 n4;
+                fill_tap(p, x, y, dy, dx, zn, ok, n4);
+                if (ok) {
+                    const int e0 = gc.x - n4.x, e1 = gc.y - n4.y, e2 = gc.z - n4.z;
+                    w = dmul(bl.sw[dy + R][dx + R],
+                             __ldg(bl.range_w + (e0 * e0 + e1 * e1 + e2 * e2)));
+                    wz = dmul(w, (double)zn);
+                }
+            }
+            cnt += __popc(__ballot_sync(0xffffffffu, ok));
+            const int m = ntaps - c0 < 32 ? ntaps - c0 : 32;
+            for (int t = 0; t < m; ++t) {
+                const double wt = __shfl_sync(0xffffffffu, w, t);
+                const double wzt = __shfl_sync(0xffffffffu, wz, t);
+                num = dadd(num, wzt);
+                den = dadd(den, wt);
+            }
+        }
+        if (lane != 0 || !(cnt >= bl.min_valid && den > 0.0)) continue;
+        const float z = __double2float_rn(ddiv(num, den));
+        if (p.depth_out) p.depth_out[i] = z;
+        if (p.validity_out) p.validity_out[i] = FVV_VALID;
+        if (p.warp_depth) p.warp_depth[i] = z;
+        if (p.texel && !p.color_valid)
+            reinterpret_cast<uint8_t *>(p.texel + i)[3] = (uint8_t)kFlagLiveValid;
+    }
+}
+
+// kernels a launcher issued beyond the one LAUNCH_K counts (fvv_launch_count)
+static thread_local int t_extra_launches = 0;
+
 cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
     if (b.n <= 0) return cudaSuccess;
     int W = 0, H = 0;
@@ -361,15 +411,32 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
         W = b.cam[i].W > W ? b.cam[i].W : W;
         H = b.cam[i].H > H ? b.cam[i].H : H;
     }
+    const bool fill = b.bil.radius > 0;
+    if (fill) {
+        cudaError_t e = cudaMemsetAsync(b.ncand, 0, sizeof(int), s);
+        if (e != cudaSuccess) return e;
+    }
     dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
     k_preprocess<<<grid, 256, 0, s>>>(b);
+    if (fill) {
+        k_fill<<<148 * 8, 256, 0, s>>>(b);
+        ++t_extra_launches;
+    }
     return cudaGetLastError();
+}
+
+int take_extra_launches() {
+    const int n = t_extra_launches;
+    t_extra_launches = 0;
+    return n;
 }
 
 cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
     PreprocBatch b{};
     b.bil = static_cast<const BilateralParams &>(p);
     b.n = 1;
+    b.cand = p.cand;
+    b.ncand = p.ncand;
     b.cam[0] = static_cast<const PreprocCore &>(p);
     return launch_preprocess_batch(b, s);
 }

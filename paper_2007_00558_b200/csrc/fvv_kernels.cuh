@@ -45,12 +45,19 @@ struct BilateralParams {
 
 constexpr int kRangeTableLen = 3 * 255 * 255 + 1;
 
-struct PreprocParams : PreprocCore, BilateralParams {};
+struct PreprocParams : PreprocCore, BilateralParams {
+    uint32_t *cand;          // K1 candidate list (see PreprocBatch)
+    int *ncand;
+};
 
 // several cameras in one launch (blockIdx.z = camera), same bilateral params
 struct PreprocBatch {
     BilateralParams bil;
     int n;
+    // K1 candidate list (camera << 26 | pixel) and its length, device memory
+    // owned by the context; needed when bil.radius > 0
+    uint32_t *cand;
+    int *ncand;
     PreprocCore cam[FVV_MAX_REFS];
 };
 
@@ -142,6 +149,7 @@ cudaError_t launch_composite(const double *fg_c, const uint8_t *fg_v, const doub
 cudaError_t launch_selftest_div(long long n, uint64_t seed, int mode, unsigned long long *mism,
                                 cudaStream_t s);
 cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s);
+int take_extra_launches();  // kernels beyond one issued by the last launcher call
 cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
 size_t resolve_smem_bytes(int maxr);
 

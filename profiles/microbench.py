@@ -64,6 +64,26 @@ def main():
                       dtype=torch.uint8, device=dev)
     out["render_view_us"] = timed(lambda: eng.render([wl.virtuals[0]], [wl.refs[0]], out=img),
                                   args.reps)
+    # device time of the batched reference-camera ingest (K0+K1), with and
+    # without the hole fill, and of one view: the calls are captured into a
+    # CUDA graph and replayed, so host submission gaps are excluded
+    many = {c2: staged[c2] for c2 in wl.refs[0]}
+
+    def graphed(fn, n=20):
+        fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(n):
+                fn()
+        torch.cuda.synchronize()
+        return timed(g.replay, max(args.reps // n, 5)) / n
+
+    out["graph_ingest_nofill_us"] = graphed(lambda: eng.ingest_mm_many(many, hole_closing=False))
+    out["graph_ingest_fill_us"] = graphed(lambda: eng.ingest_mm_many(many, hole_closing=True))
+    out["graph_render_us"] = graphed(lambda: eng.render([wl.virtuals[0]], [wl.refs[0]], out=img))
     eng.ctx.profile(True)
     for _ in range(args.reps):
         eng.render([wl.virtuals[0]], [wl.refs[0]], out=img)
