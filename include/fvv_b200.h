@@ -222,6 +222,28 @@ int fvv_capture_encode(fvv_ctx *ctx, const float *depth, const uint8_t *validity
                        double threshold, double z_near, double z_far, uint8_t *y_out,
                        uint8_t *u_out, uint8_t *v_out, uint16_t *codes_out);
 
+/* ---- MED + Golomb-Rice lossless plane codec ----------
+ * The Rice stage of depthcodec's CODEC_PRED_RICE (depthcodec.py:281-409):
+ * LOCO-I median prediction, zig-zag, one Rice parameter per plane, MSB-first
+ * bits. The plane header (">BBIII") and the optional zlib stage around the
+ * stream stay with the caller, as the reference's struct/zlib calls. Both
+ * calls are synchronous. */
+/* bytes a stream buffer must hold for a width x height plane */
+int64_t fvv_rice_stream_bound(int32_t width, int32_t height);
+/* _compress_plane's MED + Rice part (depthcodec.py:376-383): k_out = the
+ * cheapest k of 0..14 (ties -> smaller k), nbits_out = stream length in bits;
+ * stream_out (device) receives (nbits+7)/8 bytes. */
+int fvv_rice_encode_plane(fvv_ctx *ctx, const uint8_t *plane, int32_t width, int32_t height,
+                          uint8_t *stream_out, int32_t *k_out, int64_t *nbits_out);
+/* _decompress_plane's Rice + MED part (depthcodec.py:386-409): decodes
+ * n_symbols (must be width*height) symbols of parameter k from the device
+ * stream, rebuilds the plane and returns its adler32 (the caller compares it
+ * with the header's). FVV_EINVAL "rice stream truncated" when the stream runs
+ * out early (the reference's DecodeError). */
+int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, int32_t k,
+                          int64_t n_symbols, int32_t width, int32_t height, uint8_t *plane_out,
+                          uint32_t *adler_out);
+
 /* ---- session path: resident camera slots, batched views ---------------------
  * The edge server keeps a slot per rig camera: its calibration, its static
  * BG model (uploaded once, pipeline.py:445) and its latest live frame. */

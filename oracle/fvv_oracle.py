@@ -580,3 +580,132 @@ def remove_bg_depth(depth, validity, fg_mask):
     val[bg] = BACKGROUND
     d[bg] = 0.0
     return d, val
+
+
+# ---------------------------------------------------------------------------
+# MED + Golomb-Rice plane codec (depthcodec.py:281-409), numpy restatement
+
+
+def med_residuals(x: np.ndarray) -> np.ndarray:
+    """``_med_residuals_py`` (depthcodec.py:281-298): x - MED(a left, b up,
+    c up-left), zero outside the plane, as int32 (vectorised: the predictor
+    reads only the input plane)."""
+    x = x.astype(np.int32)
+    a = np.zeros_like(x)
+    b = np.zeros_like(x)
+    c = np.zeros_like(x)
+    a[:, 1:] = x[:, :-1]
+    b[1:, :] = x[:-1, :]
+    c[1:, 1:] = x[:-1, :-1]
+    mx, mn = np.maximum(a, b), np.minimum(a, b)
+    p = np.where(c >= mx, mn, np.where(c <= mn, mx, a + b - c))
+    return x - p
+
+
+def med_reconstruct(r: np.ndarray) -> np.ndarray:
+    """``_med_reconstruct_py`` (depthcodec.py:301-316): the inverse recurrence,
+    row by row (int64 running values; the caller casts to uint8)."""
+    h, w = r.shape
+    x = np.zeros((h, w), np.int64)
+    for i in range(h):
+        up = x[i - 1] if i > 0 else np.zeros(w, np.int64)
+        left = 0
+        for j in range(w):
+            a = left if j > 0 else 0
+            b = int(up[j])
+            c = int(up[j - 1]) if (i > 0 and j > 0) else 0
+            mx, mn = (a, b) if a > b else (b, a)
+            p = mn if c >= mx else (mx if c <= mn else a + b - c)
+            left = int(r[i, j]) + p
+            x[i, j] = left
+    return x
+
+
+def zigzag(r: np.ndarray) -> np.ndarray:
+    return np.where(r >= 0, 2 * r.astype(np.int64), -2 * r.astype(np.int64) - 1)
+
+
+def rice_k(zz: np.ndarray) -> int:
+    """depthcodec.py:380-381: the k of min over (cost, k), k in 0..14."""
+    return min((int(np.sum((zz >> k) + 1 + k)), k) for k in range(15))[1]
+
+
+def rice_encode(zz: np.ndarray, k: int) -> bytes:
+    """``_rice_encode_py`` (depthcodec.py:319-334): q zeros, a one, k bits
+    MSB-first; vectorised over symbols with a cumulative bit offset."""
+    zz = np.asarray(zz, np.int64).ravel()
+    q = zz >> k
+    lens = q + 1 + k
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]) if zz.size else np.zeros(0, np.int64)
+    nbits = int(lens.sum())
+    bits = np.zeros(nbits, np.uint8)
+    one = off + q
+    bits[one] = 1
+    for bi in range(k):
+        bits[one + 1 + bi] = (zz >> (k - 1 - bi)) & 1
+    return np.packbits(bits).tobytes()
+
+
+def rice_decode(buf: bytes, n: int, k: int):
+    """``_rice_decode_py`` (depthcodec.py:337-355): (symbols, ok)."""
+    bits = np.unpackbits(np.frombuffer(buf, np.uint8))
+    nbits = bits.size
+    ones = np.flatnonzero(bits)
+    zz = np.zeros(n, np.int64)
+    pos = 0
+    for s in range(n):
+        i = np.searchsorted(ones, pos)
+        if i >= ones.size:
+            return zz, False
+        t = int(ones[i])
+        if t + 1 + k > nbits:
+            return zz, False
+        rem = 0
+        for b in bits[t + 1:t + 1 + k]:
+            rem = (rem << 1) | int(b)
+        zz[s] = ((t - pos) << k) | rem
+        pos = t + 1 + k
+    return zz, True
+
+
+def compress_plane(plane: np.ndarray) -> bytes:
+    """``_compress_plane`` (depthcodec.py:373-383)."""
+    import struct
+    import zlib
+
+    zz = zigzag(med_residuals(plane)).ravel()
+    k = rice_k(zz)
+    stream = rice_encode(zz, k)
+    deflated = zlib.compress(stream, 6)
+    blob, flag = (deflated, 1) if len(deflated) < len(stream) else (stream, 0)
+    return struct.pack(">BBIII", k, flag, zz.size, len(blob),
+                       zlib.adler32(np.ascontiguousarray(plane, np.uint8).tobytes())) + blob
+
+
+def decompress_plane(data: bytes, offset: int, shape):
+    """``_decompress_plane`` (depthcodec.py:386-409); raises ValueError."""
+    import struct
+    import zlib
+
+    k, flag, n, blen, check = struct.unpack_from(">BBIII", data, offset)
+    offset += 14
+    blob = data[offset:offset + blen]
+    if len(blob) != blen:
+        raise ValueError("plane blob truncated")
+    offset += blen
+    stream = zlib.decompress(blob) if flag else blob
+    if n != shape[0] * shape[1]:
+        raise ValueError("plane symbol count mismatch")
+    zz, ok = rice_decode(stream, n, k)
+    if not ok:
+        raise ValueError("rice stream truncated")
+    r = np.where(zz % 2 == 0, zz // 2, -(zz + 1) // 2).astype(np.int32)
+    x = med_reconstruct(r.reshape(shape)).astype(np.uint8)
+    if zlib.adler32(x.tobytes()) != check:
+        raise ValueError("plane checksum mismatch")
+    return x, offset
+
+
+def encode_lossless_payload(y, u, v) -> bytes:
+    """encode_lossless's CODEC_PRED_RICE payload (depthcodec.py:437-438)."""
+    return b"".join(compress_plane(p) for p in (y, u, v))

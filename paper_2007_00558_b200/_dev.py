@@ -25,6 +25,8 @@ def upload(a, dtype) -> torch.Tensor:
         t = a.to(device=device(), dtype=_DT[np.dtype(dtype).type])
         return t.contiguous()
     arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    if any(st < 0 for st in arr.strides):  # e.g. a reversed 1-element view
+        arr = arr.copy()
     if arr.dtype == np.uint16:
         arr = arr.view(np.int16)
     return torch.from_numpy(arr).to(device())

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "fvv_capture.cuh"
+#include "fvv_codec.cuh"
 #include "fvv_kernels.cuh"
 
 using namespace fvv;
@@ -62,6 +63,8 @@ struct fvv_ctx {
     uint32_t *cand = nullptr;
     int *ncand = nullptr;
     size_t cand_cap = 0;
+    // MED + Rice plane codec scratch
+    RiceScratch rice;
     // K1 range-weight table for range_sigma (kRangeTableLen doubles)
     double *range_w = nullptr;
     double range_sigma = -1.0;
@@ -300,6 +303,43 @@ int ensure_zsrc(fvv_ctx *ctx, int n, size_t px) {
     return FVV_OK;
 }
 
+// codec scratch for n pixels and c decode chunks
+int rice_scratch(fvv_ctx *ctx, size_t n, size_t c) {
+    RiceScratch &r = ctx->rice;
+    if (!r.costs) {
+        CK(cudaMalloc(&r.costs, 16 * sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.total, sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.changed, sizeof(int)));
+    }
+    const size_t blocks = (n + 1023) / 1024 + 1;
+    const size_t bneed = blocks > c + 1 ? blocks : c + 1;
+    if (n > r.n_cap) {
+        CK(cudaFree(r.zz));
+        CK(cudaFree(r.res));
+        r.zz = nullptr;
+        r.res = nullptr;
+        CK(cudaMalloc(&r.zz, n * sizeof(uint16_t)));
+        CK(cudaMalloc(&r.res, n * sizeof(int32_t)));
+        r.n_cap = n;
+    }
+    const size_t cneed = bneed;
+    if (cneed > r.c_cap) {
+        for (void **q : {(void **)&r.block, (void **)&r.entry, (void **)&r.exit,
+                         (void **)&r.exit_prev, (void **)&r.count, (void **)&r.trunc}) {
+            CK(cudaFree(*q));
+            *q = nullptr;
+        }
+        CK(cudaMalloc(&r.block, cneed * sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.entry, cneed * sizeof(long long)));
+        CK(cudaMalloc(&r.exit, cneed * sizeof(long long)));
+        CK(cudaMalloc(&r.exit_prev, cneed * sizeof(long long)));
+        CK(cudaMalloc(&r.count, cneed * sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.trunc, cneed * sizeof(int)));
+        r.c_cap = cneed;
+    }
+    return FVV_OK;
+}
+
 double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
     const double dx = a.C[0] - b.C[0], dy = a.C[1] - b.C[1], dz = a.C[2] - b.C[2];
     return 1.0 / (std::sqrt((dx * dx + dy * dy) + dz * dz) + eps);
@@ -429,6 +469,11 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
+    for (void *q : {(void *)ctx->rice.zz, (void *)ctx->rice.res, (void *)ctx->rice.block,
+                    (void *)ctx->rice.costs, (void *)ctx->rice.total, (void *)ctx->rice.entry,
+                    (void *)ctx->rice.exit, (void *)ctx->rice.exit_prev, (void *)ctx->rice.count,
+                    (void *)ctx->rice.trunc, (void *)ctx->rice.changed})
+        cudaFree(q);
     cudaFree(ctx->cand);
     cudaFree(ctx->ncand);
     cudaFree(ctx->iprov);
@@ -725,6 +770,50 @@ int fvv_capture_encode(fvv_ctx *ctx, const float *depth, const uint8_t *validity
     p.v = v_out;
     p.codes_out = codes_out;
     LAUNCH_K(FVV_K_OTHER, launch_capture_encode(p, ctx->stream));
+    return FVV_OK;
+}
+
+int64_t fvv_rice_stream_bound(int32_t width, int32_t height) {
+    if (width < 0 || height < 0) return -1;
+    return rice_stream_bound(width, height);
+}
+
+int fvv_rice_encode_plane(fvv_ctx *ctx, const uint8_t *plane, int32_t width, int32_t height,
+                          uint8_t *stream_out, int32_t *k_out, int64_t *nbits_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width > 0 && height > 0 && plane && stream_out && k_out && nbits_out,
+         "rice_encode_plane: bad arguments");
+    const size_t n = (size_t)width * height;
+    if ((rc = rice_scratch(ctx, n, 0))) return rc;
+    int k = 0;
+    long long nbits = 0;
+    LAUNCH(rice_encode(plane, width, height, ctx->rice, stream_out, &k, &nbits, ctx->stream));
+    ctx->launches += 3;  // k_med_zz, k_rice_lens, k_scan_blocks, k_rice_write
+    *k_out = k;
+    *nbits_out = nbits;
+    return FVV_OK;
+}
+
+int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, int32_t k,
+                          int64_t n_symbols, int32_t width, int32_t height, uint8_t *plane_out,
+                          uint32_t *adler_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width > 0 && height > 0 && plane_out && adler_out && nbytes >= 0 && (stream || !nbytes),
+         "rice_decode_plane: bad arguments");
+    NEED(k >= 0 && k <= 48, "rice parameter out of range");
+    NEED(n_symbols == (int64_t)width * height, "plane symbol count mismatch");
+    NEED(height <= 32 * kMedMaxStrips && (size_t)width * 2 * sizeof(int32_t) <= 200 * 1024,
+         "plane too large for the MED rebuild");
+    const size_t chunks = (size_t)((nbytes * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
+    if ((rc = rice_scratch(ctx, (size_t)n_symbols, chunks))) return rc;
+    int status = 0;
+    uint32_t adler = 0;
+    LAUNCH(rice_decode(stream, nbytes, k, n_symbols, width, height, ctx->rice, plane_out, &adler,
+                       &status, ctx->stream));
+    if (status) return fail(ctx, FVV_EINVAL, "rice stream truncated");
+    *adler_out = adler;
     return FVV_OK;
 }
 

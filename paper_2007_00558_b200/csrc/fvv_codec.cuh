@@ -1,0 +1,46 @@
+// MED + Golomb-Rice plane codec (fvv_codec.cu): scratch and host launchers.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fvv {
+
+constexpr int kRiceKMax = 14;          // depthcodec.py:380: k in range(15)
+constexpr int kRiceChunkBits = 256;    // decode chunk (speculative segmentation unit)
+constexpr int kMedMaxStrips = 512;     // MED rebuild: 32-row strips per plane (H <= 16384)
+
+// per-context device scratch, sized for n pixels / c chunks
+struct RiceScratch {
+    uint16_t *zz = nullptr;                 // [n] encoder symbols
+    int32_t *res = nullptr;                 // [n] decoder residuals
+    unsigned long long *block = nullptr;    // [max(n/1024, c) + 1] scan buffer
+    unsigned long long *costs = nullptr;    // [16] per-k costs / adler sums
+    unsigned long long *total = nullptr;    // [1]
+    long long *entry = nullptr, *exit = nullptr, *exit_prev = nullptr;  // [c]
+    unsigned long long *count = nullptr;    // [c]
+    int *trunc = nullptr;                   // [c]
+    int *changed = nullptr;                 // [1]
+    size_t n_cap = 0, c_cap = 0;
+};
+
+// Encode one u8 plane: MED residuals, zig-zag, cheapest k, Rice bits into
+// `stream` (zeroed here; needs rice_stream_bound bytes). Synchronises once
+// (the choice of k).
+cudaError_t rice_encode(const uint8_t *plane, int W, int H, RiceScratch &sc, uint8_t *stream,
+                        int *k_out, long long *nbits_out, cudaStream_t s);
+
+// Decode n symbols of parameter k from `stream` (nbytes), rebuild the W x H
+// plane and its adler32. *status = 1 when the stream runs out early.
+// Synchronous.
+cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long long n, int W, int H,
+                        RiceScratch &sc, uint8_t *plane, uint32_t *adler_out, int *status,
+                        cudaStream_t s);
+
+// bytes `stream` must hold for a W x H plane: the cheapest k costs at most
+// what k = 8 does (<= 10 bits per symbol for zz <= 510), plus a spill word
+inline long long rice_stream_bound(int W, int H) {
+    return ((long long)W * H * 10 + 31) / 32 * 4 + 8;
+}
+
+}  // namespace fvv

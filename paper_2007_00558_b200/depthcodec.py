@@ -7,8 +7,9 @@
 
 The encoder half (``quantize12`` / ``pack_yuv420`` and the fused
 ``capture_encode`` of the capture server's per-frame chain) is provided as
-SURVEY.md §8f's rank-1 widening. The MED+Rice entropy coder (a sequential
-bitstream) is not.
+SURVEY.md §8f's rank-1 widening; the MED + Golomb-Rice lossless plane codec
+(``encode_lossless`` / ``decode_lossless``, the wire format of the depth
+stream) as its rank-4 widening.
 """
 
 from __future__ import annotations
@@ -172,3 +173,181 @@ def capture_encode(depth, color, range_: DepthRange, correction=None, bg_model=N
              vv.data_ptr(), codes.data_ptr())
     return (Yuv420Image(_dev.host(y), _dev.host(u), _dev.host(vv)),
             DisparityMap12(W, H, _dev.host(codes, np.uint16)))
+
+
+# ---------------------------------------------------------------------------
+# Encoded frames and the MED + Golomb-Rice lossless codec (SURVEY.md §8f
+# rank 4): depthcodec.py:225-267 (frame container, registry, errors) and
+# 281-464 (plane codec). The MED prediction, zig-zag, Rice parameter choice
+# and the bit stream run on the GPU (fvv_rice_encode_plane /
+# fvv_rice_decode_plane); the per-plane header and the optional zlib stage
+# around the stream are the reference's own struct / zlib calls on the host.
+
+import struct  # noqa: E402
+import zlib  # noqa: E402
+import ctypes as C  # noqa: E402
+from typing import Callable, Dict, Tuple  # noqa: E402
+
+MEDIA_COLOR = 0
+MEDIA_DEPTH = 1
+
+CODEC_RAW = 0
+CODEC_ZLIB = 1
+CODEC_PRED_RICE = 2
+
+_HEADER = struct.Struct(">BBHHQI")        # codec, media, width, height, timestamp, length
+_PLANE_HEADER = struct.Struct(">BBIII")   # k, deflate flag, symbols, bytes, adler32
+
+
+@dataclass(frozen=True)
+class EncodedFrame:
+    """depthcodec.EncodedFrame (depthcodec.py:236-259)."""
+
+    media_type: int
+    codec_id: int
+    width: int
+    height: int
+    timestamp_us: int
+    payload: bytes
+
+    def serialize(self) -> bytes:
+        return _HEADER.pack(self.codec_id, self.media_type, self.width, self.height,
+                            self.timestamp_us, len(self.payload)) + self.payload
+
+    @staticmethod
+    def deserialize(data: bytes) -> "EncodedFrame":
+        if len(data) < _HEADER.size:
+            raise ValueError("encoded frame truncated")
+        codec, media, w, h, ts, n = _HEADER.unpack_from(data)
+        if len(data) != _HEADER.size + n:
+            raise ValueError("encoded frame length mismatch")
+        return EncodedFrame(media, codec, w, h, ts, data[_HEADER.size:])
+
+
+class UnsupportedCodecError(ValueError):
+    pass
+
+
+class DecodeError(ValueError):
+    pass
+
+
+def _compress_plane(plane: np.ndarray) -> bytes:
+    """depthcodec._compress_plane (depthcodec.py:373-383) with the MED + Rice
+    stage on the GPU."""
+    plane = np.ascontiguousarray(plane, dtype=np.uint8)
+    H, W = plane.shape
+    ctx = _native.context()
+    x = _dev.upload(plane, np.uint8)
+    bound = int(ctx.lib.fvv_rice_stream_bound(W, H))
+    stream = _dev.empty((bound,), np.uint8)
+    k, nbits = C.c_int32(), C.c_int64()
+    ctx.call("fvv_rice_encode_plane", x.data_ptr(), W, H, stream.data_ptr(), C.byref(k),
+             C.byref(nbits))
+    raw = _dev.host(stream[:(nbits.value + 7) // 8]).tobytes()
+    deflated = zlib.compress(raw, 6)
+    blob, flag = (deflated, 1) if len(deflated) < len(raw) else (raw, 0)
+    return _PLANE_HEADER.pack(k.value, flag, W * H, len(blob), zlib.adler32(plane.tobytes())) + blob
+
+
+def _decompress_plane_dev(data: bytes, offset: int, shape):
+    """depthcodec._decompress_plane (depthcodec.py:386-409) with the Rice +
+    MED stage on the GPU; returns (device plane tensor, adler32, new offset)."""
+    if len(data) - offset < _PLANE_HEADER.size:
+        raise DecodeError("plane header truncated")
+    k, flag, n, blob_len, check = _PLANE_HEADER.unpack_from(data, offset)
+    offset += _PLANE_HEADER.size
+    blob = data[offset:offset + blob_len]
+    if len(blob) != blob_len:
+        raise DecodeError("plane blob truncated")
+    offset += blob_len
+    stream = zlib.decompress(blob) if flag else blob
+    if n != shape[0] * shape[1]:
+        raise DecodeError("plane symbol count mismatch")
+    H, W = shape
+    ctx = _native.context()
+    s = _dev.upload(np.frombuffer(stream, dtype=np.uint8), np.uint8) if stream else None
+    out = _dev.empty((H, W), np.uint8)
+    adler = C.c_uint32()
+    try:
+        ctx.call("fvv_rice_decode_plane", _dev.ptr(s), len(stream), int(k), int(n), W, H,
+                 out.data_ptr(), C.byref(adler))
+    except ValueError as e:
+        raise DecodeError(str(e)) from None
+    if adler.value != check:
+        raise DecodeError("plane checksum mismatch")
+    return out, offset
+
+
+def _decompress_plane(data: bytes, offset: int, shape) -> Tuple[np.ndarray, int]:
+    out, offset = _decompress_plane_dev(data, offset, shape)
+    return _dev.host(out), offset
+
+
+_COMPRESSORS: Dict[int, Tuple[Callable[[bytes], bytes], Callable[[bytes], bytes]]] = {
+    CODEC_RAW: (lambda b: b, lambda b: b),
+    CODEC_ZLIB: (lambda b: zlib.compress(b, 6), zlib.decompress),
+}
+
+
+def register_codec(codec_id: int, compress: Callable[[bytes], bytes],
+                   decompress: Callable[[bytes], bytes]) -> None:
+    """Register an alternative lossless byte compressor (depthcodec.py:416-421)."""
+    if codec_id in _COMPRESSORS or codec_id == CODEC_PRED_RICE:
+        raise ValueError(f"codec id {codec_id} already registered")
+    _COMPRESSORS[codec_id] = (compress, decompress)
+
+
+def _codec(codec_id: int):
+    try:
+        return _COMPRESSORS[codec_id]
+    except KeyError:
+        raise UnsupportedCodecError(f"codec id {codec_id} is not a byte-stream codec") from None
+
+
+def encode_lossless(img: Yuv420Image, timestamp_us: int = 0,
+                    codec_id: int = CODEC_PRED_RICE) -> EncodedFrame:
+    """depthcodec.encode_lossless (depthcodec.py:435-443)."""
+    if codec_id == CODEC_PRED_RICE:
+        payload = b"".join(_compress_plane(p) for p in (img.y, img.u, img.v))
+    else:
+        compress, _ = _codec(codec_id)
+        payload = compress(img.y.tobytes() + img.u.tobytes() + img.v.tobytes())
+    return EncodedFrame(MEDIA_DEPTH, codec_id, img.width, img.height, timestamp_us, payload)
+
+
+def decode_lossless_planes(frame: EncodedFrame):
+    """The three YUV420 planes of a CODEC_PRED_RICE depth frame as device
+    tensors (the form the edge server feeds K0, pipeline.py:469-472)."""
+    w, h = frame.width, frame.height
+    try:
+        y, off = _decompress_plane_dev(frame.payload, 0, (h, w))
+        u, off = _decompress_plane_dev(frame.payload, off, (h // 2, w // 2))
+        v, off = _decompress_plane_dev(frame.payload, off, (h // 2, w // 2))
+    except DecodeError:
+        raise
+    except Exception as e:
+        raise DecodeError(f"payload does not decode: {e}") from e
+    if off != len(frame.payload):
+        raise DecodeError("trailing bytes after planes")
+    return y, u, v
+
+
+def decode_lossless(frame: EncodedFrame) -> Yuv420Image:
+    """depthcodec.decode_lossless (depthcodec.py:446-470)."""
+    w, h = frame.width, frame.height
+    if frame.codec_id == CODEC_PRED_RICE:
+        y, u, v = decode_lossless_planes(frame)
+        return Yuv420Image(_dev.host(y), _dev.host(u), _dev.host(v))
+    _, decompress = _codec(frame.codec_id)
+    try:
+        raw = decompress(frame.payload)
+    except Exception as e:
+        raise DecodeError(f"payload does not decode: {e}") from e
+    if len(raw) != w * h + 2 * (w // 2) * (h // 2):
+        raise DecodeError("decoded plane size mismatch")
+    y = np.frombuffer(raw, dtype=np.uint8, count=w * h).reshape(h, w)
+    cn = (w // 2) * (h // 2)
+    u = np.frombuffer(raw, dtype=np.uint8, count=cn, offset=w * h).reshape(h // 2, w // 2)
+    v = np.frombuffer(raw, dtype=np.uint8, count=cn, offset=w * h + cn).reshape(h // 2, w // 2)
+    return Yuv420Image(y.copy(), u.copy(), v.copy())

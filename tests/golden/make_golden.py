@@ -227,7 +227,54 @@ def capture_case():
     print("capture ok: fg", int(fg.sum()), "codes", np.bincount(codes.values.ravel() > 1))
 
 
+def rice_case():
+    """encode_lossless (MED + Golomb-Rice, depthcodec.py:281-443) payloads of
+    the reference for small explicit planes and for the c1 depth raster at
+    half resolution (the latter is regenerated by the tests from the seeded
+    generator + the oracle's quantize12/pack_yuv420, checked by sha)."""
+    out = {}
+    rng = np.random.default_rng(31)
+    small = {
+        "noise": rng.integers(0, 256, (48, 64)).astype(np.uint8),
+        "zero": np.zeros((16, 32), np.uint8),
+        "ramp": (np.add.outer(np.arange(10) * 7, np.arange(6) * 3) % 256).astype(np.uint8),
+        "sparse": (rng.random((40, 56)) < 0.02).astype(np.uint8) * 200,
+    }
+    for name, y in small.items():
+        H, W = y.shape
+        u = np.ascontiguousarray(y[::2, ::2])
+        v = np.ascontiguousarray(255 - y[1::2, 1::2])
+        img = rcodec.Yuv420Image(y, u, v)
+        enc = rcodec.encode_lossless(img, timestamp_us=7)
+        out[f"{name}_y"], out[f"{name}_u"], out[f"{name}_v"] = y, u, v
+        out[f"{name}_payload"] = np.frombuffer(enc.payload, np.uint8)
+    wl = workload("c1", 2, 2007)
+    c = wl.frames[0][wl.refs[0][0]]
+    H, W = c.mm.shape
+    d = np.where(c.mm > 0, c.mm.astype(np.float32) / 1000.0,
+                 np.where(c.bg_validity == 0, c.bg_depth, 0.0)).astype(np.float32)
+    val = np.where(d > 0, 0, 1).astype(np.uint8)
+    codes = rcodec.quantize12(rc.DepthFrame(W, H, d, val), rc.DepthRange(0.5, 6.5))
+    img = rcodec.pack_yuv420(codes)
+    enc = rcodec.encode_lossless(img)
+    out["scene_sha"] = np.array(sha(img.y, img.u, img.v))
+    out["scene_payload"] = np.frombuffer(enc.payload, np.uint8)
+    heads = []
+    off = 0
+    for shape in ((H, W), (H // 2, W // 2), (H // 2, W // 2)):
+        k, flag, n, blen, chk = rcodec._PLANE_HEADER.unpack_from(enc.payload, off)
+        heads.append((k, flag, n, blen))
+        off += rcodec._PLANE_HEADER.size + blen
+    out["scene_heads"] = np.array(heads, np.int64)
+    np.savez_compressed(OUT / "rice.npz", **out)
+    print("rice ok:", {k: v.size for k, v in out.items() if k.endswith("payload")}, heads)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["rice"]:
+        rice_case()
+        sys.exit(0)
+    rice_case()
     capture_case()
     for args in SYN_CASES:
         syn_case(*args)
