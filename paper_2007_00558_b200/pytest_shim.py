@@ -14,8 +14,15 @@ What is rebound:
 * ``fvv.pipeline.synthesis`` — the module global ``EdgeServer.render_tick``
   reaches through ``synthesize_with_config`` (pipeline.py:546, 569-570);
 * ``fvv.depthproc.bilateral_close_holes`` (called at pipeline.py:518-519);
-* with ``FVV_SHIM_CODEC=1`` also ``fvv.depthcodec.unpack_yuv420`` /
-  ``dequantize12`` (pipeline.py:469-472).
+* with ``FVV_SHIM_CODEC=1`` also the depth codec the edge server runs before
+  synthesis and the capture server after capture: ``fvv.depthcodec``'s
+  ``unpack_yuv420`` / ``dequantize12`` (pipeline.py:469-472), ``quantize12`` /
+  ``pack_yuv420`` (pipeline.py:392-393) and the MED + Rice
+  ``encode_lossless`` / ``decode_lossless`` (pipeline.py:394, 469). This
+  module's codec then builds and raises the reference's own types
+  (EncodedFrame, Yuv420Image, DisparityMap12, DecodeError,
+  UnsupportedCodecError), so callers that catch or isinstance-check them
+  keep working.
 """
 
 from __future__ import annotations
@@ -58,8 +65,12 @@ def install() -> types.ModuleType:
 
         from . import depthcodec as ours_codec
 
-        ref_codec.unpack_yuv420 = ours_codec.unpack_yuv420
-        ref_codec.dequantize12 = ours_codec.dequantize12
+        for name in ("EncodedFrame", "Yuv420Image", "DisparityMap12", "DecodeError",
+                     "UnsupportedCodecError"):
+            setattr(ours_codec, name, getattr(ref_codec, name))
+        for name in ("unpack_yuv420", "dequantize12", "quantize12", "pack_yuv420",
+                     "encode_lossless", "decode_lossless"):
+            setattr(ref_codec, name, getattr(ours_codec, name))
     installed["synthesis"] = mod
     return mod
 

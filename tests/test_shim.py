@@ -37,3 +37,27 @@ print("OK")
                          cwd="/tmp")
     assert out.returncode == 0, out.stderr
     assert "OK" in out.stdout
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference package not present on this host")
+def test_shim_codec_rebinding_uses_reference_types():
+    code = r"""
+import os
+os.environ["FVV_SHIM_CODEC"] = "1"
+from paper_2007_00558_b200 import pytest_shim, depthcodec as ours
+pytest_shim.install()
+import fvv.depthcodec as rc
+for n in ("unpack_yuv420", "dequantize12", "quantize12", "pack_yuv420", "encode_lossless",
+          "decode_lossless"):
+    assert getattr(rc, n) is getattr(ours, n), n
+for n in ("EncodedFrame", "Yuv420Image", "DisparityMap12", "DecodeError",
+          "UnsupportedCodecError"):
+    assert getattr(ours, n) is getattr(rc, n), n
+print("OK")
+"""
+    env = {"PYTHONPATH": f"{REF_SRC}:{ROOT}", "PYTHONDONTWRITEBYTECODE": "1",
+           "PATH": "/usr/bin:/bin"}
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd="/tmp")
+    assert out.returncode == 0, out.stderr
+    assert "OK" in out.stdout
