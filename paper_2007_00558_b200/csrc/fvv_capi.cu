@@ -303,8 +303,8 @@ int ensure_zsrc(fvv_ctx *ctx, int n, size_t px) {
     return FVV_OK;
 }
 
-// codec scratch for n pixels and c decode chunks
-int rice_scratch(fvv_ctx *ctx, size_t n, size_t c) {
+// codec scratch for n pixels (ns in the skewed rebuild layout) and c chunks
+int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
     RiceScratch &r = ctx->rice;
     if (!r.costs) {
         CK(cudaMalloc(&r.costs, 16 * sizeof(unsigned long long)));
@@ -313,14 +313,18 @@ int rice_scratch(fvv_ctx *ctx, size_t n, size_t c) {
     }
     const size_t blocks = (n + 1023) / 1024 + 1;
     const size_t bneed = blocks > c + 1 ? blocks : c + 1;
-    if (n > r.n_cap) {
+    const size_t nn = n > ns ? n : ns;
+    if (nn > r.n_cap) {
         CK(cudaFree(r.zz));
         CK(cudaFree(r.res));
+        CK(cudaFree(r.skew));
         r.zz = nullptr;
         r.res = nullptr;
-        CK(cudaMalloc(&r.zz, n * sizeof(uint16_t)));
-        CK(cudaMalloc(&r.res, n * sizeof(int32_t)));
-        r.n_cap = n;
+        r.skew = nullptr;
+        CK(cudaMalloc(&r.zz, nn * sizeof(uint16_t)));
+        CK(cudaMalloc(&r.res, nn * sizeof(int32_t)));
+        CK(cudaMalloc(&r.skew, nn));
+        r.n_cap = nn;
     }
     const size_t cneed = bneed;
     if (cneed > r.c_cap) {
@@ -469,7 +473,8 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
-    for (void *q : {(void *)ctx->rice.zz, (void *)ctx->rice.res, (void *)ctx->rice.block,
+    for (void *q : {(void *)ctx->rice.zz, (void *)ctx->rice.res, (void *)ctx->rice.skew,
+                    (void *)ctx->rice.block,
                     (void *)ctx->rice.costs, (void *)ctx->rice.total, (void *)ctx->rice.entry,
                     (void *)ctx->rice.exit, (void *)ctx->rice.exit_prev, (void *)ctx->rice.count,
                     (void *)ctx->rice.trunc, (void *)ctx->rice.changed})
@@ -804,10 +809,10 @@ int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, i
          "rice_decode_plane: bad arguments");
     NEED(k >= 0 && k <= 48, "rice parameter out of range");
     NEED(n_symbols == (int64_t)width * height, "plane symbol count mismatch");
-    NEED(height <= 32 * kMedMaxStrips && (size_t)width * 2 * sizeof(int32_t) <= 200 * 1024,
-         "plane too large for the MED rebuild");
+    NEED(width <= kMedMaxWidth, "plane too wide for the MED rebuild");
     const size_t chunks = (size_t)((nbytes * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
-    if ((rc = rice_scratch(ctx, (size_t)n_symbols, chunks))) return rc;
+    if ((rc = rice_scratch(ctx, (size_t)n_symbols, chunks, rice_skew_size(width, height))))
+        return rc;
     int status = 0;
     uint32_t adler = 0;
     LAUNCH(rice_decode(stream, nbytes, k, n_symbols, width, height, ctx->rice, plane_out, &adler,

@@ -27,8 +27,21 @@
 //           k_adler       adler32 of the rebuilt plane (zlib.adler32 check)
 
 #include <cstdint>
+#include <cstdio>
 
 #include "fvv_codec.cuh"
+
+#ifdef FVV_CODEC_TRACE
+#define TRACE_EV(name)                                                       \
+    do {                                                                     \
+        cudaEvent_t e_; cudaEventCreate(&e_); cudaEventRecord(e_, s);        \
+        cudaEventSynchronize(e_);                                            \
+        float ms_ = 0; cudaEventElapsedTime(&ms_, t0_, e_);                  \
+        fprintf(stderr, "[codec] %-10s %8.1f us\n", name, ms_ * 1e3f);       \
+    } while (0)
+#else
+#define TRACE_EV(name) do { } while (0)
+#endif
 
 namespace fvv {
 
@@ -270,8 +283,17 @@ __global__ void k_rice_sync(RiceChunks c, const long long *exit_prev, int *chang
     atomicAdd(changed, 1);
 }
 
+// Position of residual (row, col) in the rebuild's skewed layout: strip
+// (32 rows) by strip, step t = col + lane by step, 32 lanes contiguous, so the
+// wavefront's warp reads (and writes) 32 consecutive words per step.
+__device__ __forceinline__ long long skew_index(long long idx, int W) {
+    const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
+    const int lane = row & 31;
+    return ((long long)(row >> 5) * (W + 31) + col + lane) * 32 + lane;
+}
+
 // residuals of the first n symbols (zig-zag inverse, depthcodec.py:389)
-__global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long long n,
+__global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long long n, int W,
                             int32_t *res) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= c.nchunks) return;
@@ -282,7 +304,7 @@ __global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long l
         unsigned long long zz = 0;
         p += rice_one(c.s, c.nbytes, c.nbits, c.k, p, zz);
         const long long z = (long long)zz;
-        res[idx] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
+        res[skew_index((long long)idx, W)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
     }
 }
 
@@ -290,63 +312,101 @@ __global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long l
 // on one plane per CTA. Warp w rebuilds 32-row strips w, w+32, ...; lane l
 // holds row 32*strip + l and reaches column j at step j + l, so its up and
 // up-left neighbours are lane l-1's values of the two previous steps
-// (shuffles). Lane 0 reads them from the previous strip's last row, which
-// that strip publishes column by column into one of two shared-memory row
-// slots, with a per-strip progress counter. Two row slots are enough: strip
-// S+1 overwrites column j of slot (S+1)%2 only after its lane 0 consumed
-// column j of strip S, i.e. after strip S's lane 0 read column j of strip
-// S-1 from that slot. (A shared progress word per slot would not do: strip
-// S+1's progress could then satisfy strip S's wait for strip S-1.)
+// (shuffles). Lane 0 takes them from the previous strip's last row, which
+// that strip's lane 31 publishes column by column into one of two shared-
+// memory row slots as 64-bit (strip tag << 32 | x) words: one aligned 8-byte
+// store is atomic, so the consumer spins on the word itself and needs no
+// fence. Two slots are enough: strip S+1 overwrites column j of slot (S+1)%2
+// only after its lane 0 consumed column j of strip S, i.e. after strip S's
+// lane 0 read column j of strip S-1 from that slot.
+#ifndef FVV_MED_SLEEP
+#define FVV_MED_SLEEP 32
+#endif
+#ifndef FVV_MED_PF
+#define FVV_MED_PF 4
+#endif
+constexpr int kPf = FVV_MED_PF;  // residual prefetch depth of the MED rebuild
+
 __global__ void __launch_bounds__(1024, 1) k_med_rebuild(const int32_t *res, int W, int H,
-                                                         uint8_t *out) {
-    extern __shared__ int32_t s_rows[];         // [2][W] last rows of strips
-    __shared__ volatile int s_prog[kMedMaxStrips];  // columns published per strip
+                                                         uint8_t *out_skew) {
+    extern __shared__ long long s_rows[];       // [2][W] (strip << 32 | x)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nstrips = (H + 31) / 32;
-    for (int i = threadIdx.x; i < kMedMaxStrips; i += blockDim.x) s_prog[i] = 0;
+    for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) s_rows[i] = -1ll << 32;
     __syncthreads();
+    volatile long long *vrows = s_rows;
     for (int strip = warp; strip < nstrips; strip += 32) {
         const int row = strip * 32 + lane;
         const bool live = row < H;
         const int slot = strip & 1, pslot = slot ^ 1;
         int cur = 0, prev = 0;   // this lane's x at columns j-1 and j-2
+        int bprev = 0;           // lane 0: the previous strip's x at column j-1
         const int steps = W + 31;
-        for (int t = 0; t < steps; ++t) {
-            const int j = t - lane;
-            // up / up-left: lane l-1's values from the last two steps
-            const int up_l = __shfl_up_sync(0xffffffffu, cur, 1);
-            const int upl_l = __shfl_up_sync(0xffffffffu, prev, 1);
-            int x = 0;
-            if (j >= 0 && j < W && live) {
-                int b, c;
-                if (lane == 0) {
-                    if (strip == 0) {
-                        b = 0;
-                        c = 0;
+        // residuals and outputs in the skewed layout (skew_index): step t of
+        // this strip is 32 consecutive words / bytes. The residuals stream
+        // through a kPf-deep register window loaded kPf steps ahead.
+        const long long sbase = (long long)strip * (W + 31) * 32 + lane;
+        int32_t win[kPf];
+#pragma unroll
+        for (int q = 0; q < kPf; ++q) {
+            const int jq = q - lane;
+            win[q] = (live && jq >= 0 && jq < W) ? __ldg(res + sbase + (long long)q * 32) : 0;
+        }
+        // unrolled by kPf so window slot u is consumed at step t0 + u and
+        // refilled for step t0 + u + kPf: each load has kPf steps to land
+        for (int t0 = 0; t0 < steps; t0 += kPf) {
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                const int t = t0 + u;
+                if (t >= steps) break;
+                const int j = t - lane;
+                // up / up-left: lane l-1's values from the last two steps
+                const int up_l = __shfl_up_sync(0xffffffffu, cur, 1);
+                const int upl_l = __shfl_up_sync(0xffffffffu, prev, 1);
+                int x = 0;
+                if (j >= 0 && j < W && live) {
+                    int b, c;
+                    if (lane == 0) {
+                        if (strip == 0) {
+                            b = 0;
+                        } else {
+                            long long w;
+                            // a waiting lane backs off, leaving issue slots
+                            // to the producing warps on the same SM
+                            while ((int)((w = vrows[pslot * W + j]) >> 32) != strip - 1)
+                                __nanosleep(FVV_MED_SLEEP);
+                            b = (int)(uint32_t)w;
+                        }
+                        c = j > 0 ? bprev : 0;
+                        bprev = b;
                     } else {
-                        while (s_prog[strip - 1] <= j) { }
-                        b = s_rows[pslot * W + j];
-                        c = j > 0 ? s_rows[pslot * W + j - 1] : 0;
+                        b = up_l;
+                        c = j > 0 ? upl_l : 0;
                     }
-                } else {
-                    b = up_l;
-                    c = j > 0 ? upl_l : 0;
+                    const int a = j > 0 ? cur : 0;
+                    x = win[u] + med(a, b, c);
+                    out_skew[sbase + (long long)t * 32] = (uint8_t)x;   // astype(uint8): mod 256
+                    if (lane == 31 && strip + 1 < nstrips)
+                        vrows[slot * W + j] = ((long long)strip << 32) | (uint32_t)x;
                 }
-                const int a = j > 0 ? cur : 0;
-                x = res[(long long)row * W + j] + med(a, b, c);
-                out[(long long)row * W + j] = (uint8_t)x;   // astype(uint8): modulo 256
-                if (lane == 31 && strip + 1 < nstrips) {
-                    s_rows[slot * W + j] = x;
-                    __threadfence_block();
-                    s_prog[strip] = j + 1;
+                if (j >= 0 && j < W) {
+                    prev = cur;
+                    cur = x;
                 }
-            }
-            if (j >= 0 && j < W) {
-                prev = cur;
-                cur = x;
+                const int jn = j + kPf;
+                win[u] = (live && jn >= 0 && jn < W)
+                             ? __ldg(res + sbase + (long long)(t + kPf) * 32) : 0;
             }
         }
     }
+}
+
+// skewed rebuild output -> raster plane
+__global__ void k_deskew(const uint8_t *skew, int W, int H, uint8_t *out) {
+    const long long n = (long long)W * H;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = skew[skew_index(i, W)];
 }
 
 // adler32 (zlib) of n bytes: A = 1 + sum d_i, B = n + sum (n - i) d_i, mod 65521
@@ -415,8 +475,15 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
     c.count = sc.count;
     c.trunc = sc.trunc;
     const unsigned g = (unsigned)((c.nchunks + 127) / 128);
+#ifdef FVV_CODEC_TRACE
+    cudaEvent_t t0_;
+    cudaEventCreate(&t0_);
+    cudaEventRecord(t0_, s);
+    int rounds_ = 0;
+#endif
     if (c.nchunks) {
         k_rice_spec<<<g, 128, 0, s>>>(c);
+        TRACE_EV("spec");
         for (int round = 0;; ++round) {
             if ((e = cudaMemcpyAsync(sc.exit_prev, sc.exit, sizeof(long long) * c.nchunks,
                                      cudaMemcpyDeviceToDevice, s)))
@@ -427,6 +494,10 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
             if ((e = cudaMemcpyAsync(&changed, sc.changed, sizeof(int), cudaMemcpyDeviceToHost, s)))
                 return e;
             if ((e = cudaStreamSynchronize(s))) return e;
+#ifdef FVV_CODEC_TRACE
+            ++rounds_;
+            fprintf(stderr, "[codec] round %d changed %d\n", rounds_, changed);
+#endif
             if (!changed) break;
             if (round > c.nchunks) return cudaErrorUnknown;  // cannot happen: one chunk per round
         }
@@ -442,9 +513,19 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
     if ((e = cudaMemcpyAsync(&total, sc.total, sizeof(total), cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
     if ((long long)total < n) { *status = 1; return cudaSuccess; }   // stream runs out early
-    if (c.nchunks) k_rice_emit<<<g, 128, 0, s>>>(c, sc.block, n, sc.res);
-    const size_t smem = (size_t)2 * W * sizeof(int32_t);
-    k_med_rebuild<<<1, 1024, smem, s>>>(sc.res, W, H, plane);
+    TRACE_EV("sync+scan");
+    if (c.nchunks) k_rice_emit<<<g, 128, 0, s>>>(c, sc.block, n, W, sc.res);
+    TRACE_EV("emit");
+    const size_t smem = (size_t)2 * W * sizeof(long long);
+    static int smem_set = 0;
+    if ((int)smem > smem_set && smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_med_rebuild, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        smem_set = (int)smem;
+    }
+    k_med_rebuild<<<1, 1024, smem, s>>>(sc.res, W, H, sc.skew);
+    k_deskew<<<148 * 4, 256, 0, s>>>(sc.skew, W, H, plane);
+    TRACE_EV("rebuild");
     if ((e = cudaMemsetAsync(sc.costs, 0, 2 * sizeof(unsigned long long), s))) return e;
     k_adler<<<148 * 4, 256, 0, s>>>(plane, n, sc.costs);
     unsigned long long ab[2];

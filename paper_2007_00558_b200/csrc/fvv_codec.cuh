@@ -8,12 +8,13 @@ namespace fvv {
 
 constexpr int kRiceKMax = 14;          // depthcodec.py:380: k in range(15)
 constexpr int kRiceChunkBits = 256;    // decode chunk (speculative segmentation unit)
-constexpr int kMedMaxStrips = 512;     // MED rebuild: 32-row strips per plane (H <= 16384)
+constexpr int kMedMaxWidth = 12288;    // MED rebuild: 2 x W x 8 B of row slots in shared memory
 
 // per-context device scratch, sized for n pixels / c chunks
 struct RiceScratch {
     uint16_t *zz = nullptr;                 // [n] encoder symbols
-    int32_t *res = nullptr;                 // [n] decoder residuals
+    int32_t *res = nullptr;                 // [skewed n] decoder residuals (rice_skew_size)
+    uint8_t *skew = nullptr;                // [skewed n] rebuilt plane, skewed layout
     unsigned long long *block = nullptr;    // [max(n/1024, c) + 1] scan buffer
     unsigned long long *costs = nullptr;    // [16] per-k costs / adler sums
     unsigned long long *total = nullptr;    // [1]
@@ -36,6 +37,11 @@ cudaError_t rice_encode(const uint8_t *plane, int W, int H, RiceScratch &sc, uin
 cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long long n, int W, int H,
                         RiceScratch &sc, uint8_t *plane, uint32_t *adler_out, int *status,
                         cudaStream_t s);
+
+// elements of the rebuild's skewed layout for a W x H plane
+inline size_t rice_skew_size(int W, int H) {
+    return (size_t)((H + 31) / 32) * (size_t)(W + 31) * 32;
+}
 
 // bytes `stream` must hold for a W x H plane: the cheapest k costs at most
 // what k = 8 does (<= 10 bits per symbol for zz <= 510), plus a spill word
