@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     const PreprocCore &p = batch.cam[blockIdx.z];
     const BilateralParams &bl = batch.bil;
     __shared__ __align__(8) uint8_t sv[PSR * PSC + 8];
-    __shared__ int s_holes;
+    __shared__ int s_holes, s_base;
+    __shared__ int s_wcnt[PY];
 
     const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
             sv[ry * SC + rx] = vv;
         }
         __syncthreads();
+        unsigned cm[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             bool cand = false;
@@ -268,13 +270,29 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                 }
                 cand = cnt >= bl.min_valid;
             }
-            const unsigned m = __ballot_sync(0xffffffffu, cand);
-            int base = 0;
-            if (lane == 0 && m) base = atomicAdd(batch.ncand, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (cand)
-                batch.cand[base + __popc(m & ((1u << lane) - 1u))] =
+            cm[q] = __ballot_sync(0xffffffffu, cand);
+        }
+        // one global atomic per tile (a single list counter is hit by every
+        // tile with candidates): warp counts -> tile prefix -> list slots
+        if (lane == 0) s_wcnt[ty] = __popc(cm[0]) + __popc(cm[1]) + __popc(cm[2]) + __popc(cm[3]);
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < PY; ++w) {
+                const int c = s_wcnt[w];
+                s_wcnt[w] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(batch.ncand, tot) : 0;
+        }
+        __syncthreads();
+        int base = s_base + s_wcnt[ty];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((cm[q] >> lane) & 1u)
+                batch.cand[base + __popc(cm[q] & ((1u << lane) - 1u))] =
                     ((uint32_t)blockIdx.z << 26) | (uint32_t)(rowbase + xb + q);
+            base += __popc(cm[q]);
         }
     }
 
@@ -343,6 +361,55 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
         load_depth(p, qy, qx, z, v, nullptr);
         ok = v == FVV_VALID;
         if (ok) g = load_rgb(p, (size_t)qy * p.W + qx);
+    }
+}
+
+// Radius 2 (the reference default, depthproc.py:173): one thread per
+// candidate with all 24 taps' loads issued before any is used, then all 24
+// table reads, then the ordered accumulation in registers: two memory round
+// trips per candidate and no cross-lane traffic.
+__device__ __forceinline__ void fill_r2(const BilateralParams &bl, const PreprocCore &p, int i) {
+    const int y = i / p.W, x = i - y * p.W;
+    const uchar4 gc = load_rgb(p, (size_t)i);
+    float zt[24];
+    bool ok[24];
+    int d2[24];
+#pragma unroll
+    for (int k = 0; k < 24; ++k) {
+        const int kk = k < 12 ? k : k + 1;  // skip the centre
+        uchar4 n4;
+        fill_tap(p, x, y, kk / 5 - 2, kk % 5 - 2, zt[k], ok[k], n4);
+        const int e0 = gc.x - n4.x, e1 = gc.y - n4.y, e2 = gc.z - n4.z;
+        d2[k] = e0 * e0 + e1 * e1 + e2 * e2;
+    }
+    double rw[24];
+#pragma unroll
+    for (int k = 0; k < 24; ++k) rw[k] = ok[k] ? __ldg(bl.range_w + d2[k]) : 0.0;
+    double num = 0.0, den = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 24; ++k) {
+        const int kk = k < 12 ? k : k + 1;
+        if (!ok[k]) continue;
+        const double w = dmul(bl.sw[kk / 5][kk % 5], rw[k]);
+        num = dadd(num, dmul(w, (double)zt[k]));
+        den = dadd(den, w);
+        ++cnt;
+    }
+    if (!(cnt >= bl.min_valid && den > 0.0)) return;
+    const float z = __double2float_rn(ddiv(num, den));
+    if (p.depth_out) p.depth_out[i] = z;
+    if (p.validity_out) p.validity_out[i] = FVV_VALID;
+    if (p.warp_depth) p.warp_depth[i] = z;
+    if (p.texel && !p.color_valid)
+        reinterpret_cast<uint8_t *>(p.texel + i)[3] = (uint8_t)kFlagLiveValid;
+}
+
+__global__ void __launch_bounds__(128) k_fill_r2(const __grid_constant__ PreprocBatch batch) {
+    const int n = *batch.ncand;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const uint32_t ent = batch.cand[e];
+        fill_r2(batch.bil, batch.cam[ent >> 26], (int)(ent & ((1u << 26) - 1)));
     }
 }
 
@@ -419,6 +486,10 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
     dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
     k_preprocess<<<grid, 256, 0, s>>>(b);
     if (fill) {
+#ifdef FVV_FILL_THREAD
+        if (b.bil.radius == 2) k_fill_r2<<<148 * 4, 128, 0, s>>>(b);
+        else
+#endif
         k_fill<<<148 * 8, 256, 0, s>>>(b);
         ++t_extra_launches;
     }
