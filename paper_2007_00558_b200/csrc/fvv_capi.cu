@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -59,6 +60,10 @@ struct fvv_ctx {
     uint8_t *iprov = nullptr;
     float *idepth = nullptr;
     size_t icap = 0;
+    // K3's TMA map of the canvases and what it was built for
+    CUtensorMap kmap;
+    const void *kmap_base = nullptr;
+    long long kmap_pitch = 0, kmap_rows = 0, kmap_n = 0, kmap_per = 0;
     // K1 candidate list (camera << 26 | pixel) + its length
     uint32_t *cand = nullptr;
     int *ncand = nullptr;
@@ -344,6 +349,51 @@ int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
     return FVV_OK;
 }
 
+// cuTensorMapEncodeTiled from the driver, through the runtime (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// K3's 3-D TMA map {pitch, rows, n} over the canvas allocation (cached)
+int canvas_tensor_map(fvv_ctx *ctx, int n, int W, int H, int r, ResolveParams &rp) {
+    const long long pitch = canvas_pitch(W, r), rows = H + 2 * r;
+    const long long per = (long long)canvas_per(W, H, r);
+    if (!(ctx->kmap_base == ctx->canvas && ctx->kmap_pitch == pitch && ctx->kmap_rows == rows &&
+          ctx->kmap_n == n && ctx->kmap_per == per)) {
+        auto enc = tensor_map_encoder();
+        if (!enc) return fail(ctx, FVV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)rows, (cuuint64_t)n};
+        const cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)per * 8};
+        const cuuint32_t box[3] = {36, 12, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult e = enc(&ctx->kmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, ctx->canvas, dims,
+                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (e != CUDA_SUCCESS) return fail(ctx, FVV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)e);
+        ctx->kmap_base = ctx->canvas;
+        ctx->kmap_pitch = pitch;
+        ctx->kmap_rows = rows;
+        ctx->kmap_n = n;
+        ctx->kmap_per = per;
+    }
+    rp.kmap = ctx->kmap;
+    rp.has_kmap = 1;
+    return FVV_OK;
+}
+
 double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
     const double dx = a.C[0] - b.C[0], dy = a.C[1] - b.C[1], dz = a.C[2] - b.C[2];
     return 1.0 / (std::sqrt((dx * dx + dy * dy) + dz * dz) + eps);
@@ -425,6 +475,9 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         ip.prov = rp.prov_out;
         ip.depth = ctx->idepth;
     }
+    if (r == 1 && resolve_uses_tma() &&
+        (rc = canvas_tensor_map(ctx, ctx->cn, virt.width, virt.height, r, rp)))
+        return rc;
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
     if (ip.rgb) LAUNCH(launch_inpaint(ip, ctx->stream));
@@ -1082,6 +1135,9 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.c[0] = ResolveContrib{s.dev, s.texel, ctx->zsrc, ctx->canvas + 1,
                              host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
                              layer_fg ? 1 : 0};
+    if (r == 1 && resolve_uses_tma() &&
+        (rc = canvas_tensor_map(ctx, ctx->cn, dst->width, dst->height, r, rp)))
+        return rc;
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
     return FVV_OK;
 }

@@ -977,6 +977,43 @@ __device__ __forceinline__ void stage_keys(uint64_t *dst, const uint64_t *canvas
     }
 }
 
+// TMA (cp.async.bulk.tensor) staging of a key tile with mbarrier completion:
+// one elected thread issues a 36 x 12 box of the 3-D canvas map; every
+// thread waits on the buffer's mbarrier with the item's phase parity.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            int c2, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 // exact f64 z of a winner index: the value K2 computed and stored for it
 __device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &,
                                            uint32_t idx) {
@@ -1140,6 +1177,11 @@ __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst
 #ifndef FVV_K3_NBUF
 #define FVV_K3_NBUF 2
 #endif
+// K3 key staging: 0 = cp.async (default: measured 3 % faster at c1 than the
+// TMA + mbarrier variant, 224 vs 231 us), 1 = cp.async.bulk.tensor (TMA)
+#ifndef FVV_K3_TMA
+#define FVV_K3_TMA 0
+#endif
 constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of the one shaded)
 
 // One 32x8 tile per CTA; the 12x36 key tiles of the next three contributions
@@ -1148,7 +1190,8 @@ constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of
 // per-pixel work of contribution q.
 template <int MAXR, bool DBG, bool ANG>
 __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[NBUF];                // TMA completion per buffer
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
     uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
@@ -1175,6 +1218,30 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     if (tid < TX) sray[tid] = ddiv(dsub((double)(x0 + tid), dst.cx), dst.fx);
     else if (tid < TX + TY) sray[tid] = ddiv(dsub((double)(y0 + tid - TX), dst.cy), dst.fy);
 
+#if FVV_K3_TMA
+    // key tiles by TMA: thread 0 arms buffer q % NBUF's mbarrier and issues
+    // the box; canvas column x0-1 .. x0+34 is tensor x = x0 .. x0+35 (the
+    // allocation's +1 offset), out-of-canvas boxes are zero-filled (they only
+    // feed out-of-image cells, which are never resolved)
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(&s_bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto stage = [&](int q) {
+        if (tid == 0 && q < nitems) {
+            uint64_t *bar = &s_bar[q % NBUF];
+            mbar_expect_tx(bar, FKEYS * sizeof(uint64_t));
+            tma_load_3d(sk + (q % NBUF) * FKEYS, &p.kmap, x0, y0 - 1, q, bar);
+        }
+    };
+    auto wait_keys = [&](int q) {
+        if (q < nitems) mbar_wait(&s_bar[q % NBUF], (unsigned)((q / NBUF) & 1));
+    };
+#pragma unroll
+    for (int q = 0; q < NBUF; ++q) stage(q);
+    wait_keys(0);
+#else
     auto stage = [&](int q) {
         if (q < nitems) stage_keys(sk + (q % NBUF) * FKEYS, p.c[q].canvas, x0, y0, P, Hc, tid);
         cp_async_commit();  // (possibly empty) group per item keeps the accounting uniform
@@ -1184,6 +1251,7 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     for (int q = 0; q < NBUF; ++q) stage(q);
     cp_async_wait<NBUF - 1>();
     __syncthreads();
+#endif
     int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
     bool fv = false, bv = false;
@@ -1195,10 +1263,19 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         const int j = fgl ? k : k - p.n_fg;
         // keys of q+1 must have landed (groups q+1 done, q+2 may pend); cells of q
         // complete
+#if FVV_K3_TMA
+        wait_keys(q + 1);
+        const int any = __syncthreads_or(any_next);
+        // keys of q+NBUF into the buffer item q's cells phase used (all reads of
+        // it by the generic proxy are ordered before the barrier above)
+        if (tid == 0) fence_proxy_async();
+        stage(q + NBUF);
+#else
         cp_async_wait<NBUF - 2>();
         const int any = __syncthreads_or(any_next);
         // keys of q+NBUF into the buffer item q's cells phase (iteration q-1) used
         stage(q + NBUF);
+#endif
         // cells of q+1 (other warps' per-pixel work of q overlaps it)
         any_next = 0;
         if (q + 1 < nitems)
@@ -1324,7 +1401,9 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
                 p.depth_out[pix] = (float)(fv ? sfg[3 * NT + tid] : (bv ? sbg[3 * NT + tid] : 0.0));
         }
     }
+#if !FVV_K3_TMA
     cp_async_wait<0>();
+#endif
 }
 
 template <typename K>
@@ -1361,13 +1440,15 @@ static void launch_fast_r(const ResolveParams &p, bool dbg, dim3 grid, cudaStrea
 }
 
 
+bool resolve_uses_tma() { return FVV_K3_TMA != 0; }
+
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     dim3 grid((p.dst.W + TX - 1) / TX, (p.dst.H + TY - 1) / TY);
     const int maxn = p.n_fg > p.n_bg ? p.n_fg : p.n_bg;
     const bool dbg = p.dbg.contrib_color || p.dbg.contrib_depth || p.dbg.contrib_valid ||
                      p.dbg.contrib_winner || p.dbg.contrib_stage || p.dbg.merged_color ||
                      p.dbg.merged_depth || p.dbg.merged_valid;
-    if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0) {
+    if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0 && (p.has_kmap || !FVV_K3_TMA)) {
         if (maxn <= 3) launch_fast_r<3>(p, dbg, grid, s);
         else if (maxn <= 4) launch_fast_r<4>(p, dbg, grid, s);
         else launch_fast_r<FVV_MAX_REFS>(p, dbg, grid, s);

@@ -1,6 +1,8 @@
 // Kernel parameter blocks and host launchers (implemented in fvv_kernels.cu).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "fvv_common.cuh"
 
 namespace fvv {
@@ -97,6 +99,12 @@ struct ResolveContrib {
 };
 
 struct ResolveParams {
+    // TMA map of the keyed canvases: dims {pitch, Hd + 2r, n contributions}
+    // over the canvas allocation, so canvas element (k, cy, cx) is tensor
+    // element (cx + 1, cy, k) (the +1 allocation offset). Used by the fast
+    // path (r = 1, window 3) when has_kmap.
+    CUtensorMap kmap;
+    int has_kmap;
     DevCam dst;
     int r, window, need;
     int pitch;
@@ -142,6 +150,7 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s);
 cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s);
 cudaError_t launch_forward_warp(const WarpParams &p, long long max_src_pixels, cudaStream_t s);
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s);
+bool resolve_uses_tma();  // the fast path stages key tiles by TMA (needs ResolveParams::kmap)
 cudaError_t launch_mix(const MixParams &p, cudaStream_t s);
 cudaError_t launch_composite(const double *fg_c, const uint8_t *fg_v, const double *bg_c,
                              const uint8_t *bg_v, int W, int H, const double hole[3],
