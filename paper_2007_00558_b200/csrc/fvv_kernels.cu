@@ -1117,7 +1117,8 @@ double crack_z(const ResolveContrib &c, const DevCam &dst,
     cswap(v1, v2); cswap(v3, v4); cswap(v5, v6);
     *stage = kStageCrack;
     const double lo = cnt <= 6 ? v2 : v3;
-    return (cnt & 1) ? lo : ddiv(dadd(lo, cnt == 6 ? v3 : v4), 2.0);
+    // even count: mean of the middle pair; halving is exact, so * 0.5 == / 2
+    return (cnt & 1) ? lo : dmul(dadd(lo, cnt == 6 ? v3 : v4), 0.5);
 }
 
 // backward projection + masked bilinear fetch of one covered pixel

@@ -30,8 +30,18 @@ from .types import ColorFrame
 
 class EdgeRenderer:
     def __init__(self, rig: Sequence, bg_models: Optional[Mapping] = None,
-                 cfg: Optional[SynthesisConfig] = None, device: Optional[int] = None):
-        self.ctx = _native.context(device)
+                 cfg: Optional[SynthesisConfig] = None, device: Optional[int] = None,
+                 private: bool = False):
+        """``private=True`` gives the renderer its own library context (own
+        slots, canvases and stream binding), so several renderers can work on
+        different frames concurrently on different CUDA streams; the default
+        shares the device's context."""
+        if private:
+            import torch
+
+            self.ctx = _native.Context(torch.cuda.current_device() if device is None else device)
+        else:
+            self.ctx = _native.context(device)
         self.cfg = cfg or SynthesisConfig()
         self.rig = list(rig)
         self.by_id = {c.id: c for c in self.rig}

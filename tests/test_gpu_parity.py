@@ -244,3 +244,27 @@ def test_batched_ingest_equals_per_camera_ingest(cuda):
     np.testing.assert_array_equal(outs[0], outs[1])
     o_rgb, _ = O.es_view(wl.virtuals[0], _es_frames(wl))
     np.testing.assert_array_equal(outs[1], o_rgb)
+
+
+def test_private_renderers_on_two_streams_match(cuda):
+    """Two private renderers (own contexts) working on alternating frames on
+    their own CUDA streams (bench.py --pipelines) give the shared renderer's
+    views."""
+    import torch
+
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    wl = workload("c2", 8, 2007)
+    ref = _renderer(wl).render(wl.virtuals, wl.refs).cpu().numpy()
+    engs = [EdgeRenderer(wl.rig, private=True) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = []
+    for i, (e, st) in enumerate(zip(engs, streams)):
+        with torch.cuda.stream(st):
+            for cid, c in wl.frames[0].items():
+                e.set_bg_model(cid, c.bg_depth, c.bg_validity)
+                e.ingest_mm(cid, c.rgb, c.mm, c.validity, hole_closing=True)
+            outs.append(e.render(wl.virtuals[i::2], wl.refs[i::2]))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(outs[0].cpu().numpy(), ref[0::2])
+    np.testing.assert_array_equal(outs[1].cpu().numpy(), ref[1::2])
