@@ -1314,15 +1314,17 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         }
         if (!ok) { c0 = c1 = c2 = 0.0; }
         const double zd = ok ? z : 0.0;
-        sres[(j * 4 + 0) * NT + tid] = c0;
-        sres[(j * 4 + 1) * NT + tid] = c1;
-        sres[(j * 4 + 2) * NT + tid] = c2;
-        sres[(j * 4 + 3) * NT + tid] = zd;
-        if (ANG)
-            swt[j * NT + tid] = ok ? c.weight * angular_factor(dst, c.src, sray[tx], sray[TX + ty],
-                                                               z, p.ang_eps)
-                                   : c.weight;
-        if (ok) vmask |= 1u << j;
+        // the mixes read only contributions whose vmask bit is set
+        if (ok) {
+            sres[(j * 4 + 0) * NT + tid] = c0;
+            sres[(j * 4 + 1) * NT + tid] = c1;
+            sres[(j * 4 + 2) * NT + tid] = c2;
+            sres[(j * 4 + 3) * NT + tid] = zd;
+            if (ANG)
+                swt[j * NT + tid] =
+                    c.weight * angular_factor(dst, c.src, sray[tx], sray[TX + ty], z, p.ang_eps);
+            vmask |= 1u << j;
+        }
         if (DBG && inimg) {
             const size_t o = (size_t)k * plane + pix;
             if (p.dbg.contrib_color) {
@@ -1340,16 +1342,19 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         if (last) {
             const int n = j + 1;
             const int kb = k - j;
+            // valid contributions only, in ascending (reference) order
             double zmin = INFINITY;
-            for (int qq = 0; qq < n; ++qq) {
+            for (unsigned m = vmask; m; m &= m - 1) {
+                const int qq = __ffs(m) - 1;
                 const double zj = sres[(qq * 4 + 3) * NT + tid];
-                if (((vmask >> qq) & 1u) && zj < zmin) zmin = zj;
+                if (zj < zmin) zmin = zj;
             }
             const double thr = dadd(zmin, dmul(p.band_rel, zmin));
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
-            for (int qq = 0; qq < n; ++qq) {
+            for (unsigned m = vmask; m; m &= m - 1) {
+                const int qq = __ffs(m) - 1;
                 const double zj = sres[(qq * 4 + 3) * NT + tid];
-                if (((vmask >> qq) & 1u) && zj <= thr) {
+                if (zj <= thr) {
                     const double w = ANG ? swt[qq * NT + tid] : p.c[kb + qq].weight;
                     a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * NT + tid]));
                     a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * NT + tid]));
