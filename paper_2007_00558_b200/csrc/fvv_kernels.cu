@@ -198,8 +198,11 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
 #pragma unroll
         for (int q = 0; q < 4; ++q) sv[(ty + R) * SC + lane * 4 + q + R] = val[q];
         const int SR = PY + 2 * R;
-        const int ring = vec && R == 2 ? 0 : SR * SC - PY * PX;
-        if (vec && R == 2) {
+        // block-uniform choice (a thread's own `vec` is false on rows / columns
+        // past the image, which must not change how the halo is split up)
+        const bool hvec = R == 2 && (p.W & 3) == 0 && p.src == kSrcMM && p.validity;
+        const int ring = hvec ? 0 : SR * SC - PY * PX;
+        if (hvec) {
             // halo validity with 16-byte-group loads: rows y0-2, y0-1, y0+8,
             // y0+9 as 34 aligned 4-px groups each (columns x0-4 .. x0+131),
             // then the 2-px side columns of the 8 tile rows
@@ -405,6 +408,63 @@ __device__ __forceinline__ void fill_r2(const BilateralParams &bl, const Preproc
         reinterpret_cast<uint8_t *>(p.texel + i)[3] = (uint8_t)kFlagLiveValid;
 }
 
+// Radius 2, the default: 4 candidates per warp, 8 lanes per candidate, lane
+// t evaluating taps t, t+8, t+16 (loads + table read + weight products);
+// the products go through shared memory and the group's first lane adds the
+// 24 taps in the reference's order. All 4 groups accumulate in the same
+// instructions, so a candidate costs ~1/4 of a warp pass.
+__global__ void __launch_bounds__(256) k_fill_g8(const __grid_constant__ PreprocBatch batch) {
+    __shared__ double2 s_w[8][4][24];   // [warp][group][tap] = (w, w * z)
+    const BilateralParams &bl = batch.bil;
+    const int n = *batch.ncand;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 3, t = lane & 7;
+    const unsigned gmask = 0xFFu << (8 * g);
+    for (int base = (blockIdx.x * 8 + warp) * 4; base < n; base += gridDim.x * 8 * 4) {
+        const int e = base + g;
+        const bool live = e < n;
+        const uint32_t ent = live ? batch.cand[e] : 0u;
+        const PreprocCore &p = batch.cam[ent >> 26];
+        const int i = (int)(ent & ((1u << 26) - 1));
+        const int y = i / p.W, x = i - y * p.W;
+        const uchar4 gc = live ? load_rgb(p, (size_t)i) : make_uchar4(0, 0, 0, 0);
+        int cnt = 0;
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            const int k = t + 8 * m, kk = k < 12 ? k : k + 1;  // skip the centre
+            float zn = 0.0f;
+            bool ok = false;
+            uchar4 n4 = make_uchar4(0, 0, 0, 0);
+            if (live) fill_tap(p, x, y, kk / 5 - 2, kk % 5 - 2, zn, ok, n4);
+            double w = 0.0;
+            if (ok) {
+                const int e0 = gc.x - n4.x, e1 = gc.y - n4.y, e2 = gc.z - n4.z;
+                w = dmul(bl.sw[kk / 5][kk % 5], __ldg(bl.range_w + (e0 * e0 + e1 * e1 + e2 * e2)));
+            }
+            s_w[warp][g][k] = make_double2(w, dmul(w, (double)zn));
+            cnt += __popc(__ballot_sync(0xffffffffu, ok) & gmask);
+        }
+        __syncwarp();
+        if (t == 0 && live) {
+            double num = 0.0, den = 0.0;
+#pragma unroll
+            for (int k = 0; k < 24; ++k) {
+                const double2 v = s_w[warp][g][k];
+                num = dadd(num, v.y);
+                den = dadd(den, v.x);
+            }
+            if (cnt >= bl.min_valid && den > 0.0) {
+                const float z = __double2float_rn(ddiv(num, den));
+                if (p.depth_out) p.depth_out[i] = z;
+                if (p.validity_out) p.validity_out[i] = FVV_VALID;
+                if (p.warp_depth) p.warp_depth[i] = z;
+                if (p.texel && !p.color_valid)
+                    reinterpret_cast<uint8_t *>(p.texel + i)[3] = (uint8_t)kFlagLiveValid;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(128) k_fill_r2(const __grid_constant__ PreprocBatch batch) {
     const int n = *batch.ncand;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -490,7 +550,8 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
         if (b.bil.radius == 2) k_fill_r2<<<148 * 4, 128, 0, s>>>(b);
         else
 #endif
-        k_fill<<<148 * 8, 256, 0, s>>>(b);
+        if (b.bil.radius == 2) k_fill_g8<<<148 * 4, 256, 0, s>>>(b);
+        else k_fill<<<148 * 8, 256, 0, s>>>(b);
         ++t_extra_launches;
     }
     return cudaGetLastError();

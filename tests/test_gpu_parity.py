@@ -268,3 +268,37 @@ def test_private_renderers_on_two_streams_match(cuda):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(outs[0].cpu().numpy(), ref[0::2])
     np.testing.assert_array_equal(outs[1].cpu().numpy(), ref[1::2])
+
+
+@pytest.mark.parametrize("W,H", [(260, 36), (132, 20), (1000, 522)])
+def test_fused_ingest_fill_on_partial_tiles(cuda, W, H):
+    """K0's fused mm decode + candidate listing + K1 fill where the 128x8
+    tiles overhang the image (the halo split must not depend on which
+    threads lie inside): equal to the oracle's decode + bilateral."""
+    import torch
+
+    from paper_2007_00558_b200.engine import EdgeRenderer
+    from paper_2007_00558_b200.types import (CameraCalibration, CameraIntrinsics,
+                                             CameraPose)
+
+    rng = np.random.default_rng(W * 31 + H)
+    yy, xx = np.mgrid[0:H, 0:W]
+    mm = (2000 + 400 * np.sin(xx / 9.0) + 300 * np.cos(yy / 7.0)).astype(np.uint16)
+    val = np.where(rng.random((H, W)) < 0.15, 1, 0).astype(np.uint8)   # Invalid sprinkles
+    val[rng.random((H, W)) < 0.2] = 2
+    mm[val != 0] = 0
+    rgb = rng.integers(0, 256, (H, W, 3)).astype(np.uint8)
+    # smooth colour so many fills succeed (range weights do not underflow)
+    rgb[..., 0] = (xx * 3 % 256).astype(np.uint8)
+    cam = CameraCalibration(0, CameraIntrinsics(500.0, 500.0, W / 2, H / 2, W, H),
+                            CameraPose(np.eye(3), np.zeros(3)))
+    r = EdgeRenderer([cam])
+    d_out = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    v_out = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    for rep in range(3):
+        r.ingest_mm(0, rgb, mm, val, hole_closing=True, depth_out=d_out, validity_out=v_out)
+        d, v = O.decode_mm(mm, val)
+        od, ov, filled = O.bilateral_close_holes(d, v, rgb)
+        assert filled.any()
+        np.testing.assert_array_equal(v_out.cpu().numpy(), ov)
+        np.testing.assert_array_equal(d_out.cpu().numpy(), od)
