@@ -367,47 +367,6 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
     }
 }
 
-// Radius 2 (the reference default, depthproc.py:173): one thread per
-// candidate with all 24 taps' loads issued before any is used, then all 24
-// table reads, then the ordered accumulation in registers: two memory round
-// trips per candidate and no cross-lane traffic.
-__device__ __forceinline__ void fill_r2(const BilateralParams &bl, const PreprocCore &p, int i) {
-    const int y = i / p.W, x = i - y * p.W;
-    const uchar4 gc = load_rgb(p, (size_t)i);
-    float zt[24];
-    bool ok[24];
-    int d2[24];
-#pragma unroll
-    for (int k = 0; k < 24; ++k) {
-        const int kk = k < 12 ? k : k + 1;  // skip the centre
-        uchar4 n4;
-        fill_tap(p, x, y, kk / 5 - 2, kk % 5 - 2, zt[k], ok[k], n4);
-        const int e0 = gc.x - n4.x, e1 = gc.y - n4.y, e2 = gc.z - n4.z;
-        d2[k] = e0 * e0 + e1 * e1 + e2 * e2;
-    }
-    double rw[24];
-#pragma unroll
-    for (int k = 0; k < 24; ++k) rw[k] = ok[k] ? __ldg(bl.range_w + d2[k]) : 0.0;
-    double num = 0.0, den = 0.0;
-    int cnt = 0;
-#pragma unroll
-    for (int k = 0; k < 24; ++k) {
-        const int kk = k < 12 ? k : k + 1;
-        if (!ok[k]) continue;
-        const double w = dmul(bl.sw[kk / 5][kk % 5], rw[k]);
-        num = dadd(num, dmul(w, (double)zt[k]));
-        den = dadd(den, w);
-        ++cnt;
-    }
-    if (!(cnt >= bl.min_valid && den > 0.0)) return;
-    const float z = __double2float_rn(ddiv(num, den));
-    if (p.depth_out) p.depth_out[i] = z;
-    if (p.validity_out) p.validity_out[i] = FVV_VALID;
-    if (p.warp_depth) p.warp_depth[i] = z;
-    if (p.texel && !p.color_valid)
-        reinterpret_cast<uint8_t *>(p.texel + i)[3] = (uint8_t)kFlagLiveValid;
-}
-
 // Radius 2, the default: 4 candidates per warp, 8 lanes per candidate, lane
 // t evaluating taps t, t+8, t+16 (loads + table read + weight products);
 // the products go through shared memory and the group's first lane adds the
@@ -462,14 +421,6 @@ __global__ void __launch_bounds__(256) k_fill_g8(const __grid_constant__ Preproc
             }
         }
         __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(128) k_fill_r2(const __grid_constant__ PreprocBatch batch) {
-    const int n = *batch.ncand;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-        const uint32_t ent = batch.cand[e];
-        fill_r2(batch.bil, batch.cam[ent >> 26], (int)(ent & ((1u << 26) - 1)));
     }
 }
 
@@ -546,10 +497,6 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
     dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
     k_preprocess<<<grid, 256, 0, s>>>(b);
     if (fill) {
-#ifdef FVV_FILL_THREAD
-        if (b.bil.radius == 2) k_fill_r2<<<148 * 4, 128, 0, s>>>(b);
-        else
-#endif
         if (b.bil.radius == 2) k_fill_g8<<<148 * 4, 256, 0, s>>>(b);
         else k_fill<<<148 * 8, 256, 0, s>>>(b);
         ++t_extra_launches;
@@ -1009,8 +956,12 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 #ifndef FVV_K3_MINB
 #define FVV_K3_MINB 4
 #endif
-constexpr int FKR = TY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36
-constexpr int FBR = TY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+#ifndef FVV_K3_TY
+#define FVV_K3_TY 8
+#endif
+constexpr int FTY = FVV_K3_TY, FNT = TX * FTY;                   // fast-path tile: 32 x FTY
+constexpr int FKR = FTY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36 (FTY = 8)
+constexpr int FBR = FTY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
 constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
@@ -1100,7 +1051,7 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
     int any = 0;
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep) {
-        const int i = tid + rep * NT;
+        const int i = tid + rep * FNT;
         if (i >= FCELLS) break;
         const int by = i / FBC, bx = i - by * FBC;
         const int qy = y0 - 1 + by, qx = x0 - 1 + bx;
@@ -1251,22 +1202,22 @@ constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of
 // cells phase of contribution q+1 runs in the same barrier interval as the
 // per-pixel work of contribution q.
 template <int MAXR, bool DBG, bool ANG>
-__global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
+__global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[NBUF];                // TMA completion per buffer
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
     uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
-    double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][NT]
-    double *sfg = sres + MAXR * 4 * NT;                          // [4][NT] merged FG colour, z
-    double *sbg = sfg + 4 * NT;                                  // [4][NT] merged BG colour, z
-    double *sray = sbg + 4 * NT;                                 // [TX] rx, [TY] ry
-    double *swt = sray + TX + TY;                                // [MAXR][NT] weights (ANG)
-    uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (ANG ? MAXR * NT : 0));  // [2][FCELLS] (DBG)
+    double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][FNT]
+    double *sfg = sres + MAXR * 4 * FNT;                          // [4][FNT] merged FG colour, z
+    double *sbg = sfg + 4 * FNT;                                  // [4][FNT] merged BG colour, z
+    double *sray = sbg + 4 * FNT;                                 // [TX] rx, [FTY] ry
+    double *swt = sray + TX + FTY;                                // [MAXR][FNT] weights (ANG)
+    uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (ANG ? MAXR * FNT : 0));  // [2][FCELLS] (DBG)
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const DevCam &dst = p.dst;
     const int Wd = dst.W, Hd = dst.H;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * FTY;
     const int ix = x0 + tx, iy = y0 + ty;
     const bool inimg = ix < Wd && iy < Hd;
     const size_t pix = (size_t)iy * Wd + ix;
@@ -1278,7 +1229,7 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
     // virtual-camera rays of the tile's columns and rows (pixel_rays,
     // core.py:224-227), once per CTA
     if (tid < TX) sray[tid] = ddiv(dsub((double)(x0 + tid), dst.cx), dst.fx);
-    else if (tid < TX + TY) sray[tid] = ddiv(dsub((double)(y0 + tid - TX), dst.cy), dst.fy);
+    else if (tid < TX + FTY) sray[tid] = ddiv(dsub((double)(y0 + tid - TX), dst.cy), dst.fy);
 
 #if FVV_K3_TMA
     // key tiles by TMA: thread 0 arms buffer q % NBUF's mbarrier and issues
@@ -1377,12 +1328,12 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         const double zd = ok ? z : 0.0;
         // the mixes read only contributions whose vmask bit is set
         if (ok) {
-            sres[(j * 4 + 0) * NT + tid] = c0;
-            sres[(j * 4 + 1) * NT + tid] = c1;
-            sres[(j * 4 + 2) * NT + tid] = c2;
-            sres[(j * 4 + 3) * NT + tid] = zd;
+            sres[(j * 4 + 0) * FNT + tid] = c0;
+            sres[(j * 4 + 1) * FNT + tid] = c1;
+            sres[(j * 4 + 2) * FNT + tid] = c2;
+            sres[(j * 4 + 3) * FNT + tid] = zd;
             if (ANG)
-                swt[j * NT + tid] =
+                swt[j * FNT + tid] =
                     c.weight * angular_factor(dst, c.src, sray[tx], sray[TX + ty], z, p.ang_eps);
             vmask |= 1u << j;
         }
@@ -1407,19 +1358,19 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
             double zmin = INFINITY;
             for (unsigned m = vmask; m; m &= m - 1) {
                 const int qq = __ffs(m) - 1;
-                const double zj = sres[(qq * 4 + 3) * NT + tid];
+                const double zj = sres[(qq * 4 + 3) * FNT + tid];
                 if (zj < zmin) zmin = zj;
             }
             const double thr = dadd(zmin, dmul(p.band_rel, zmin));
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
             for (unsigned m = vmask; m; m &= m - 1) {
                 const int qq = __ffs(m) - 1;
-                const double zj = sres[(qq * 4 + 3) * NT + tid];
+                const double zj = sres[(qq * 4 + 3) * FNT + tid];
                 if (zj <= thr) {
-                    const double w = ANG ? swt[qq * NT + tid] : p.c[kb + qq].weight;
-                    a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * NT + tid]));
-                    a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * NT + tid]));
-                    a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * NT + tid]));
+                    const double w = ANG ? swt[qq * FNT + tid] : p.c[kb + qq].weight;
+                    a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * FNT + tid]));
+                    a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * FNT + tid]));
+                    a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * FNT + tid]));
                     if (DBG || p.depth_out) ad = dadd(ad, dmul(w, zj));
                     aw = dadd(aw, w);
                 }
@@ -1434,9 +1385,9 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
             }
             double *sl = fgl ? sfg : sbg;
             sl[tid] = m0;
-            sl[NT + tid] = m1;
-            sl[2 * NT + tid] = m2;
-            if (p.depth_out) sl[3 * NT + tid] = mv ? ddiv(ad, aw) : 0.0;
+            sl[FNT + tid] = m1;
+            sl[2 * FNT + tid] = m2;
+            if (p.depth_out) sl[3 * FNT + tid] = mv ? ddiv(ad, aw) : 0.0;
             if (fgl) fv = mv;
             else bv = mv;
             vmask = 0;
@@ -1454,8 +1405,8 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
         // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
         if (k == ntot - 1 && inimg) {
             double o0, o1, o2;
-            if (fv) { o0 = sfg[tid]; o1 = sfg[NT + tid]; o2 = sfg[2 * NT + tid]; }
-            else if (bv) { o0 = sbg[tid]; o1 = sbg[NT + tid]; o2 = sbg[2 * NT + tid]; }
+            if (fv) { o0 = sfg[tid]; o1 = sfg[FNT + tid]; o2 = sfg[2 * FNT + tid]; }
+            else if (bv) { o0 = sbg[tid]; o1 = sbg[FNT + tid]; o2 = sbg[2 * FNT + tid]; }
             else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
             if (p.rgb_out) {
                 uint8_t *o = p.rgb_out + pix * 3;
@@ -1465,7 +1416,7 @@ __global__ void __launch_bounds__(NT, FVV_K3_MINB) k_resolve_fast(const __grid_c
             }
             if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
             if (p.depth_out)
-                p.depth_out[pix] = (float)(fv ? sfg[3 * NT + tid] : (bv ? sbg[3 * NT + tid] : 0.0));
+                p.depth_out[pix] = (float)(fv ? sfg[3 * FNT + tid] : (bv ? sbg[3 * FNT + tid] : 0.0));
         }
     }
 #if !FVV_K3_TMA
@@ -1481,8 +1432,8 @@ static void raise_smem(K kernel, size_t bytes) {
 template <int MAXR, bool ANG>
 static size_t fast_smem() {
     return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
-           (size_t)MAXR * 4 * NT * sizeof(double) + (8 * NT + TX + TY) * sizeof(double) +
-           (ANG ? (size_t)MAXR * NT * sizeof(double) : 0) + 2 * FCELLS;
+           (size_t)MAXR * 4 * FNT * sizeof(double) + (8 * FNT + TX + FTY) * sizeof(double) +
+           (ANG ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
 }
 
 template <int MAXR, bool DBG, bool ANG>
@@ -1492,7 +1443,7 @@ static void launch_fast(const ResolveParams &p, dim3 grid, cudaStream_t s) {
         raise_smem(k_resolve_fast<MAXR, DBG, ANG>, fast_smem<MAXR, ANG>());
         init = true;
     }
-    k_resolve_fast<MAXR, DBG, ANG><<<grid, NT, fast_smem<MAXR, ANG>(), s>>>(p);
+    k_resolve_fast<MAXR, DBG, ANG><<<grid, FNT, fast_smem<MAXR, ANG>(), s>>>(p);
 }
 
 template <int MAXR>
@@ -1511,14 +1462,15 @@ bool resolve_uses_tma() { return FVV_K3_TMA != 0; }
 
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     dim3 grid((p.dst.W + TX - 1) / TX, (p.dst.H + TY - 1) / TY);
+    dim3 fgrid((p.dst.W + TX - 1) / TX, (p.dst.H + FTY - 1) / FTY);
     const int maxn = p.n_fg > p.n_bg ? p.n_fg : p.n_bg;
     const bool dbg = p.dbg.contrib_color || p.dbg.contrib_depth || p.dbg.contrib_valid ||
                      p.dbg.contrib_winner || p.dbg.contrib_stage || p.dbg.merged_color ||
                      p.dbg.merged_depth || p.dbg.merged_valid;
     if (p.r == 1 && p.window == 3 && p.n_fg + p.n_bg > 0 && (p.has_kmap || !FVV_K3_TMA)) {
-        if (maxn <= 3) launch_fast_r<3>(p, dbg, grid, s);
-        else if (maxn <= 4) launch_fast_r<4>(p, dbg, grid, s);
-        else launch_fast_r<FVV_MAX_REFS>(p, dbg, grid, s);
+        if (maxn <= 3) launch_fast_r<3>(p, dbg, fgrid, s);
+        else if (maxn <= 4) launch_fast_r<4>(p, dbg, fgrid, s);
+        else launch_fast_r<FVV_MAX_REFS>(p, dbg, fgrid, s);
         return cudaGetLastError();
     }
     if (maxn <= 4) {
