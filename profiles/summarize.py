@@ -28,6 +28,8 @@ RAW = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
        "launch__registers_per_thread", "smsp__inst_executed.sum",
        "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum",
+       "lts__t_requests_srcunit_tex_op_red.sum", "lts__t_sectors_srcunit_tex_op_red.sum.per_second",
+       "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed",
        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
