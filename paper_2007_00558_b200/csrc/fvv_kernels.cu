@@ -1059,38 +1059,38 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
         uint8_t sq = kStageNone;
         if (qy >= 0 && qy < Hd && qx >= 0 && qx < Wd) {
             const int kc = (by + 1) * FKC + bx + 1;
+            // a key is fresh (this view's generation) iff it is below `lim`:
+            // older generations carry larger tags and empty is all ones
+            const uint64_t lim = (gen + 1) << kGenShift;
             w = K[kc];
-            if ((w >> kGenShift) == gen) {
+            if (w < lim) {
                 sq = kStageCenter;
             } else {
                 const uint64_t n0 = K[kc - FKC - 1], n1 = K[kc - FKC], n2 = K[kc - FKC + 1];
                 const uint64_t n3 = K[kc - 1], n4 = K[kc + 1];
                 const uint64_t n5 = K[kc + FKC - 1], n6 = K[kc + FKC], n7 = K[kc + FKC + 1];
-                // stale generations compare larger than any fresh key
-                uint64_t m = n0 < n1 ? n0 : n1;
-                m = m < n2 ? m : n2;
-                m = m < n3 ? m : n3;
-                m = m < n4 ? m : n4;
-                m = m < n5 ? m : n5;
-                m = m < n6 ? m : n6;
-                m = m < n7 ? m : n7;
+                const bool f0 = n0 < lim, f1 = n1 < lim, f2 = n2 < lim, f3 = n3 < lim,
+                           f4 = n4 < lim, f5 = n5 < lim, f6 = n6 < lim, f7 = n7 < lim;
                 w = kEmpty;
-                if ((m >> kGenShift) == gen) {
+                bool keep = f0 | f1 | f2 | f3 | f4 | f5 | f6 | f7;   // any splat at all
+                if (keep && c.layer_fg) {
+                    // _neighbor_count (synthesis.py:79-87): in-image centre hits
+                    const bool up = qy > 0, dn = qy + 1 < Hd, lf = qx > 0, rt = qx + 1 < Wd;
+                    const int cnt = (up && lf && f0) + (up && f1) + (up && rt && f2) + (lf && f3) +
+                                    (rt && f4) + (dn && lf && f5) + (dn && f6) + (dn && rt && f7);
+                    keep = cnt >= 5;
+                }
+                if (keep) {
+                    // the 8-ring min; stale keys compare larger than any fresh one
+                    uint64_t m = n0 < n1 ? n0 : n1;
+                    m = m < n2 ? m : n2;
+                    m = m < n3 ? m : n3;
+                    m = m < n4 ? m : n4;
+                    m = m < n5 ? m : n5;
+                    m = m < n6 ? m : n6;
+                    m = m < n7 ? m : n7;
                     w = m;
                     sq = kStageSplat;
-                    if (c.layer_fg) {
-                        // _neighbor_count (synthesis.py:79-87): in-image centre hits
-                        const bool up = qy > 0, dn = qy + 1 < Hd, lf = qx > 0, rt = qx + 1 < Wd;
-                        const int cnt = (up && lf && (n0 >> kGenShift) == gen) +
-                                        (up && (n1 >> kGenShift) == gen) +
-                                        (up && rt && (n2 >> kGenShift) == gen) +
-                                        (lf && (n3 >> kGenShift) == gen) +
-                                        (rt && (n4 >> kGenShift) == gen) +
-                                        (dn && lf && (n5 >> kGenShift) == gen) +
-                                        (dn && (n6 >> kGenShift) == gen) +
-                                        (dn && rt && (n7 >> kGenShift) == gen);
-                        if (cnt < 5) { w = kEmpty; sq = kStageNone; }
-                    }
                 }
             }
             any |= w != kEmpty;
