@@ -1319,9 +1319,6 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
                 z = crack_z(c, dst, W, bi, &stc);
                 st = (uint8_t)stc;
             }
-#ifdef FVV_EXP_NO_BACKWARD
-            if (z < INFINITY) { ok = true; c0 = z; c1 = z; c2 = z; z = INFINITY; }
-#endif
             if (z < INFINITY) ok = fetch(c, dst, sray[tx], sray[TX + ty], z, c0, c1, c2);
         }
         if (!ok) { c0 = c1 = c2 = 0.0; }
