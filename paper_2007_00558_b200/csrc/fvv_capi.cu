@@ -862,7 +862,7 @@ int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, i
          "rice_decode_plane: bad arguments");
     NEED(k >= 0 && k <= 48, "rice parameter out of range");
     NEED(n_symbols == (int64_t)width * height, "plane symbol count mismatch");
-    NEED(width <= kMedMaxWidth, "plane too wide for the MED rebuild");
+    NEED(width <= kMedMaxWidth && height <= 4096, "plane too large for the MED rebuild");
     const size_t chunks = (size_t)((nbytes * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
     if ((rc = rice_scratch(ctx, (size_t)n_symbols, chunks, rice_skew_size(width, height))))
         return rc;

@@ -196,9 +196,22 @@ __global__ void k_rice_write(const uint16_t *zz, long long n, int k,
 // decode
 
 // 64 stream bits starting at bit p (MSB-first), zero past the end
+__device__ __forceinline__ unsigned long long bswap64(unsigned long long x) {
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    return ((unsigned long long)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+
 __device__ __forceinline__ unsigned long long peek64(const uint8_t *s, long long nbytes,
                                                      long long p) {
     const long long b = p >> 3;
+    const long long w = b >> 3;
+    if ((((uintptr_t)s) & 7) == 0 && (w + 2) * 8 <= nbytes) {
+        // two aligned big-endian words hold bits p .. p+63
+        const unsigned long long *q = reinterpret_cast<const unsigned long long *>(s);
+        const unsigned long long hi = bswap64(__ldg(q + w)), lo = bswap64(__ldg(q + w + 1));
+        const int sh = (int)(p - w * 64);
+        return sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+    }
     unsigned long long v = 0;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -286,15 +299,26 @@ __global__ void k_rice_sync(RiceChunks c, const long long *exit_prev, int *chang
 // Position of residual (row, col) in the rebuild's skewed layout: strip
 // (32 rows) by strip, step t = col + lane by step, 32 lanes contiguous, so the
 // wavefront's warp reads (and writes) 32 consecutive words per step.
-__device__ __forceinline__ long long skew_index(long long idx, int W) {
+#ifndef FVV_MED_DIAG
+#define FVV_MED_DIAG 1
+#endif
+
+__device__ __forceinline__ long long skew_index(long long idx, int W, int H) {
     const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
+#if FVV_MED_DIAG
+    // anti-diagonal major: diagonal t = row + col holds rows 0..H-1 at t*H + row
+    (void)W;
+    return (long long)(row + col) * H + row;
+#else
+    (void)H;
     const int lane = row & 31;
     return ((long long)(row >> 5) * (W + 31) + col + lane) * 32 + lane;
+#endif
 }
 
 // residuals of the first n symbols (zig-zag inverse, depthcodec.py:389)
 __global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long long n, int W,
-                            int32_t *res) {
+                            int H, int32_t *res) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= c.nchunks) return;
     long long p = c.entry[j];
@@ -304,7 +328,7 @@ __global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long l
         unsigned long long zz = 0;
         p += rice_one(c.s, c.nbytes, c.nbits, c.k, p, zz);
         const long long z = (long long)zz;
-        res[skew_index((long long)idx, W)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
+        res[skew_index((long long)idx, W, H)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
     }
 }
 
@@ -401,12 +425,64 @@ __global__ void __launch_bounds__(1024, 1) k_med_rebuild(const int32_t *res, int
     }
 }
 
+// The MED recurrence as an anti-diagonal wavefront in one CTA: step t
+// computes every (row, t - row) at once, since x(i, j) needs only diagonal
+// t-1 (left (i, j-1), up (i-1, j)) and t-2 (up-left). The last two diagonals
+// live in shared memory indexed by row; residuals and outputs use the
+// anti-diagonal-major layout, so each step reads and writes contiguous
+// words. One barrier per step; each thread owns rows tid, tid + blockDim, ...
+constexpr int kDiagPf = 8;  // residual prefetch depth (steps)
+
+template <int ROWS>
+__global__ void __launch_bounds__(1024, 1) k_med_rebuild_diag(const int32_t *res, int W, int H,
+                                                              uint8_t *out_diag) {
+    extern __shared__ int32_t s_diag[];   // [3][H]: diagonals t, t-1, t-2 (rotating)
+    const int nt = blockDim.x;
+    const int steps = W + H - 1;
+    // residuals of this thread's rows, kDiagPf steps ahead: ring slot u
+    // holds step t0 + u and is refilled with step t0 + u + kDiagPf
+    int32_t ring[kDiagPf][ROWS];
+    auto fetch = [&](int t, int q) -> int32_t {
+        const int i = threadIdx.x + q * nt;
+        return (i < H && i <= t && t - i < W) ? __ldg(res + (long long)t * H + i) : 0;
+    };
+#pragma unroll
+    for (int u = 0; u < kDiagPf; ++u)
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) ring[u][q] = fetch(u, q);
+    for (int t0 = 0; t0 < steps; t0 += kDiagPf) {
+#pragma unroll
+        for (int u = 0; u < kDiagPf; ++u) {
+            const int t = t0 + u;
+            if (t >= steps) break;
+            int32_t *d0 = s_diag + (t % 3) * H;
+            const int32_t *d1 = s_diag + ((t + 2) % 3) * H;   // t - 1
+            const int32_t *d2 = s_diag + ((t + 1) % 3) * H;   // t - 2
+#pragma unroll
+            for (int q = 0; q < ROWS; ++q) {
+                const int i = threadIdx.x + q * nt;
+                const int j = t - i;
+                if (i < H && j >= 0 && j < W) {
+                    const int a = j > 0 ? d1[i] : 0;
+                    const int b = i > 0 ? d1[i - 1] : 0;
+                    const int c = (i > 0 && j > 0) ? d2[i - 1] : 0;
+                    const int x = ring[u][q] + med(a, b, c);
+                    d0[i] = x;
+                    out_diag[(long long)t * H + i] = (uint8_t)x;   // astype(uint8): modulo 256
+                }
+                ring[u][q] = fetch(t + kDiagPf, q);
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // skewed rebuild output -> raster plane
 __global__ void k_deskew(const uint8_t *skew, int W, int H, uint8_t *out) {
     const long long n = (long long)W * H;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        out[i] = skew[skew_index(i, W)];
+        out[i] = skew[skew_index(i, W, H)];
 }
 
 // adler32 (zlib) of n bytes: A = 1 + sum d_i, B = n + sum (n - i) d_i, mod 65521
@@ -484,12 +560,16 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
     if (c.nchunks) {
         k_rice_spec<<<g, 128, 0, s>>>(c);
         TRACE_EV("spec");
-        for (int round = 0;; ++round) {
-            if ((e = cudaMemcpyAsync(sc.exit_prev, sc.exit, sizeof(long long) * c.nchunks,
-                                     cudaMemcpyDeviceToDevice, s)))
-                return e;
-            if ((e = cudaMemsetAsync(sc.changed, 0, sizeof(int), s))) return e;
-            k_rice_sync<<<g, 128, 0, s>>>(c, sc.exit_prev, sc.changed);
+        for (int round = 0;; round += 2) {
+            // two Jacobi rounds per host check: segmentations settle after
+            // the first round in practice, so one read-back confirms them
+            for (int r2 = 0; r2 < 2; ++r2) {
+                if ((e = cudaMemcpyAsync(sc.exit_prev, sc.exit, sizeof(long long) * c.nchunks,
+                                         cudaMemcpyDeviceToDevice, s)))
+                    return e;
+                if ((e = cudaMemsetAsync(sc.changed, 0, sizeof(int), s))) return e;
+                k_rice_sync<<<g, 128, 0, s>>>(c, sc.exit_prev, sc.changed);
+            }
             int changed = 0;
             if ((e = cudaMemcpyAsync(&changed, sc.changed, sizeof(int), cudaMemcpyDeviceToHost, s)))
                 return e;
@@ -514,8 +594,21 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
     if ((e = cudaStreamSynchronize(s))) return e;
     if ((long long)total < n) { *status = 1; return cudaSuccess; }   // stream runs out early
     TRACE_EV("sync+scan");
-    if (c.nchunks) k_rice_emit<<<g, 128, 0, s>>>(c, sc.block, n, W, sc.res);
+    if (c.nchunks) k_rice_emit<<<g, 128, 0, s>>>(c, sc.block, n, W, H, sc.res);
     TRACE_EV("emit");
+#if FVV_MED_DIAG
+    {
+        // one row per thread up to 1024 rows (fewer warps per barrier), else
+        // 1024 threads with up to kDiagRows rows each
+        const size_t sm = (size_t)3 * H * sizeof(int32_t);
+        if (H <= 1024)
+            k_med_rebuild_diag<1><<<1, (H + 31) / 32 * 32, sm, s>>>(sc.res, W, H, sc.skew);
+        else if (H <= 2048)
+            k_med_rebuild_diag<2><<<1, 1024, sm, s>>>(sc.res, W, H, sc.skew);
+        else
+            k_med_rebuild_diag<4><<<1, 1024, sm, s>>>(sc.res, W, H, sc.skew);
+    }
+#else
     const size_t smem = (size_t)2 * W * sizeof(long long);
     static int smem_set = 0;
     if ((int)smem > smem_set && smem > 48 * 1024) {
@@ -524,6 +617,7 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
         smem_set = (int)smem;
     }
     k_med_rebuild<<<1, 1024, smem, s>>>(sc.res, W, H, sc.skew);
+#endif
     k_deskew<<<148 * 4, 256, 0, s>>>(sc.skew, W, H, plane);
     TRACE_EV("rebuild");
     if ((e = cudaMemsetAsync(sc.costs, 0, 2 * sizeof(unsigned long long), s))) return e;

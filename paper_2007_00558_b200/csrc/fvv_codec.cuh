@@ -40,7 +40,9 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
 
 // elements of the rebuild's skewed layout for a W x H plane
 inline size_t rice_skew_size(int W, int H) {
-    return (size_t)((H + 31) / 32) * (size_t)(W + 31) * 32;
+    const size_t strips = (size_t)((H + 31) / 32) * (size_t)(W + 31) * 32;
+    const size_t diags = (size_t)(W + H - 1) * (size_t)H;
+    return strips > diags ? strips : diags;
 }
 
 // bytes `stream` must hold for a W x H plane: the cheapest k costs at most
