@@ -610,12 +610,9 @@ cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long lon
     }
 #else
     const size_t smem = (size_t)2 * W * sizeof(long long);
-    static int smem_set = 0;
-    if ((int)smem > smem_set && smem > 48 * 1024) {
+    if (smem > 48 * 1024)   // per-device attribute: set on every launch of this variant
         cudaFuncSetAttribute(k_med_rebuild, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        smem_set = (int)smem;
-    }
     k_med_rebuild<<<1, 1024, smem, s>>>(sc.res, W, H, sc.skew);
 #endif
     k_deskew<<<148 * 4, 256, 0, s>>>(sc.skew, W, H, plane);

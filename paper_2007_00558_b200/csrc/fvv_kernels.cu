@@ -13,6 +13,7 @@
 // Each kernel cites the reference lines it replaces; the numerics contract is
 // in fvv_common.cuh and oracle/fvv_oracle.py.
 
+#include <atomic>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -1421,9 +1422,16 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
 #endif
 }
 
+// The dynamic shared-memory limit is a per-device function attribute: raise
+// it once per (kernel, device). `done` is the kernel's bitmask of devices.
 template <typename K>
-static void raise_smem(K kernel, size_t bytes) {
+static void raise_smem(K kernel, size_t bytes, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 template <int MAXR, bool ANG>
@@ -1435,11 +1443,8 @@ static size_t fast_smem() {
 
 template <int MAXR, bool DBG, bool ANG>
 static void launch_fast(const ResolveParams &p, dim3 grid, cudaStream_t s) {
-    static bool init = false;
-    if (!init) {
-        raise_smem(k_resolve_fast<MAXR, DBG, ANG>, fast_smem<MAXR, ANG>());
-        init = true;
-    }
+    static std::atomic<uint64_t> done{0};
+    raise_smem(k_resolve_fast<MAXR, DBG, ANG>, fast_smem<MAXR, ANG>(), done);
     k_resolve_fast<MAXR, DBG, ANG><<<grid, FNT, fast_smem<MAXR, ANG>(), s>>>(p);
 }
 
@@ -1471,18 +1476,12 @@ cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
         return cudaGetLastError();
     }
     if (maxn <= 4) {
-        static bool attr4 = false;
-        if (!attr4) {
-            raise_smem(k_resolve_generic<4>, resolve_smem_bytes(4));
-            attr4 = true;
-        }
+        static std::atomic<uint64_t> done4{0};
+        raise_smem(k_resolve_generic<4>, resolve_smem_bytes(4), done4);
         k_resolve_generic<4><<<grid, NT, resolve_smem_bytes(4), s>>>(p);
     } else {
-        static bool attr_set = false;
-        if (!attr_set) {
-            raise_smem(k_resolve_generic<FVV_MAX_REFS>, resolve_smem_bytes(FVV_MAX_REFS));
-            attr_set = true;
-        }
+        static std::atomic<uint64_t> done16{0};
+        raise_smem(k_resolve_generic<FVV_MAX_REFS>, resolve_smem_bytes(FVV_MAX_REFS), done16);
         k_resolve_generic<FVV_MAX_REFS><<<grid, NT, resolve_smem_bytes(FVV_MAX_REFS), s>>>(p);
     }
     return cudaGetLastError();
