@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 // then mix_layer x2 and composite per pixel.
 
 #ifndef FVV_K3_MINB
-#define FVV_K3_MINB 4
+#define FVV_K3_MINB 5
 #endif
 #ifndef FVV_K3_TY
 #define FVV_K3_TY 8
@@ -1025,6 +1025,12 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// composite's per-channel conversion: np.clip(np.round(v), 0, 255) -> uint8
+// (half-even rint, synthesis.py:312)
+__device__ __forceinline__ uint32_t rgb_u8(double v) {
+    return (uint32_t)fmin(fmax(rint(v), 0.0), 255.0);
 }
 
 // exact f64 z of a winner index: the value K2 computed and stored for it
@@ -1209,9 +1215,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
     uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][FNT]
-    double *sfg = sres + MAXR * 4 * FNT;                          // [4][FNT] merged FG colour, z
-    double *sbg = sfg + 4 * FNT;                                  // [4][FNT] merged BG colour, z
-    double *sray = sbg + 4 * FNT;                                 // [TX] rx, [FTY] ry
+    double *sray = sres + MAXR * 4 * FNT;                         // [TX] rx, [FTY] ry
     double *swt = sray + TX + FTY;                                // [MAXR][FNT] weights (ANG)
     uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (ANG ? MAXR * FNT : 0));  // [2][FCELLS] (DBG)
 
@@ -1269,6 +1273,8 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
     bool fv = false, bv = false;
+    uint32_t fgc = 0, bgc = 0;   // rounded merged layer colours (R | G << 8 | B << 16)
+    float fgz = 0.0f, bgz = 0.0f;
     uint32_t vmask = 0;
 #pragma unroll 1
     for (int q = 0; q < nitems; ++q) {
@@ -1381,13 +1387,18 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
                 m1 = div_rcp(a1, aw, ra);
                 m2 = div_rcp(a2, aw, ra);
             }
-            double *sl = fgl ? sfg : sbg;
-            sl[tid] = m0;
-            sl[FNT + tid] = m1;
-            sl[2 * FNT + tid] = m2;
-            if (p.depth_out) sl[3 * FNT + tid] = mv ? ddiv(ad, aw) : 0.0;
-            if (fgl) fv = mv;
-            else bv = mv;
+            const float mz = (p.depth_out && mv) ? (float)ddiv(ad, aw) : 0.0f;
+            if (fgl) {
+                // composite needs only the FG layer's rounded colour (it wins
+                // wherever valid, synthesis.py:309-312): one packed register
+                fv = mv;
+                fgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
+                fgz = mz;
+            } else {
+                bv = mv;
+                bgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
+                bgz = mz;
+            }
             vmask = 0;
             if (DBG && inimg) {
                 const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
@@ -1402,19 +1413,17 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         }
         // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
         if (k == ntot - 1 && inimg) {
-            double o0, o1, o2;
-            if (fv) { o0 = sfg[tid]; o1 = sfg[FNT + tid]; o2 = sfg[2 * FNT + tid]; }
-            else if (bv) { o0 = sbg[tid]; o1 = sbg[FNT + tid]; o2 = sbg[2 * FNT + tid]; }
-            else { o0 = p.hole[0]; o1 = p.hole[1]; o2 = p.hole[2]; }
+            const uint32_t hole = rgb_u8(p.hole[0]) | (rgb_u8(p.hole[1]) << 8) |
+                                  (rgb_u8(p.hole[2]) << 16);
+            const uint32_t oc = fv ? fgc : (bv ? bgc : hole);
             if (p.rgb_out) {
                 uint8_t *o = p.rgb_out + pix * 3;
-                o[0] = (uint8_t)fmin(fmax(rint(o0), 0.0), 255.0);
-                o[1] = (uint8_t)fmin(fmax(rint(o1), 0.0), 255.0);
-                o[2] = (uint8_t)fmin(fmax(rint(o2), 0.0), 255.0);
+                o[0] = (uint8_t)oc;
+                o[1] = (uint8_t)(oc >> 8);
+                o[2] = (uint8_t)(oc >> 16);
             }
             if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
-            if (p.depth_out)
-                p.depth_out[pix] = (float)(fv ? sfg[3 * FNT + tid] : (bv ? sbg[3 * FNT + tid] : 0.0));
+            if (p.depth_out) p.depth_out[pix] = fv ? fgz : (bv ? bgz : 0.0f);
         }
     }
 #if !FVV_K3_TMA
@@ -1437,7 +1446,7 @@ static void raise_smem(K kernel, size_t bytes, std::atomic<uint64_t> &done) {
 template <int MAXR, bool ANG>
 static size_t fast_smem() {
     return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
-           (size_t)MAXR * 4 * FNT * sizeof(double) + (8 * FNT + TX + FTY) * sizeof(double) +
+           (size_t)MAXR * 4 * FNT * sizeof(double) + (TX + FTY) * sizeof(double) +
            (ANG ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
 }
 
