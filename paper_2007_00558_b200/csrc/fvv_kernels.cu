@@ -1197,10 +1197,12 @@ __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst
 #ifndef FVV_K3_NBUF
 #define FVV_K3_NBUF 2
 #endif
-// K3 key staging: 0 = cp.async (default: measured 3 % faster at c1 than the
-// TMA + mbarrier variant, 224 vs 231 us), 1 = cp.async.bulk.tensor (TMA)
+// K3 key staging: 1 = cp.async.bulk.tensor (TMA) + mbarrier (default: at 5
+// CTAs/SM it measured 209.4 vs 212.9 us for cp.async; at 4 CTAs/SM, before
+// the merged layers left shared memory, cp.async had been 3 % faster),
+// 0 = per-thread 16-byte cp.async
 #ifndef FVV_K3_TMA
-#define FVV_K3_TMA 0
+#define FVV_K3_TMA 1
 #endif
 constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of the one shaded)
 
