@@ -66,10 +66,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipelines", type=int, default=2,
+    ap.add_argument("--pipelines", type=int, default=None,
                     help="frames in flight: steps alternate over this many private renderers "
                          "on their own CUDA streams, so one frame's decode/fill (K0/K1) "
-                         "overlaps another's warp/resolve (K2/K3)")
+                         "overlaps another's warp/resolve (K2/K3); default 2, and 1 for c0 "
+                         "whose 0.1 ms steps are bound by the host's launch calls")
     ap.add_argument("--gen", default="auto", choices=("auto", "host", "gpu"),
                     help="input generator: numpy ray caster on the host, or scenes_gpu in "
                          "HBM (auto: gpu for c3/c4, whose host generation takes minutes)")
@@ -78,6 +79,8 @@ def parse():
         args.gen = "gpu" if args.config in ("c3", "c4") else "host"
     if args.frames is None:
         args.frames = 300 if args.config == "c3" else 4
+    if args.pipelines is None:
+        args.pipelines = 1 if args.config == "c0" else 2
     return args
 
 
