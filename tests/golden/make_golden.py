@@ -270,10 +270,35 @@ def rice_case():
     print("rice ok:", {k: v.size for k, v in out.items() if k.endswith("payload")}, heads)
 
 
+def silhouette_case():
+    """The reference's own silhouette hole-fill scene (test_depthproc.py:
+    297-319): simple scene, rig camera 4 of the 128x96 test rig, depth
+    degraded with 2-px holes on the BG side of silhouettes; stored with the
+    ground-truth and BG-model depths the test's accuracy criteria use and the
+    reference's bilateral_close_holes output."""
+    from fvv.scenegen import DepthErrorSpec
+
+    rig = rscene.build_camera_arc(9, 0.270, 60.0, width=128, height=96)
+    scene = rscene.make_scene("simple")
+    mvd, fg = rscene.render_with_mask(scene, rig[4], 0.0)
+    degraded = rscene.degrade_depth(mvd.depth, DepthErrorSpec(0.0, 1.0, hole_width=2), seed=6,
+                                    fg_mask=fg)
+    out = rproc.bilateral_close_holes(degraded, mvd.color)
+    bg = rscene.bg_depth_model(scene, rig[4]).depth
+    np.savez_compressed(OUT / "silhouette.npz", depth=degraded.depth, validity=degraded.validity,
+                        rgb=mvd.color.pixels, gt=mvd.depth.depth, bg=bg, out_depth=out.depth,
+                        out_validity=out.validity)
+    print("silhouette ok: holes", int((degraded.validity == 1).sum()))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["rice"]:
         rice_case()
         sys.exit(0)
+    if sys.argv[1:] == ["silhouette"]:
+        silhouette_case()
+        sys.exit(0)
+    silhouette_case()
     rice_case()
     capture_case()
     for args in SYN_CASES:

@@ -438,3 +438,37 @@ def test_engine_synthesize_matches_drop_in(cuda):
     assert got2.pixels.shape == want.pixels.shape
     with pytest.raises(ValueError):
         eng.render([case.virtual], [[999]])
+
+
+def test_silhouette_holes_mostly_filled_to_ground_truth(P, T):
+    """test_depthproc.py:297-319 on the reference's own scene (stored by
+    tests/golden/make_golden.py): >= 95 % of interior silhouette holes filled,
+    fills on gently sloped background within 2 % of the exact render, and the
+    whole output bit-identical to the reference's."""
+    from oracle.fvv_oracle import shift2d
+
+    g = golden("silhouette.npz")
+    H, W = g["depth"].shape
+    out = P.bilateral_close_holes(T.DepthFrame(W, H, g["depth"], g["validity"]),
+                                  T.ColorFrame(W, H, g["rgb"]))
+    np.testing.assert_array_equal(out.validity, g["out_validity"])
+    np.testing.assert_array_equal(out.depth, g["out_depth"])
+    holes = g["validity"] == 1
+    interior = np.zeros_like(holes)
+    interior[2:-2, 2:-2] = True
+    holes &= interior
+    filled = holes & (out.validity == 0)
+    assert filled.sum() / holes.sum() >= 0.95
+    gt = g["gt"].astype(np.float64)
+    rel = np.abs(out.depth - gt) / gt
+    bg = g["bg"].astype(np.float64)
+    gy, gx = np.gradient(bg)
+    grad = (np.abs(gy) + np.abs(gx)) / bg
+    window_grad = grad.copy()
+    for dy in range(-2, 3):
+        for dx in range(-2, 3):
+            window_grad = np.maximum(window_grad, shift2d(grad, dy, dx))
+    gentle = window_grad < 0.01
+    assert (rel[filled & gentle] <= 0.02).all()
+    assert (filled & gentle).sum() > 100
+    assert np.median(rel[filled]) <= 0.02

@@ -193,3 +193,11 @@ def test_c_oracle_preprocessing_matches_reference(name):
     np.testing.assert_array_equal(fv, g["fill_validity"])
     # the C restatement reads np.exp's range weights, so it is bit-exact
     np.testing.assert_array_equal(fd, g["fill_depth"])
+
+
+def test_oracle_bilateral_on_the_reference_silhouette_scene():
+    """The reference's own hole-fill scene (test_depthproc.py:297-319)."""
+    g = golden("silhouette.npz")
+    d, v, _ = O.bilateral_close_holes(g["depth"], g["validity"], g["rgb"])
+    np.testing.assert_array_equal(v, g["out_validity"])
+    np.testing.assert_array_equal(d, g["out_depth"])
