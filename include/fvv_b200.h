@@ -243,6 +243,15 @@ int fvv_rice_encode_plane(fvv_ctx *ctx, const uint8_t *plane, int32_t width, int
 int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, int32_t k,
                           int64_t n_symbols, int32_t width, int32_t height, uint8_t *plane_out,
                           uint32_t *adler_out);
+/* The same for n planes at once (up to 48: e.g. Y, U, V of every reference
+ * camera of a render tick): the Rice segmentation of all streams runs in the
+ * same kernels and the planes' MED recurrences run concurrently, one CTA
+ * each. Host arrays of n entries; status_out[i] = 1 when stream i runs out
+ * early (adlers_out[i] then 0). */
+int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *streams,
+                           const int64_t *nbytes, const int32_t *ks, const int32_t *widths,
+                           const int32_t *heights, uint8_t *const *planes_out,
+                           uint32_t *adlers_out, int32_t *status_out);
 
 /* ---- session path: resident camera slots, batched views ---------------------
  * The edge server keeps a slot per rig camera: its calibration, its static

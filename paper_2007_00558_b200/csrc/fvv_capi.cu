@@ -312,8 +312,8 @@ int ensure_zsrc(fvv_ctx *ctx, int n, size_t px) {
 int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
     RiceScratch &r = ctx->rice;
     if (!r.costs) {
-        CK(cudaMalloc(&r.costs, 16 * sizeof(unsigned long long)));
-        CK(cudaMalloc(&r.total, sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.costs, 2 * kRiceMaxPlanes * sizeof(unsigned long long)));
+        CK(cudaMalloc(&r.total, kRiceMaxPlanes * sizeof(unsigned long long)));
         CK(cudaMalloc(&r.changed, sizeof(int)));
     }
     const size_t blocks = (n + 1023) / 1024 + 1;
@@ -334,7 +334,7 @@ int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
     const size_t cneed = bneed;
     if (cneed > r.c_cap) {
         for (void **q : {(void **)&r.block, (void **)&r.entry, (void **)&r.exit,
-                         (void **)&r.exit_prev, (void **)&r.count, (void **)&r.trunc}) {
+                         (void **)&r.exit_prev, (void **)&r.count}) {
             CK(cudaFree(*q));
             *q = nullptr;
         }
@@ -343,7 +343,6 @@ int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
         CK(cudaMalloc(&r.exit, cneed * sizeof(long long)));
         CK(cudaMalloc(&r.exit_prev, cneed * sizeof(long long)));
         CK(cudaMalloc(&r.count, cneed * sizeof(unsigned long long)));
-        CK(cudaMalloc(&r.trunc, cneed * sizeof(int)));
         r.c_cap = cneed;
     }
     return FVV_OK;
@@ -528,7 +527,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
                     (void *)ctx->rice.block,
                     (void *)ctx->rice.costs, (void *)ctx->rice.total, (void *)ctx->rice.entry,
                     (void *)ctx->rice.exit, (void *)ctx->rice.exit_prev, (void *)ctx->rice.count,
-                    (void *)ctx->rice.trunc, (void *)ctx->rice.changed})
+                    (void *)ctx->rice.changed})
         cudaFree(q);
     cudaFree(ctx->cand);
     cudaFree(ctx->ncand);
@@ -851,6 +850,45 @@ int fvv_rice_encode_plane(fvv_ctx *ctx, const uint8_t *plane, int32_t width, int
     return FVV_OK;
 }
 
+int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *streams,
+                           const int64_t *nbytes, const int32_t *ks, const int32_t *widths,
+                           const int32_t *heights, uint8_t *const *planes_out,
+                           uint32_t *adlers_out, int32_t *status_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(n >= 0 && n <= kRiceMaxPlanes, "rice_decode_planes: 0..48 planes per call");
+    if (!n) return FVV_OK;
+    NEED(streams && nbytes && ks && widths && heights && planes_out && adlers_out && status_out,
+         "rice_decode_planes: NULL argument array");
+    RicePlane pl[kRiceMaxPlanes];
+    size_t px = 0, skew = 0, chunks = 0;
+    for (int i = 0; i < n; ++i) {
+        NEED(widths[i] > 0 && heights[i] > 0 && planes_out[i] && nbytes[i] >= 0 &&
+                 (streams[i] || !nbytes[i]),
+             "rice_decode_planes: bad plane");
+        NEED(ks[i] >= 0 && ks[i] <= 48, "rice parameter out of range");
+        NEED(widths[i] <= kMedMaxWidth && heights[i] <= 4096, "plane too large for the MED rebuild");
+        pl[i] = RicePlane{};
+        pl[i].s = streams[i];
+        pl[i].nbytes = nbytes[i];
+        pl[i].k = ks[i];
+        pl[i].W = widths[i];
+        pl[i].H = heights[i];
+        pl[i].out = planes_out[i];
+        px += (size_t)widths[i] * heights[i];
+        skew += rice_skew_size(widths[i], heights[i]);
+        chunks += (size_t)((nbytes[i] * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
+    }
+    if ((rc = rice_scratch(ctx, px, chunks + n, skew))) return rc;
+    LAUNCH(rice_decode_batch(pl, n, ctx->rice, ctx->stream));
+    ctx->launches += 6;  // spec, >= 2 sync rounds, scan, emit, rebuild, deskew, adler (counted once)
+    for (int i = 0; i < n; ++i) {
+        status_out[i] = pl[i].status;
+        adlers_out[i] = pl[i].status ? 0u : pl[i].adler;
+    }
+    return FVV_OK;
+}
+
 int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, int32_t k,
                           int64_t n_symbols, int32_t width, int32_t height, uint8_t *plane_out,
                           uint32_t *adler_out) {
@@ -858,18 +896,12 @@ int fvv_rice_decode_plane(fvv_ctx *ctx, const uint8_t *stream, int64_t nbytes, i
     if (rc) return rc;
     NEED(width > 0 && height > 0 && plane_out && adler_out && nbytes >= 0 && (stream || !nbytes),
          "rice_decode_plane: bad arguments");
-    NEED(k >= 0 && k <= 48, "rice parameter out of range");
     NEED(n_symbols == (int64_t)width * height, "plane symbol count mismatch");
-    NEED(width <= kMedMaxWidth && height <= 4096, "plane too large for the MED rebuild");
-    const size_t chunks = (size_t)((nbytes * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
-    if ((rc = rice_scratch(ctx, (size_t)n_symbols, chunks, rice_skew_size(width, height))))
+    int32_t status = 0;
+    if ((rc = fvv_rice_decode_planes(ctx, 1, &stream, &nbytes, &k, &width, &height, &plane_out,
+                                     adler_out, &status)))
         return rc;
-    int status = 0;
-    uint32_t adler = 0;
-    LAUNCH(rice_decode(stream, nbytes, k, n_symbols, width, height, ctx->rice, plane_out, &adler,
-                       &status, ctx->stream));
     if (status) return fail(ctx, FVV_EINVAL, "rice stream truncated");
-    *adler_out = adler;
     return FVV_OK;
 }
 

@@ -20,10 +20,9 @@
 //                         settle an exact symbol segmentation
 //           k_scan_blocks symbol base of every chunk
 //           k_rice_emit   each chunk writes its residuals
-//           k_med_rebuild the MED recurrence as a wavefront: one CTA per
-//                         plane, a warp per 32-row strip with lane = row and
-//                         columns skewed by lane; strips hand their last row
-//                         to the next strip's warp through shared memory
+//           k_med_rebuild_diag  the MED recurrence as an anti-diagonal
+//                         wavefront, one CTA per plane, one barrier per
+//                         diagonal; all planes of a batch run concurrently
 //           k_adler       adler32 of the rebuilt plane (zlib.adler32 check)
 
 #include <cstdint>
@@ -108,9 +107,8 @@ __global__ void k_rice_lens(const uint16_t *zz, long long n, int k,
     }
 }
 
-// exclusive scan of v[0..n) in place (one CTA of 1024 threads); total in *total
-__global__ void __launch_bounds__(1024) k_scan_blocks(unsigned long long *v, long long n,
-                                                      unsigned long long *total) {
+// exclusive scan of v[0..n) in place by one CTA of 1024 threads; total in *total
+__device__ void scan_segment(unsigned long long *v, long long n, unsigned long long *total) {
     __shared__ unsigned long long ws[32];
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) carry = 0;
@@ -142,6 +140,11 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(unsigned long long *v, lon
         __syncthreads();
     }
     if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_blocks(unsigned long long *v, long long n,
+                                                      unsigned long long *total) {
+    scan_segment(v, n, total);
 }
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -249,179 +252,99 @@ __device__ __forceinline__ long long rice_one(const uint8_t *s, long long nbytes
     return t + 1 + k - p;
 }
 
-struct RiceChunks {
-    const uint8_t *s;
-    long long nbytes, nbits;
-    int k;
-    long long nchunks;
-    long long *entry;              // symbol start the chunk decodes from
+// Position of residual (row, col) in the rebuild's anti-diagonal-major
+// layout: diagonal t = row + col holds rows 0..H-1 at t*H + row, so each
+// wavefront step reads and writes contiguous words.
+__device__ __forceinline__ long long skew_index(long long idx, int W, int H) {
+    const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
+    return (long long)(row + col) * H + row;
+}
+
+// A batch of planes decoded together (all depth planes of a render tick):
+// their chunks are numbered consecutively, plane p owning chunks
+// [pl[p].c0, pl[p].c0 + pl[p].nchunks).
+struct RiceBatch {
+    int np;
+    RicePlane pl[kRiceMaxPlanes];
+    long long nchunks;             // over all planes
+    long long *entry;              // symbol start the chunk decodes from (plane bits)
     long long *exit;               // first symbol start at or past the chunk end
     unsigned long long *count;     // symbols starting inside the chunk
-    int *trunc;                    // 1: the chunk's last symbol is truncated
 };
 
-__device__ void chunk_decode(const RiceChunks &c, long long j, long long e) {
-    const long long end = (j + 1) * kRiceChunkBits < c.nbits ? (j + 1) * kRiceChunkBits : c.nbits;
+__device__ __forceinline__ int plane_of(const RiceBatch &b, long long j) {
+    int p = 0;
+    while (p + 1 < b.np && j >= b.pl[p + 1].c0) ++p;
+    return p;
+}
+
+__device__ void chunk_decode(const RiceBatch &b, const RicePlane &pl, long long j, long long lj,
+                             long long e) {
+    const long long end =
+        (lj + 1) * kRiceChunkBits < pl.nbits ? (lj + 1) * kRiceChunkBits : pl.nbits;
     long long p = e;
     unsigned long long n = 0;
-    int tr = 0;
     while (p < end) {
         unsigned long long zz;
-        const long long len = rice_one(c.s, c.nbytes, c.nbits, c.k, p, zz);
-        if (!len) { tr = 1; p = c.nbits; break; }
+        const long long len = rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
+        if (!len) { p = pl.nbits; break; }   // truncated: no further symbols
         p += len;
         ++n;
     }
-    c.entry[j] = e;
-    c.exit[j] = p;
-    c.count[j] = n;
-    c.trunc[j] = tr;
+    b.entry[j] = e;
+    b.exit[j] = p;
+    b.count[j] = n;
 }
 
 // round 0: every chunk guesses that a symbol starts at its first bit
-__global__ void k_rice_spec(RiceChunks c) {
+__global__ void k_rice_spec(const __grid_constant__ RiceBatch b) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < c.nchunks) chunk_decode(c, j, j == 0 ? 0 : j * kRiceChunkBits);
+    if (j >= b.nchunks) return;
+    const RicePlane &pl = b.pl[plane_of(b, j)];
+    const long long lj = j - pl.c0;
+    chunk_decode(b, pl, j, lj, lj * kRiceChunkBits);
 }
 
-// later rounds: entry(j) = exit(j-1) of the previous round (Jacobi); chunks
-// whose entry changed decode again. `exit_prev` is the previous round's
-// exits; `changed` counts the chunks that moved.
-__global__ void k_rice_sync(RiceChunks c, const long long *exit_prev, int *changed) {
+// later rounds: entry(j) = exit(j-1) of the previous round (Jacobi, within a
+// plane); chunks whose entry changed decode again, `changed` counts them
+__global__ void k_rice_sync(const __grid_constant__ RiceBatch b, const long long *exit_prev,
+                            int *changed) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= c.nchunks || j == 0) return;
+    if (j >= b.nchunks) return;
+    const RicePlane &pl = b.pl[plane_of(b, j)];
+    const long long lj = j - pl.c0;
+    if (lj == 0) return;
     const long long e = exit_prev[j - 1];
-    if (e == c.entry[j]) return;
-    chunk_decode(c, j, e);
+    if (e == b.entry[j]) return;
+    chunk_decode(b, pl, j, lj, e);
     atomicAdd(changed, 1);
 }
 
-// Position of residual (row, col) in the rebuild's skewed layout: strip
-// (32 rows) by strip, step t = col + lane by step, 32 lanes contiguous, so the
-// wavefront's warp reads (and writes) 32 consecutive words per step.
-#ifndef FVV_MED_DIAG
-#define FVV_MED_DIAG 1
-#endif
-
-__device__ __forceinline__ long long skew_index(long long idx, int W, int H) {
-    const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
-#if FVV_MED_DIAG
-    // anti-diagonal major: diagonal t = row + col holds rows 0..H-1 at t*H + row
-    (void)W;
-    return (long long)(row + col) * H + row;
-#else
-    (void)H;
-    const int lane = row & 31;
-    return ((long long)(row >> 5) * (W + 31) + col + lane) * 32 + lane;
-#endif
+// exclusive scan of each plane's chunk counts (one CTA per plane); a
+// plane's total goes to totals[p]
+__global__ void __launch_bounds__(1024) k_scan_planes(const __grid_constant__ RiceBatch b,
+                                                      unsigned long long *v,
+                                                      unsigned long long *totals) {
+    const RicePlane &pl = b.pl[blockIdx.x];
+    scan_segment(v + pl.c0, pl.nchunks, totals + blockIdx.x);
 }
 
-// residuals of the first n symbols (zig-zag inverse, depthcodec.py:389)
-__global__ void k_rice_emit(RiceChunks c, const unsigned long long *base, long long n, int W,
-                            int H, int32_t *res) {
+// residuals of each plane's first n symbols (zig-zag inverse,
+// depthcodec.py:389), into the rebuild's anti-diagonal layout
+__global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned long long *base,
+                            int32_t *res) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= c.nchunks) return;
-    long long p = c.entry[j];
+    if (j >= b.nchunks) return;
+    const RicePlane &pl = b.pl[plane_of(b, j)];
+    long long p = b.entry[j];
     unsigned long long idx = base[j];
-    const unsigned long long cnt = c.count[j];
-    for (unsigned long long s = 0; s < cnt && (long long)idx < n; ++s, ++idx) {
+    const unsigned long long cnt = b.count[j];
+    int32_t *r = res + pl.rbase;
+    for (unsigned long long s = 0; s < cnt && (long long)idx < pl.n; ++s, ++idx) {
         unsigned long long zz = 0;
-        p += rice_one(c.s, c.nbytes, c.nbits, c.k, p, zz);
+        p += rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
         const long long z = (long long)zz;
-        res[skew_index((long long)idx, W, H)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
-    }
-}
-
-// The MED recurrence x = r + med(left, up, up-left) (depthcodec.py:301-316)
-// on one plane per CTA. Warp w rebuilds 32-row strips w, w+32, ...; lane l
-// holds row 32*strip + l and reaches column j at step j + l, so its up and
-// up-left neighbours are lane l-1's values of the two previous steps
-// (shuffles). Lane 0 takes them from the previous strip's last row, which
-// that strip's lane 31 publishes column by column into one of two shared-
-// memory row slots as 64-bit (strip tag << 32 | x) words: one aligned 8-byte
-// store is atomic, so the consumer spins on the word itself and needs no
-// fence. Two slots are enough: strip S+1 overwrites column j of slot (S+1)%2
-// only after its lane 0 consumed column j of strip S, i.e. after strip S's
-// lane 0 read column j of strip S-1 from that slot.
-#ifndef FVV_MED_SLEEP
-#define FVV_MED_SLEEP 32
-#endif
-#ifndef FVV_MED_PF
-#define FVV_MED_PF 4
-#endif
-constexpr int kPf = FVV_MED_PF;  // residual prefetch depth of the MED rebuild
-
-__global__ void __launch_bounds__(1024, 1) k_med_rebuild(const int32_t *res, int W, int H,
-                                                         uint8_t *out_skew) {
-    extern __shared__ long long s_rows[];       // [2][W] (strip << 32 | x)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nstrips = (H + 31) / 32;
-    for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) s_rows[i] = -1ll << 32;
-    __syncthreads();
-    volatile long long *vrows = s_rows;
-    for (int strip = warp; strip < nstrips; strip += 32) {
-        const int row = strip * 32 + lane;
-        const bool live = row < H;
-        const int slot = strip & 1, pslot = slot ^ 1;
-        int cur = 0, prev = 0;   // this lane's x at columns j-1 and j-2
-        int bprev = 0;           // lane 0: the previous strip's x at column j-1
-        const int steps = W + 31;
-        // residuals and outputs in the skewed layout (skew_index): step t of
-        // this strip is 32 consecutive words / bytes. The residuals stream
-        // through a kPf-deep register window loaded kPf steps ahead.
-        const long long sbase = (long long)strip * (W + 31) * 32 + lane;
-        int32_t win[kPf];
-#pragma unroll
-        for (int q = 0; q < kPf; ++q) {
-            const int jq = q - lane;
-            win[q] = (live && jq >= 0 && jq < W) ? __ldg(res + sbase + (long long)q * 32) : 0;
-        }
-        // unrolled by kPf so window slot u is consumed at step t0 + u and
-        // refilled for step t0 + u + kPf: each load has kPf steps to land
-        for (int t0 = 0; t0 < steps; t0 += kPf) {
-#pragma unroll
-            for (int u = 0; u < kPf; ++u) {
-                const int t = t0 + u;
-                if (t >= steps) break;
-                const int j = t - lane;
-                // up / up-left: lane l-1's values from the last two steps
-                const int up_l = __shfl_up_sync(0xffffffffu, cur, 1);
-                const int upl_l = __shfl_up_sync(0xffffffffu, prev, 1);
-                int x = 0;
-                if (j >= 0 && j < W && live) {
-                    int b, c;
-                    if (lane == 0) {
-                        if (strip == 0) {
-                            b = 0;
-                        } else {
-                            long long w;
-                            // a waiting lane backs off, leaving issue slots
-                            // to the producing warps on the same SM
-                            while ((int)((w = vrows[pslot * W + j]) >> 32) != strip - 1)
-                                __nanosleep(FVV_MED_SLEEP);
-                            b = (int)(uint32_t)w;
-                        }
-                        c = j > 0 ? bprev : 0;
-                        bprev = b;
-                    } else {
-                        b = up_l;
-                        c = j > 0 ? upl_l : 0;
-                    }
-                    const int a = j > 0 ? cur : 0;
-                    x = win[u] + med(a, b, c);
-                    out_skew[sbase + (long long)t * 32] = (uint8_t)x;   // astype(uint8): mod 256
-                    if (lane == 31 && strip + 1 < nstrips)
-                        vrows[slot * W + j] = ((long long)strip << 32) | (uint32_t)x;
-                }
-                if (j >= 0 && j < W) {
-                    prev = cur;
-                    cur = x;
-                }
-                const int jn = j + kPf;
-                win[u] = (live && jn >= 0 && jn < W)
-                             ? __ldg(res + sbase + (long long)(t + kPf) * 32) : 0;
-            }
-        }
+        r[skew_index((long long)idx, pl.W, pl.H)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
     }
 }
 
@@ -434,8 +357,14 @@ __global__ void __launch_bounds__(1024, 1) k_med_rebuild(const int32_t *res, int
 constexpr int kDiagPf = 8;  // residual prefetch depth (steps)
 
 template <int ROWS>
-__global__ void __launch_bounds__(1024, 1) k_med_rebuild_diag(const int32_t *res, int W, int H,
-                                                              uint8_t *out_diag) {
+__global__ void __launch_bounds__(1024, 1) k_med_rebuild_diag(const __grid_constant__ RiceBatch b,
+                                                              const int32_t *res_all,
+                                                              uint8_t *diag_all) {
+    // one CTA per plane
+    const RicePlane &pl = b.pl[blockIdx.x];
+    const int W = pl.W, H = pl.H;
+    const int32_t *res = res_all + pl.rbase;
+    uint8_t *out_diag = diag_all + pl.rbase;
     extern __shared__ int32_t s_diag[];   // [3][H]: diagonals t, t-1, t-2 (rotating)
     const int nt = blockDim.x;
     const int steps = W + H - 1;
@@ -477,30 +406,34 @@ __global__ void __launch_bounds__(1024, 1) k_med_rebuild_diag(const int32_t *res
     }
 }
 
-// skewed rebuild output -> raster plane
-__global__ void k_deskew(const uint8_t *skew, int W, int H, uint8_t *out) {
-    const long long n = (long long)W * H;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+// anti-diagonal rebuild output -> raster plane (blockIdx.y = plane)
+__global__ void k_deskew(const __grid_constant__ RiceBatch b, const uint8_t *diag_all) {
+    const RicePlane &pl = b.pl[blockIdx.y];
+    const uint8_t *skew = diag_all + pl.rbase;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pl.n;
          i += (long long)gridDim.x * blockDim.x)
-        out[i] = skew[skew_index(i, W, H)];
+        pl.out[i] = skew[skew_index(i, pl.W, pl.H)];
 }
 
-// adler32 (zlib) of n bytes: A = 1 + sum d_i, B = n + sum (n - i) d_i, mod 65521
-__global__ void k_adler(const uint8_t *d, long long n, unsigned long long *sums) {
-    unsigned long long a = 0, b = 0;
+// adler32 (zlib) of each rebuilt plane: A = 1 + sum d_i, B = n + sum (n - i) d_i,
+// mod 65521 (blockIdx.y = plane; sums[2p], sums[2p+1])
+__global__ void k_adler(const __grid_constant__ RiceBatch b, unsigned long long *sums) {
+    const RicePlane &pl = b.pl[blockIdx.y];
+    const long long n = pl.n;
+    unsigned long long a = 0, c = 0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long v = d[i];
+        const unsigned long long v = pl.out[i];
         a += v;
-        b += (unsigned long long)(n - i) * v;
+        c += (unsigned long long)(n - i) * v;
     }
     for (int o = 16; o; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sums[0], a % 65521ull);
-        atomicAdd(&sums[1], b % 65521ull);
+        atomicAdd(&sums[2 * blockIdx.y], a % 65521ull);
+        atomicAdd(&sums[2 * blockIdx.y + 1], c % 65521ull);
     }
 }
 
@@ -534,97 +467,90 @@ cudaError_t rice_encode(const uint8_t *plane, int W, int H, RiceScratch &sc, uin
     return cudaGetLastError();
 }
 
-cudaError_t rice_decode(const uint8_t *stream, long long nbytes, int k, long long n, int W, int H,
-                        RiceScratch &sc, uint8_t *plane, uint32_t *adler_out, int *status,
-                        cudaStream_t s) {
-    *status = 0;
+cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaStream_t s) {
     cudaError_t e;
-    const long long nbits = nbytes * 8;
-    RiceChunks c{};
-    c.s = stream;
-    c.nbytes = nbytes;
-    c.nbits = nbits;
-    c.k = k;
-    c.nchunks = nbits ? (nbits + kRiceChunkBits - 1) / kRiceChunkBits : 0;
-    c.entry = sc.entry;
-    c.exit = sc.exit;
-    c.count = sc.count;
-    c.trunc = sc.trunc;
-    const unsigned g = (unsigned)((c.nchunks + 127) / 128);
-#ifdef FVV_CODEC_TRACE
-    cudaEvent_t t0_;
-    cudaEventCreate(&t0_);
-    cudaEventRecord(t0_, s);
-    int rounds_ = 0;
-#endif
-    if (c.nchunks) {
-        k_rice_spec<<<g, 128, 0, s>>>(c);
-        TRACE_EV("spec");
-        for (int round = 0;; round += 2) {
+    RiceBatch b{};
+    b.np = np;
+    long long c0 = 0, rbase = 0;
+    int maxH = 0;
+    for (int p = 0; p < np; ++p) {
+        RicePlane &pl = planes[p];
+        pl.nbits = pl.nbytes * 8;
+        pl.n = (long long)pl.W * pl.H;
+        pl.c0 = c0;
+        pl.nchunks = pl.nbits ? (pl.nbits + kRiceChunkBits - 1) / kRiceChunkBits : 0;
+        pl.rbase = rbase;
+        pl.status = 0;
+        c0 += pl.nchunks;
+        rbase += (long long)rice_skew_size(pl.W, pl.H);
+        maxH = pl.H > maxH ? pl.H : maxH;
+        b.pl[p] = pl;
+    }
+    b.nchunks = c0;
+    b.entry = sc.entry;
+    b.exit = sc.exit;
+    b.count = sc.count;
+    const unsigned g = (unsigned)((b.nchunks + 127) / 128);
+    unsigned long long tot[kRiceMaxPlanes] = {0};
+    if (b.nchunks) {
+        k_rice_spec<<<g, 128, 0, s>>>(b);
+        for (long long round = 0;; round += 2) {
             // two Jacobi rounds per host check: segmentations settle after
             // the first round in practice, so one read-back confirms them
             for (int r2 = 0; r2 < 2; ++r2) {
-                if ((e = cudaMemcpyAsync(sc.exit_prev, sc.exit, sizeof(long long) * c.nchunks,
+                if ((e = cudaMemcpyAsync(sc.exit_prev, sc.exit, sizeof(long long) * b.nchunks,
                                          cudaMemcpyDeviceToDevice, s)))
                     return e;
                 if ((e = cudaMemsetAsync(sc.changed, 0, sizeof(int), s))) return e;
-                k_rice_sync<<<g, 128, 0, s>>>(c, sc.exit_prev, sc.changed);
+                k_rice_sync<<<g, 128, 0, s>>>(b, sc.exit_prev, sc.changed);
             }
             int changed = 0;
             if ((e = cudaMemcpyAsync(&changed, sc.changed, sizeof(int), cudaMemcpyDeviceToHost, s)))
                 return e;
             if ((e = cudaStreamSynchronize(s))) return e;
-#ifdef FVV_CODEC_TRACE
-            ++rounds_;
-            fprintf(stderr, "[codec] round %d changed %d\n", rounds_, changed);
-#endif
             if (!changed) break;
-            if (round > c.nchunks) return cudaErrorUnknown;  // cannot happen: one chunk per round
+            if (round > b.nchunks) return cudaErrorUnknown;  // cannot happen: >= 1 chunk settles per round
         }
-        if ((e = cudaMemcpyAsync(sc.block, sc.count, sizeof(unsigned long long) * c.nchunks,
+        if ((e = cudaMemcpyAsync(sc.block, sc.count, sizeof(unsigned long long) * b.nchunks,
                                  cudaMemcpyDeviceToDevice, s)))
             return e;
-        k_scan_blocks<<<1, 1024, 0, s>>>(sc.block, c.nchunks, sc.total);
-    } else if ((e = cudaMemsetAsync(sc.total, 0, sizeof(unsigned long long), s))) {
+        k_scan_planes<<<np, 1024, 0, s>>>(b, sc.block, sc.total);
+        if ((e = cudaMemcpyAsync(tot, sc.total, sizeof(unsigned long long) * np,
+                                 cudaMemcpyDeviceToHost, s)))
+            return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+    }
+    // a plane whose stream runs out before its n symbols (a truncated symbol
+    // ends its chain) is reported and left undecoded
+    bool any = false;
+    for (int p = 0; p < np; ++p) {
+        planes[p].status = (long long)tot[p] < planes[p].n ? 1 : 0;
+        b.pl[p].status = planes[p].status;
+        any |= planes[p].status == 0;
+    }
+    if (!any) return cudaSuccess;
+    if (b.nchunks) k_rice_emit<<<g, 128, 0, s>>>(b, sc.block, sc.res);
+    const size_t sm = (size_t)3 * maxH * sizeof(int32_t);
+    if (maxH <= 1024)
+        k_med_rebuild_diag<1><<<np, (maxH + 31) / 32 * 32, sm, s>>>(b, sc.res, sc.skew);
+    else if (maxH <= 2048)
+        k_med_rebuild_diag<2><<<np, 1024, sm, s>>>(b, sc.res, sc.skew);
+    else
+        k_med_rebuild_diag<4><<<np, 1024, sm, s>>>(b, sc.res, sc.skew);
+    k_deskew<<<dim3(148 * 2, np), 256, 0, s>>>(b, sc.skew);
+    if ((e = cudaMemsetAsync(sc.costs, 0, 2 * np * sizeof(unsigned long long), s))) return e;
+    k_adler<<<dim3(148, np), 256, 0, s>>>(b, sc.costs);
+    unsigned long long ab[2 * kRiceMaxPlanes];
+    if ((e = cudaMemcpyAsync(ab, sc.costs, 2 * np * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s)))
         return e;
-    }
-    // the symbol a truncated chunk stopped at must lie past the n we need
-    unsigned long long total = 0;
-    if ((e = cudaMemcpyAsync(&total, sc.total, sizeof(total), cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
-    if ((long long)total < n) { *status = 1; return cudaSuccess; }   // stream runs out early
-    TRACE_EV("sync+scan");
-    if (c.nchunks) k_rice_emit<<<g, 128, 0, s>>>(c, sc.block, n, W, H, sc.res);
-    TRACE_EV("emit");
-#if FVV_MED_DIAG
-    {
-        // one row per thread up to 1024 rows (fewer warps per barrier), else
-        // 1024 threads with up to kDiagRows rows each
-        const size_t sm = (size_t)3 * H * sizeof(int32_t);
-        if (H <= 1024)
-            k_med_rebuild_diag<1><<<1, (H + 31) / 32 * 32, sm, s>>>(sc.res, W, H, sc.skew);
-        else if (H <= 2048)
-            k_med_rebuild_diag<2><<<1, 1024, sm, s>>>(sc.res, W, H, sc.skew);
-        else
-            k_med_rebuild_diag<4><<<1, 1024, sm, s>>>(sc.res, W, H, sc.skew);
+    for (int p = 0; p < np; ++p) {
+        const unsigned long long n = (unsigned long long)planes[p].n;
+        const uint32_t A = (uint32_t)((1 + ab[2 * p]) % 65521ull);
+        const uint32_t B = (uint32_t)((n % 65521ull + ab[2 * p + 1]) % 65521ull);
+        planes[p].adler = (B << 16) | A;
     }
-#else
-    const size_t smem = (size_t)2 * W * sizeof(long long);
-    if (smem > 48 * 1024)   // per-device attribute: set on every launch of this variant
-        cudaFuncSetAttribute(k_med_rebuild, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    k_med_rebuild<<<1, 1024, smem, s>>>(sc.res, W, H, sc.skew);
-#endif
-    k_deskew<<<148 * 4, 256, 0, s>>>(sc.skew, W, H, plane);
-    TRACE_EV("rebuild");
-    if ((e = cudaMemsetAsync(sc.costs, 0, 2 * sizeof(unsigned long long), s))) return e;
-    k_adler<<<148 * 4, 256, 0, s>>>(plane, n, sc.costs);
-    unsigned long long ab[2];
-    if ((e = cudaMemcpyAsync(ab, sc.costs, sizeof(ab), cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    const uint32_t A = (uint32_t)((1 + ab[0]) % 65521ull);
-    const uint32_t B = (uint32_t)(((unsigned long long)n % 65521ull + ab[1]) % 65521ull);
-    *adler_out = (B << 16) | A;
     return cudaGetLastError();
 }
 

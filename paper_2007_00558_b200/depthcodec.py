@@ -250,9 +250,10 @@ def _compress_plane(plane: np.ndarray) -> bytes:
     return _PLANE_HEADER.pack(k.value, flag, W * H, len(blob), zlib.adler32(plane.tobytes())) + blob
 
 
-def _decompress_plane_dev(data: bytes, offset: int, shape):
-    """depthcodec._decompress_plane (depthcodec.py:386-409) with the Rice +
-    MED stage on the GPU; returns (device plane tensor, adler32, new offset)."""
+def _parse_plane(data: bytes, offset: int, shape):
+    """Host half of depthcodec._decompress_plane (depthcodec.py:386-397): the
+    plane header, the blob and the zlib stage. Returns (k, stream, adler32,
+    new offset)."""
     if len(data) - offset < _PLANE_HEADER.size:
         raise DecodeError("plane header truncated")
     k, flag, n, blob_len, check = _PLANE_HEADER.unpack_from(data, offset)
@@ -261,21 +262,49 @@ def _decompress_plane_dev(data: bytes, offset: int, shape):
     if len(blob) != blob_len:
         raise DecodeError("plane blob truncated")
     offset += blob_len
-    stream = zlib.decompress(blob) if flag else blob
+    try:
+        stream = zlib.decompress(blob) if flag else blob
+    except zlib.error as e:
+        raise DecodeError(f"payload does not decode: {e}") from None
     if n != shape[0] * shape[1]:
         raise DecodeError("plane symbol count mismatch")
-    H, W = shape
+    return k, stream, check, offset
+
+
+def _decode_planes_dev(planes):
+    """Rice + MED stage of several planes in ONE batched GPU call
+    (fvv_rice_decode_planes; their recurrences run concurrently). `planes` is
+    a list of (k, stream bytes, adler32, (H, W)); returns device tensors."""
     ctx = _native.context()
-    s = _dev.upload(np.frombuffer(stream, dtype=np.uint8), np.uint8) if stream else None
-    out = _dev.empty((H, W), np.uint8)
-    adler = C.c_uint32()
+    n = len(planes)
+    keep, outs = [], []
+    for k, stream, _, (H, W) in planes:
+        keep.append(_dev.upload(np.frombuffer(stream, dtype=np.uint8), np.uint8)
+                    if stream else None)
+        outs.append(_dev.empty((H, W), np.uint8))
+    VP = C.c_void_p * n
+    I64, I32 = C.c_int64 * n, C.c_int32 * n
+    adlers, status = (C.c_uint32 * n)(), I32()
+    ctx.call("fvv_rice_decode_planes", n, VP(*[_dev.ptr(t) for t in keep]),
+             I64(*[len(p[1]) for p in planes]), I32(*[int(p[0]) for p in planes]),
+             I32(*[int(p[3][1]) for p in planes]), I32(*[int(p[3][0]) for p in planes]),
+             VP(*[t.data_ptr() for t in outs]), adlers, status)
+    for i, (_, _, check, _) in enumerate(planes):
+        if status[i]:
+            raise DecodeError("rice stream truncated")
+        if adlers[i] != check:
+            raise DecodeError("plane checksum mismatch")
+    return outs
+
+
+def _decompress_plane_dev(data: bytes, offset: int, shape):
+    """depthcodec._decompress_plane (depthcodec.py:386-409), GPU Rice + MED;
+    returns (device plane tensor, new offset)."""
+    k, stream, check, offset = _parse_plane(data, offset, shape)
     try:
-        ctx.call("fvv_rice_decode_plane", _dev.ptr(s), len(stream), int(k), int(n), W, H,
-                 out.data_ptr(), C.byref(adler))
+        out = _decode_planes_dev([(k, stream, check, shape)])[0]
     except ValueError as e:
         raise DecodeError(str(e)) from None
-    if adler.value != check:
-        raise DecodeError("plane checksum mismatch")
     return out, offset
 
 
@@ -316,21 +345,41 @@ def encode_lossless(img: Yuv420Image, timestamp_us: int = 0,
     return EncodedFrame(MEDIA_DEPTH, codec_id, img.width, img.height, timestamp_us, payload)
 
 
-def decode_lossless_planes(frame: EncodedFrame):
-    """The three YUV420 planes of a CODEC_PRED_RICE depth frame as device
-    tensors (the form the edge server feeds K0, pipeline.py:469-472)."""
-    w, h = frame.width, frame.height
+def decode_lossless_many(frames):
+    """The YUV420 planes of several CODEC_PRED_RICE depth frames (e.g. every
+    reference camera of a render tick) as device tensors, decoded in one
+    batched GPU call: returns [(y, u, v), ...] (the form the edge server feeds
+    K0, pipeline.py:469-472)."""
+    planes, layout = [], []
+    for frame in frames:
+        if frame.codec_id != CODEC_PRED_RICE:
+            raise UnsupportedCodecError("decode_lossless_many takes CODEC_PRED_RICE frames")
+        w, h = frame.width, frame.height
+        try:
+            off = 0
+            for shape in ((h, w), (h // 2, w // 2), (h // 2, w // 2)):
+                k, stream, check, off = _parse_plane(frame.payload, off, shape)
+                planes.append((k, stream, check, shape))
+        except DecodeError:
+            raise
+        except Exception as e:
+            raise DecodeError(f"payload does not decode: {e}") from e
+        if off != len(frame.payload):
+            raise DecodeError("trailing bytes after planes")
+        layout.append(len(planes) - 3)
     try:
-        y, off = _decompress_plane_dev(frame.payload, 0, (h, w))
-        u, off = _decompress_plane_dev(frame.payload, off, (h // 2, w // 2))
-        v, off = _decompress_plane_dev(frame.payload, off, (h // 2, w // 2))
+        outs = _decode_planes_dev(planes)
     except DecodeError:
         raise
-    except Exception as e:
-        raise DecodeError(f"payload does not decode: {e}") from e
-    if off != len(frame.payload):
-        raise DecodeError("trailing bytes after planes")
-    return y, u, v
+    except ValueError as e:
+        raise DecodeError(str(e)) from None
+    return [tuple(outs[i:i + 3]) for i in layout]
+
+
+def decode_lossless_planes(frame: EncodedFrame):
+    """The three YUV420 planes of one CODEC_PRED_RICE depth frame as device
+    tensors (one batched GPU call)."""
+    return decode_lossless_many([frame])[0]
 
 
 def decode_lossless(frame: EncodedFrame) -> Yuv420Image:

@@ -127,6 +127,19 @@ class EdgeRenderer:
                       int(bool(hole_closing)), None, None)
         self.ingested.add(cid)
 
+    def ingest_encoded_many(self, frames: Mapping, depth_range,
+                            hole_closing: bool = True) -> None:
+        """Live frames in the edge server's wire format, ``{cam_id: (rgb,
+        EncodedFrame)}`` with MED + Rice coded 12-bit YUV420 depth
+        (pipeline.py:466-472): every camera's depth planes are decoded in one
+        batched GPU call, then K0 (YUV420 decode + fill candidates) and K1."""
+        from .depthcodec import decode_lossless_many
+
+        items = list(frames.items())
+        planes = decode_lossless_many([enc for _, (_, enc) in items])
+        for (cid, (rgb, _)), (y, u, v) in zip(items, planes):
+            self.ingest_yuv(cid, rgb, y, u, v, depth_range, hole_closing=hole_closing)
+
     # -- rendering -------------------------------------------------------------
 
     def plan(self, virtuals: Sequence, refs=None):

@@ -170,3 +170,55 @@ def test_edge_server_ingests_the_wire_format(DC):
             r.ingest_yuv(cid, c.rgb, *planes, rng_)
         outs.append(r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.gpu
+def test_batched_decode_of_several_frames(DC):
+    """decode_lossless_many (all planes of several frames in one GPU call)
+    equals per-frame decoding, including planes of different sizes."""
+    g = golden("rice.npz")
+    frames, expect = [], []
+    for name in SMALL:
+        y, u, v = g[f"{name}_y"], g[f"{name}_u"], g[f"{name}_v"]
+        frames.append(_frame(DC, g[f"{name}_payload"].tobytes(), y.shape[1], y.shape[0]))
+        expect.append((y, u, v))
+    y, u, v = scene_image()
+    frames.append(_frame(DC, g["scene_payload"].tobytes(), y.shape[1], y.shape[0]))
+    expect.append((y, u, v))
+    got = DC.decode_lossless_many(frames)
+    for planes, exp in zip(got, expect):
+        for p, e in zip(planes, exp):
+            np.testing.assert_array_equal(p.cpu().numpy(), e)
+    # one bad frame in a batch raises DecodeError
+    bad = _frame(DC, g["noise_payload"].tobytes()[:-3], 64, 48)
+    with pytest.raises(DC.DecodeError):
+        DC.decode_lossless_many(frames[:2] + [bad])
+
+
+@pytest.mark.gpu
+def test_edge_server_ingests_encoded_frames_in_one_batch(DC):
+    from paper_2007_00558_b200.engine import EdgeRenderer
+    from paper_2007_00558_b200.types import DepthRange
+
+    wl = workload("c1", 8, 2007)
+    rng_ = DepthRange(0.5, 6.5)
+    enc, planes = {}, {}
+    for cid in wl.refs[0]:
+        c = wl.frames[0][cid]
+        d = c.depth_frame()
+        y, u, v = O.pack_yuv420(O.quantize12(d.depth, d.validity, 0.5, 6.5))
+        enc[cid] = (c.rgb, DC.encode_lossless(DC.Yuv420Image(y, u, v)))
+        planes[cid] = (y, u, v)
+    outs = []
+    for batched in (False, True):
+        r = EdgeRenderer(wl.rig)
+        for cid in wl.refs[0]:
+            c = wl.frames[0][cid]
+            r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+        if batched:
+            r.ingest_encoded_many(enc, rng_)
+        else:
+            for cid in wl.refs[0]:
+                r.ingest_yuv(cid, wl.frames[0][cid].rgb, *planes[cid], rng_)
+        outs.append(r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -65,6 +65,46 @@ for name, p in (("y", y), ("u", u), ("v", v)):
     planes[name] = {"k": k.value, "stream_bytes": nbytes, "encode_us": round(dev_us, 1),
                     "decode_us": round(ddev_us, 1), "decode_wall_us": round(dwall_us, 1)}
 out["planes"] = planes
+# a render tick's worth: the 3 reference cameras' depth frames, all 9 planes
+# decoded in one batched call (the MED recurrences run concurrently)
+encs = []
+for cid in wl.refs[0]:
+    dd = wl.frames[0][cid].depth_frame()
+    yy, uu, vv = O.pack_yuv420(O.quantize12(dd.depth, dd.validity, 0.5, 6.5))
+    encs.append(DC.encode_lossless(DC.Yuv420Image(yy, uu, vv)))
+DC.decode_lossless_many(encs)
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(5):
+    DC.decode_lossless_many(encs)
+torch.cuda.synchronize()
+out["decode_3_frames_batched_ms"] = round((time.perf_counter() - t) * 1e3 / 5, 2)
+t = time.perf_counter()
+for _ in range(5):
+    for e in encs:
+        DC.decode_lossless_planes(e)
+torch.cuda.synchronize()
+out["decode_3_frames_one_by_one_ms"] = round((time.perf_counter() - t) * 1e3 / 5, 2)
+# the GPU stage alone (headers parsed and zlib-inflated beforehand)
+parsed = []
+for e in encs:
+    off = 0
+    for shape in ((e.height, e.width), (e.height // 2, e.width // 2), (e.height // 2, e.width // 2)):
+        k_, st_, ck_, off = DC._parse_plane(e.payload, off, shape)
+        parsed.append((k_, st_, ck_, shape))
+t = time.perf_counter()
+for _ in range(5):
+    DC._decode_planes_dev(parsed)
+torch.cuda.synchronize()
+out["decode_3_frames_gpu_stage_ms"] = round((time.perf_counter() - t) * 1e3 / 5, 2)
+t = time.perf_counter()
+for _ in range(5):
+    for e in encs:
+        off = 0
+        for shape in ((e.height, e.width), (e.height // 2, e.width // 2),
+                      (e.height // 2, e.width // 2)):
+            off = DC._parse_plane(e.payload, off, shape)[3]
+out["decode_3_frames_host_zlib_stage_ms"] = round((time.perf_counter() - t) * 1e3 / 5, 2)
 t = time.perf_counter()
 enc = DC.encode_lossless(img)
 out["encode_lossless_ms"] = round((time.perf_counter() - t) * 1e3, 2)
