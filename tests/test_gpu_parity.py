@@ -302,3 +302,33 @@ def test_fused_ingest_fill_on_partial_tiles(cuda, W, H):
         assert filled.any()
         np.testing.assert_array_equal(v_out.cpu().numpy(), ov)
         np.testing.assert_array_equal(d_out.cpu().numpy(), od)
+
+
+@pytest.mark.parametrize("nrefs,splat", [(9, 1), (6, 2), (16, 1)])
+def test_many_references_bit_exact(cuda, nrefs, splat):
+    """More than 4 references selects the 16-slot kernel instantiations (fast
+    path for the default splat/crack, generic otherwise); the c4 rig has 16
+    cameras."""
+    from paper_2007_00558_b200 import synthesis as S
+
+    from paper_2007_00558_b200 import scenes
+
+    wl = scenes.make_workload("c4" if nrefs > 9 else "c2", seed=2007, scale=16 if nrefs > 9 else 8,
+                              n_views=1, cameras="all")
+    v = wl.virtuals[0]
+    ids = sorted(wl.frames[0])[:nrefs]
+    refs = sorted(ids, key=lambda i: float(np.linalg.norm(wl.rig[i].pose.center
+                                                          - v.pose.center)))
+    inputs = wl.inputs(0, refs)
+    cfg = S.SynthesisConfig(splat_radius=splat)
+    ocfg = dict(O.DEFAULT_CFG, splat_radius=splat)
+    frame, prov = S.synthesize_view(v, inputs, refs, cfg, return_provenance=True)
+    arrs = []
+    for rid in refs:
+        c = wl.frames[0][rid]
+        lf = c.depth_frame()
+        arrs.append(dict(calib=c.calib, rgb=c.rgb, live_depth=lf.depth, live_validity=lf.validity,
+                         bg_depth=c.bg_depth, bg_validity=c.bg_validity))
+    o_rgb, o_prov = O.synthesize_view(v, arrs, ocfg)
+    np.testing.assert_array_equal(frame.pixels, o_rgb)
+    np.testing.assert_array_equal(prov, o_prov)
