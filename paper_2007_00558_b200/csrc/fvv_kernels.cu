@@ -1,14 +1,17 @@
 // sm_100a kernels of the edge-server view-synthesis path.
 //
-//   K0+K1+ingest  k_preprocess   decode (mm / YUV420-12 / f32), joint-bilateral
-//                                hole fill, pack RGB+flags texels, warp depth
-//   K2            k_forward_warp forward 3-D warp, one 64-bit atomicMin per
-//                                source pixel into a padded keyed z canvas
-//   K3            k_resolve      per 32x8 target tile and per contribution:
-//                                splat ring + FG cull + crack median in shared
-//                                memory, f64 backward projection, masked
-//                                bilinear fetch; then the two layer mixes and
-//                                the FG-over-BG composite -> RGB8 + provenance
+//   K0  k_preprocess     decode (mm / YUV420-12 / f32), pack RGB+flags texels
+//                        and warp depth, list the hole-fill candidates
+//   K1  k_fill_g8/k_fill joint-bilateral fill of the listed candidates
+//   K2  k_forward_warp   forward 3-D warp, one 64-bit atomicMin per source
+//                        pixel into a padded keyed z canvas, exact z kept
+//   K3  k_resolve_fast   per 32x8 target tile and per contribution: splat
+//       (k_resolve_generic for other splat radii / crack windows)
+//                        ring + FG cull + crack median in shared memory, f64
+//                        backward projection, masked bilinear fetch; then the
+//                        two layer mixes and the FG-over-BG composite -> RGB8
+//                        + provenance
+//   K4  k_inpaint        (extension) background-biased hole fill
 //
 // Each kernel cites the reference lines it replaces; the numerics contract is
 // in fvv_common.cuh and oracle/fvv_oracle.py.
@@ -944,15 +947,17 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 // synthesis.py:39-40) with every tile dimension a compile-time constant.
 //
 // Per 32x8 target tile and per contribution:
-//   keys   12x36 canvas cells (tile + 2-px halo) staged by cp.async into a
-//          double buffer (next contribution's tile in flight while the
+//   keys   12x36 canvas cells (tile + 2-px halo) staged by TMA (or cp.async)
+//          into a double buffer (next contribution's tile in flight while the
 //          current one is resolved). Keys of stale generations compare
 //          larger than any fresh key, so the ring min needs no sanitising.
 //   cells  10x34 (tile + 1-px halo): centre key or 8-ring min (splat), FG cull
-//          on < 5 centre-covered 8-neighbours, winner z recomputed in f64.
-//   pixel  crack median (8-value sorting network), backward projection and
-//          masked bilinear fetch; per-contribution result kept in smem.
-// then mix_layer x2 and composite per pixel.
+//          on < 5 centre-covered 8-neighbours.
+//   pixel  winner z from K2's exact z plane, crack median (8-value sorting
+//          network), backward projection and masked bilinear fetch; valid
+//          per-contribution results kept in smem.
+// then mix_layer x2 (valid contributions only) and the composite per pixel,
+// the merged layers held as rounded packed colours in registers.
 
 #ifndef FVV_K3_MINB
 #define FVV_K3_MINB 5
