@@ -71,6 +71,9 @@ def parse():
                          "on their own CUDA streams, so one frame's decode/fill (K0/K1) "
                          "overlaps another's warp/resolve (K2/K3); default 2, and 1 for c0 "
                          "whose 0.1 ms steps are bound by the host's launch calls")
+    ap.add_argument("--extensions", action="store_true",
+                    help="enable the two extensions outside the reference (angular blend "
+                         "weights, K4 disocclusion inpainting); default is parity mode")
     ap.add_argument("--gen", default="auto", choices=("auto", "host", "gpu"),
                     help="input generator: numpy ray caster on the host, or scenes_gpu in "
                          "HBM (auto: gpu for c3/c4, whose host generation takes minutes)")
@@ -366,7 +369,11 @@ def run_ours(args):
         views = [D.shard(nv, ws, rank)] if args.config in ("c2", "c4") else [[0]]
     cams = sorted(frames[0])
     P = max(1, args.pipelines)
-    engs = [EdgeRenderer(wl.rig, private=P > 1) for _ in range(P)]
+    from paper_2007_00558_b200.synthesis import SynthesisConfig
+
+    rcfg = SynthesisConfig(reference_count=len(wl.refs[0]), angular_weight=args.extensions,
+                           inpaint=args.extensions)
+    engs = [EdgeRenderer(wl.rig, cfg=rcfg, private=P > 1) for _ in range(P)]
     eng = engs[0]
     bg_done = set()
     for fr in frames:
@@ -580,6 +587,8 @@ def run_ours(args):
                                          f"views sharded x{ws} + NCCL frame broadcast"),
                    "views_per_step": views_per_step, "frames_rotating": len(staged),
                    "pipelines": P,
+                   "mode": "extensions (angular weights + inpainting)" if args.extensions
+                           else "parity (reference semantics)",
                    "l2": f"inputs rotate over {len(staged)} pre-staged frames; per-step "
                          f"footprint (live inputs + BG models + 2R z canvases) exceeds the "
                          f"126 MB L2 across the rotation",

@@ -63,11 +63,12 @@ typedef struct fvv_synth_cfg {
                                   by 1/(theta + angular_epsilon), theta the angle at
                                   the surface point between the reference and the
                                   virtual camera rays */
-    uint8_t inpaint;           /* 1: K4 fills holes from the background side;
-                                  provenance 3 marks inpainted pixels */
+    uint8_t inpaint;           /* 1: K4 fills each hole from the nearest non-hole
+                                  pixels left/right/up/down, background side
+                                  only; provenance 3 marks inpainted pixels */
     uint8_t reserved[3];
     double angular_epsilon;    /* rad, > 0 (default 0.0175 = 1 degree) */
-    int32_t inpaint_radius;    /* max march distance in pixels, 1..4096 (default 64) */
+    int32_t inpaint_radius;    /* max distance to a candidate, pixels, 1..4096 (default 64) */
     int32_t reserved2;
 } fvv_synth_cfg;
 

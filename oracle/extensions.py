@@ -60,14 +60,15 @@ def angular_mix(contribs, virtual, srcs, weights, band_rel, eps):
 
 
 def inpaint(rgb, prov, depth, radius=64, bg_band=0.05):
-    """K4: each hole (prov 0) takes the 1/distance-weighted mean colour of the
-    first non-hole pixel in each of 8 directions whose depth is within
-    bg_band of the farthest such pixel (f32 arithmetic). Returns (rgb, prov)."""
+    """K4: each hole (prov 0) takes the first non-hole pixel (prov 1 or 2) to
+    its left, right, top and bottom within `radius`, keeps those whose depth
+    is within bg_band of the farthest one and averages their colours with
+    1/distance weights (f32, in that order). Returns (rgb, prov)."""
     rgb = rgb.copy()
     out_prov = prov.copy()
     H, W = prov.shape
-    dirs = [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (1, -1), (-1, 1), (-1, -1)]
     src_rgb = rgb.copy()
+    dirs = [(-1, 0), (1, 0), (0, -1), (0, 1)]   # left, right, up, down
     for y, x in zip(*np.nonzero(prov == 0)):
         cands = []
         for dx, dy in dirs:
@@ -78,8 +79,7 @@ def inpaint(rgb, prov, depth, radius=64, bg_band=0.05):
                 if not (0 <= xx < W and 0 <= yy < H):
                     break
                 if prov[yy, xx] in (1, 2):
-                    dist = np.float32(1.41421356) * np.float32(s) if dx and dy else np.float32(s)
-                    cands.append((np.float32(depth[yy, xx]), dist, src_rgb[yy, xx]))
+                    cands.append((np.float32(depth[yy, xx]), np.float32(s), src_rgb[yy, xx]))
                     break
         if not cands:
             continue

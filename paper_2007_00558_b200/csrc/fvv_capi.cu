@@ -59,6 +59,7 @@ struct fvv_ctx {
     // passes no provenance buffer
     uint8_t *iprov = nullptr;
     float *idepth = nullptr;
+    int16_t *idist = nullptr;   // 4 x [px] K4 distance planes
     size_t icap = 0;
     // K3's TMA map of the canvases and what it was built for
     CUtensorMap kmap;
@@ -456,10 +457,13 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         if (px > ctx->icap) {
             CK(cudaFree(ctx->iprov));
             CK(cudaFree(ctx->idepth));
+            CK(cudaFree(ctx->idist));
             ctx->iprov = nullptr;
             ctx->idepth = nullptr;
+            ctx->idist = nullptr;
             CK(cudaMalloc(&ctx->iprov, px));
             CK(cudaMalloc(&ctx->idepth, px * sizeof(float)));
+            CK(cudaMalloc(&ctx->idist, 4 * px * sizeof(int16_t)));
             ctx->icap = px;
         }
         if (!rp.prov_out) rp.prov_out = ctx->iprov;
@@ -471,13 +475,20 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         ip.rgb = rgb_out;
         ip.prov = rp.prov_out;
         ip.depth = ctx->idepth;
+        ip.dist_l = ctx->idist;
+        ip.dist_r = ctx->idist + px;
+        ip.dist_u = ctx->idist + 2 * px;
+        ip.dist_d = ctx->idist + 3 * px;
     }
     if (r == 1 && resolve_uses_tma() &&
         (rc = canvas_tensor_map(ctx, ctx->cn, virt.width, virt.height, r, rp)))
         return rc;
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
-    if (ip.rgb) LAUNCH(launch_inpaint(ip, ctx->stream));
+    if (ip.rgb) {
+        LAUNCH(launch_inpaint(ip, ctx->stream));
+        ctx->launches += 2;   // rows, columns and fill passes
+    }
     return FVV_OK;
 }
 
@@ -533,6 +544,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     cudaFree(ctx->ncand);
     cudaFree(ctx->iprov);
     cudaFree(ctx->idepth);
+    cudaFree(ctx->idist);
     cudaFree(ctx->range_w);
     for (auto &r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);

@@ -11,7 +11,7 @@
 //                        backward projection, masked bilinear fetch; then the
 //                        two layer mixes and the FG-over-BG composite -> RGB8
 //                        + provenance
-//   K4  k_inpaint        (extension) background-biased hole fill
+//   K4  k_inpaint_rows/cols (extension) background-biased hole fill
 //
 // Each kernel cites the reference lines it replaces; the numerics contract is
 // in fvv_common.cuh and oracle/fvv_oracle.py.
@@ -1509,48 +1509,122 @@ cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
 // Background-biased disocclusion fill. A hole of a forward-warped view is
 // where the virtual camera sees past a foreground edge that no reference saw
 // behind, so the right colour is the background beside it. Each hole pixel
-// marches up to `radius` pixels in 8 directions to the first non-hole pixel,
-// keeps the candidates whose depth lies within bg_band of the farthest one,
-// and averages them with 1/distance weights. Filled pixels get provenance 3;
-// both 0 and 3 read as holes, so the result does not depend on the order in
-// which threads fill.
+// takes the first non-hole pixel to its left, right, top and bottom (within
+// `radius` pixels), keeps the candidates whose depth lies within bg_band of
+// the farthest one and averages their colours with 1/distance weights;
+// provenance 3 marks it. Two passes, O(1) per pixel however large the holes:
+//   rows     one warp per row, 512-px steps (16 px per lane, one 16-byte
+//            load), nearest-source carries by warp max/min scans, left->right
+//            and right->left; stores each hole's left / right distances
+//            (int16, -1 = none);
+//   columns  32 adjacent columns per CTA, each split into 32 row chunks
+//            (one thread each, so every row step of a warp is one coalesced
+//            load): chunk boundaries first, then every chunk rescans with the
+//            carries from above and below: up / down distances;
+//   fill     every hole pixel in parallel from its four distances.
+// Prov is only written by the fill pass, so the passes see the composite's
+// holes (0) and sources (1, 2) only.
 
-__global__ void k_inpaint(const InpaintParams p) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-    if (x >= p.W || y >= p.H) return;
-    const size_t i = (size_t)y * p.W + x;
-    if (p.prov[i] != 0) return;
-    const int dxs[8] = {1, -1, 0, 0, 1, 1, -1, -1};
-    const int dys[8] = {0, 0, 1, -1, 1, -1, 1, -1};
-    float cz[8], cd[8];
-    size_t ci[8];
-    int n = 0;
-    float zmax = 0.0f;
-    for (int d = 0; d < 8; ++d) {
-        int xx = x, yy = y;
-        for (int s = 1; s <= p.radius; ++s) {
-            xx += dxs[d];
-            yy += dys[d];
-            if (xx < 0 || xx >= p.W || yy < 0 || yy >= p.H) break;
-            const size_t j = (size_t)yy * p.W + xx;
-            const uint8_t pv = p.prov[j];
-            if (pv == 1 || pv == 2) {
-                const float z = p.depth[j];
-                cz[n] = z;
-                cd[n] = (dxs[d] && dys[d]) ? 1.41421356f * (float)s : (float)s;
-                ci[n] = j;
-                zmax = fmaxf(zmax, z);
-                ++n;
-                break;
-            }
+__device__ __forceinline__ bool inpaint_src(uint8_t pv) { return pv == 1 || pv == 2; }
+
+__global__ void k_inpaint_rows(const InpaintParams p) {
+    // one warp per row; lane l owns 16 contiguous pixels of each 512-px step
+    // (one 16-byte load), carries of the nearest source come from warp scans
+    const int lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (y >= p.H) return;
+    const uint8_t *row = p.prov + (size_t)y * p.W;
+    int16_t *L = p.dist_l + (size_t)y * p.W, *R = p.dist_r + (size_t)y * p.W;
+    const bool vec = (p.W & 15) == 0 && ((uintptr_t)row & 15) == 0;
+    const int nsteps = (p.W + 511) / 512;
+    auto load16 = [&](int x0, uint8_t (&v)[16]) {
+        if (vec && x0 + 15 < p.W) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row + x0));
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = x0 + k < p.W ? row[x0 + k] : 0;
         }
+    };
+    int carry = -1;   // last source column left of this step
+    for (int st = 0; st < nsteps; ++st) {
+        const int x0 = st * 512 + lane * 16;
+        uint8_t v[16];
+        load16(x0, v);
+        int mine = -1;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (x0 + k < p.W && inpaint_src(v[k])) mine = x0 + k;
+        // exclusive max-scan over lanes: the last source before this lane
+        int incl = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl = max(incl, t);
+        }
+        int left = __shfl_up_sync(0xffffffffu, incl, 1);
+        left = lane ? max(left, carry) : carry;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int x = x0 + k;
+            if (x >= p.W) break;
+            if (inpaint_src(v[k])) left = x;
+            else L[x] = (left >= 0 && x - left <= p.radius) ? (int16_t)(x - left) : -1;
+        }
+        carry = max(carry, __shfl_sync(0xffffffffu, incl, 31));
+    }
+    carry = -1;   // first source column right of this step
+    for (int st = nsteps - 1; st >= 0; --st) {
+        const int x0 = st * 512 + lane * 16;
+        uint8_t v[16];
+        load16(x0, v);
+        int mine = -1;
+#pragma unroll
+        for (int k = 15; k >= 0; --k)
+            if (x0 + k < p.W && inpaint_src(v[k])) mine = x0 + k;
+        // exclusive min-scan from the right (-1 = none)
+        int incl = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_down_sync(0xffffffffu, incl, o);
+            if (lane + o < 32 && t >= 0 && (incl < 0 || t < incl)) incl = t;
+        }
+        int right = __shfl_down_sync(0xffffffffu, incl, 1);
+        if (lane == 31) right = -1;
+        if (right < 0) right = carry;
+#pragma unroll
+        for (int k = 15; k >= 0; --k) {
+            const int x = x0 + k;
+            if (x >= p.W) continue;
+            if (inpaint_src(v[k])) right = x;
+            else R[x] = (right >= 0 && right - x <= p.radius) ? (int16_t)(right - x) : -1;
+        }
+        const int first = __shfl_sync(0xffffffffu, incl, 0);
+        if (first >= 0) carry = first;
+    }
+}
+
+// the fill of one hole pixel from its four candidates (left, right, up,
+// down distances; <= 0 = none), f32, in that order
+__device__ __forceinline__ void inpaint_pixel(const InpaintParams &p, size_t i, int dl, int dr,
+                                              int du, int dd) {
+    const size_t ci[4] = {i - (size_t)(dl > 0 ? dl : 0), i + (size_t)(dr > 0 ? dr : 0),
+                          i - (size_t)(du > 0 ? du : 0) * p.W, i + (size_t)(dd > 0 ? dd : 0) * p.W};
+    const int cd[4] = {dl, dr, du, dd};
+    float zmax = 0.0f, cz[4];
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cz[k] = cd[k] > 0 ? p.depth[ci[k]] : 0.0f;
+        if (cd[k] > 0) { zmax = fmaxf(zmax, cz[k]); ++n; }
     }
     if (n == 0) return;
     const float zlo = zmax * (float)(1.0 - p.bg_band);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, aw = 0.f;
-    for (int k = 0; k < n; ++k) {
-        if (cz[k] < zlo) continue;
-        const float w = 1.0f / cd[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (cd[k] <= 0 || cz[k] < zlo) continue;
+        const float w = 1.0f / (float)cd[k];
         const uint8_t *c = p.rgb + ci[k] * 3;
         a0 += w * c[0];
         a1 += w * c[1];
@@ -1564,9 +1638,78 @@ __global__ void k_inpaint(const InpaintParams p) {
     p.prov[i] = 3;
 }
 
+// Columns: a 32 x 32 CTA owns 32 adjacent columns; thread (tx, ty) scans row
+// chunk ty of column tx. Chunks publish their first / last non-hole rows,
+// then each thread rescans its chunk with the carries of the chunks above
+// and below, writing the vertical distances and filling its holes.
+__global__ void __launch_bounds__(1024) k_inpaint_cols(const InpaintParams p) {
+    __shared__ int s_first[32][33], s_last[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int x = blockIdx.x * 32 + tx;
+    const int rows = (p.H + 31) / 32;
+    const int ya = ty * rows, yb = min(p.H, ya + rows);
+    int first = -1, last = -1;
+    if (x < p.W)
+        for (int y0 = ya; y0 < yb; y0 += 8) {
+            uint8_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)   // 8 independent loads in flight
+                v[k] = y0 + k < yb ? p.prov[(size_t)(y0 + k) * p.W + x] : 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (y0 + k < yb && inpaint_src(v[k])) {
+                    if (first < 0) first = y0 + k;
+                    last = y0 + k;
+                }
+        }
+    s_first[ty][tx] = first;
+    s_last[ty][tx] = last;
+    __syncthreads();
+    if (x >= p.W) return;
+    int up = -1, down = -1;   // carries: last source above the chunk, first below
+    for (int c = ty - 1; c >= 0 && up < 0; --c) up = s_last[c][tx];
+    for (int c = ty + 1; c < 32 && down < 0; ++c) down = s_first[c][tx];
+    for (int y0 = ya; y0 < yb; y0 += 8) {
+        uint8_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = y0 + k < yb ? p.prov[(size_t)(y0 + k) * p.W + x] : 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = y0 + k;
+            if (y >= yb) break;
+            if (inpaint_src(v[k])) up = y;
+            else p.dist_u[(size_t)y * p.W + x] = (up >= 0 && y - up <= p.radius) ? (int16_t)(y - up) : -1;
+        }
+    }
+    for (int y1 = yb - 1; y1 >= ya; y1 -= 8) {
+        uint8_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = y1 - k >= ya ? p.prov[(size_t)(y1 - k) * p.W + x] : 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = y1 - k;
+            if (y < ya) break;
+            if (inpaint_src(v[k])) down = y;
+            else p.dist_d[(size_t)y * p.W + x] =
+                (down >= 0 && down - y <= p.radius) ? (int16_t)(down - y) : -1;
+        }
+    }
+}
+
+// every hole pixel in parallel, from its four distances
+__global__ void k_inpaint_fill(const InpaintParams p) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= p.W) return;
+    const size_t i = (size_t)y * p.W + x;
+    if (p.prov[i] != 0) return;
+    inpaint_pixel(p, i, p.dist_l[i], p.dist_r[i], p.dist_u[i], p.dist_d[i]);
+}
+
 cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s) {
     if (p.W <= 0 || p.H <= 0) return cudaSuccess;
-    k_inpaint<<<dim3((p.W + 127) / 128, p.H), 128, 0, s>>>(p);
+    k_inpaint_rows<<<(p.H + 7) / 8, 256, 0, s>>>(p);
+    k_inpaint_cols<<<(p.W + 31) / 32, dim3(32, 32), 0, s>>>(p);
+    k_inpaint_fill<<<dim3((p.W + 127) / 128, p.H), 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -126,11 +126,13 @@ struct ResolveParams {
 // a composited view
 struct InpaintParams {
     int W, H;
-    int radius;              // max march distance in pixels
+    int radius;              // max distance to a candidate, pixels (<= 4096)
     double bg_band;          // candidates within (1 - bg_band) * z_max count as background
     uint8_t *rgb;            // in/out: holes are filled in place
     uint8_t *prov;           // in/out: 0 hole -> 3 inpainted
     const float *depth;      // composite depth (0 at holes)
+    int16_t *dist_l, *dist_r, *dist_u, *dist_d;  // scratch [H*W]: distances to the
+                                        // nearest non-hole pixel (-1 none within radius)
 };
 
 struct MixParams {
