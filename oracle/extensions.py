@@ -36,7 +36,9 @@ def angular_factor(virtual, src, z, eps):
     den = np.sqrt(np.sum(a * a, -1) * np.sum(b * b, -1))
     with np.errstate(invalid="ignore", divide="ignore"):
         cs = np.where(den > 0, np.sum(a * b, -1) / den, 1.0)
-    return 1.0 / (np.arccos(np.clip(cs, -1.0, 1.0)) + eps)
+    # the kernel evaluates the arccos in single precision
+    theta = np.arccos(np.clip(cs, -1.0, 1.0).astype(np.float32)).astype(np.float64)
+    return 1.0 / (theta + eps)
 
 
 def angular_mix(contribs, virtual, srcs, weights, band_rel, eps):

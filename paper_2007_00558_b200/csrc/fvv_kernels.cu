@@ -682,7 +682,8 @@ __device__ __forceinline__ double ring_median(const double *sz, int BC, int cent
 // Extension (not in the reference): angular factor of a blend weight,
 // 1 / (theta + eps), theta = angle at the surface point X (the virtual pixel's
 // ray at depth z) between the rays to the reference and to the virtual camera
-// centres. Free-order f64: this path has no reference to match.
+// centres. Free-order f64 (the arccos in f32): this path has no reference
+// to match.
 __device__ __forceinline__ double angular_factor(const DevCam &dst, const DevCam &src, double rxd,
                                                  double ryd, double z, double eps) {
     const double px = rxd * z, py = ryd * z, pz = z;
@@ -694,7 +695,8 @@ __device__ __forceinline__ double angular_factor(const DevCam &dst, const DevCam
     const double den = sqrt((ax * ax + ay * ay + az * az) * (bx * bx + by * by + bz * bz));
     double cs = den > 0.0 ? (ax * bx + ay * by + az * bz) / den : 1.0;
     cs = fmin(fmax(cs, -1.0), 1.0);
-    return 1.0 / (acos(cs) + eps);
+    // a blend weight, not a parity quantity: the angle in single precision
+    return 1.0 / ((double)acosf((float)cs) + eps);
 }
 
 template <int MAXR>

@@ -41,10 +41,11 @@ def test_angular_weights_match_restatement(S, name):
         col, val = X.angular_mix(cs, case.virtual, srcs, [c.weight for c in layer],
                                  cfg.depth_band_rel, cfg.angular_epsilon)
         merged.append((col, val))
-    # merged layers: same validity, colours equal up to f64 rounding of acos/sqrt
+    # merged layers: same validity, colours equal up to the rounding of the
+    # single-precision arccos (CUDA's and numpy's may differ by an ulp)
     for (col, val), m in zip(merged, (b.fg, b.bg)):
         np.testing.assert_array_equal(np.asarray(m.valid, bool), val)
-        np.testing.assert_allclose(m.color[val], col[val], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(m.color[val], col[val], rtol=0, atol=1e-4)
     exp = _composite(merged[0][0], merged[0][1], merged[1][0], merged[1][1])
     d = np.abs(frame.pixels.astype(int) - exp.astype(int))
     assert d.max() <= 1 and (d == 0).all(-1).mean() >= 0.9999
