@@ -332,3 +332,29 @@ def test_many_references_bit_exact(cuda, nrefs, splat):
     o_rgb, o_prov = O.synthesize_view(v, arrs, ocfg)
     np.testing.assert_array_equal(frame.pixels, o_rgb)
     np.testing.assert_array_equal(prov, o_prov)
+
+
+def test_full_4k_edge_server_path_vs_c_oracle(cuda):
+    """Maximum size: c4's 3840x2160 rig, 4 references, generated in HBM by
+    scenes_gpu; mm decode + bilateral + synthesis bit-identical to the C
+    oracle (itself bit-identical to the numpy oracle, tests/test_oracle.py)."""
+    import torch
+
+    from oracle import c_oracle as CO
+    from paper_2007_00558_b200 import scenes_gpu
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    wl = scenes_gpu.make_workload("c4", seed=2007, n_views=1, dev=torch.device("cuda", 0))
+    v, refs = wl.virtuals[0], wl.refs[0]
+    r = EdgeRenderer(wl.rig)
+    frames = []
+    for cid in refs:
+        c = wl.frames[0][cid]
+        r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+        r.ingest_mm(cid, c.rgb, c.mm, c.validity, hole_closing=True)
+        h = c.host()
+        frames.append(dict(calib=h.calib, rgb=h.rgb, mm=h.mm, validity=h.validity,
+                           bg_depth=h.bg_depth, bg_validity=h.bg_validity))
+    img = r.render([v], [refs])[0].cpu().numpy()
+    o_rgb, _ = CO.es_view(v, frames)
+    np.testing.assert_array_equal(img, o_rgb)
