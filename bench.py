@@ -575,6 +575,26 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": peak_src}
+    # issue roofline of the same kernel: warp instructions per launch (ncu,
+    # committed capture) / event-timed launch duration, against the SM issue
+    # peak of 4 warp instructions per clock per SM (one per sub-partition)
+    issue = None
+    ifile = ROOT / "profiles" / "r01_inst.json"
+    if ifile.exists() and dom_bytes:
+        kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
+              "resolve": "k_resolve_fast"}.get(dom)
+        inst = json.loads(ifile.read_text()).get(kn)
+        sm_clk = (clk or {}).get("sm_mhz") or 1965.0
+        if inst:
+            import torch as _t
+
+            nsm = _t.cuda.get_device_properties(dev).multi_processor_count
+            ach_i = inst / (kern[dom]["avg_ms"] / 1e3)
+            peak_i = 4.0 * nsm * sm_clk * 1e6
+            issue = {"kernel": dom, "achieved": ach_i, "peak": peak_i,
+                     "unit": "warp instructions/s", "frac": ach_i / peak_i,
+                     "inst_per_launch": inst, "note": "instruction count from the committed ncu "
+                     "capture (profiles/r01_inst.json); peak = 4 issue slots/clock/SM"}
     pipe = value / ws * b_view / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": ws, "steps": args.steps,
@@ -595,6 +615,7 @@ def run_ours(args):
                    "path": "mm decode + bilateral hole fill + forward warp + resolve/blend "
                            "(full edge-server path)"},
         "roofline": roof,
+        "roofline_issue": issue,
         "roofline_pipeline": {"bytes_per_view": b_view, "achieved": pipe, "peak": hbm,
                               "unit": "GB/s", "frac": pipe / hbm,
                               "note": "SURVEY.md §8(d) B_view x views/s per GPU"},

@@ -2,6 +2,7 @@
 
     python profiles/summarize.py gpurun_out/prof.ncu-rep [launches.csv] > profiles/rNN_<name>.md
     python profiles/summarize.py --traffic gpurun_out/prof.ncu-rep > profiles/rNN_traffic.json
+    python profiles/summarize.py --inst gpurun_out/prof.ncu-rep > profiles/rNN_inst.json
 
 For every kernel launch in the report: duration, DRAM bytes read/written,
 DRAM / SM throughput, IPC, occupancy, registers, per-pipe utilisation, L2
@@ -131,6 +132,14 @@ def main():
             b = (val(d, "dram__bytes_read.sum") or 0) + (val(d, "dram__bytes_write.sum") or 0)
             traffic.setdefault(name, []).append(b)
         print(json.dumps({k: sum(v) / len(v) for k, v in traffic.items()}, indent=1))
+        return
+    if sys.argv[1] == "--inst":
+        inst = {}
+        for d in raw_rows(sys.argv[2]):
+            name = d.get("Kernel Name", ("", ""))[0].split("(")[0].split("<")[0].replace(
+                "void ", "").replace("fvv::", "")
+            inst.setdefault(name, []).append(val(d, "smsp__inst_executed.sum") or 0)
+        print(json.dumps({k: sum(v) / len(v) for k, v in inst.items()}, indent=1))
         return
     rep = sys.argv[1]
     print(f"# ncu summary: `{rep}`\n")
