@@ -110,7 +110,7 @@ int64_t fvv_launch_count(const fvv_ctx *ctx); /* kernels launched by this contex
 
 /* Per-kernel device timing: when enabled, every launch is bracketed by CUDA
  * events on the context's stream (the stream the kernel runs on).
- * kernel ids: 0 preprocess (K0+K1+ingest), 1 forward warp (K2),
+ * kernel ids: 0 preprocess (K0 decode/ingest + K1 hole fill), 1 forward warp (K2),
  * 2 resolve (K3), 3 canvas fill, 4 other. fvv_profile_read synchronises. */
 #define FVV_K_PREPROCESS 0
 #define FVV_K_FORWARD_WARP 1
@@ -264,8 +264,9 @@ int fvv_slot_set_bg(fvv_ctx *ctx, int32_t slot, const float *bg_depth,
  * runs K1 with the reference defaults first (pipeline.py:518-519). */
 int fvv_slot_ingest(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const float *depth,
                     const uint8_t *validity, int32_t hole_closing);
-/* Live frame from the 16-bit mm raster: fused K0 decode + K1 hole fill
- * (pipeline.py:518-519) + ingest. hole_closing=0 skips K1. depth_out /
+/* Live frame from the 16-bit mm raster: K0 decode + ingest (listing the hole
+ * candidates) then K1 hole fill (pipeline.py:518-519). hole_closing=0 skips
+ * K1. depth_out /
  * validity_out (may be NULL) receive the preprocessed DepthFrame. */
 int fvv_slot_ingest_mm(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint16_t *mm,
                        const uint8_t *validity, int32_t hole_closing, float *depth_out,

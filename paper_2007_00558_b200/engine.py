@@ -7,7 +7,8 @@ and the latest live frame resident in HBM; ``render`` then synthesizes any
 number of virtual views from them (``synthesize_with_config`` seam,
 pipeline.py:569-570). Frames arrive either as DepthFrames or in the wire
 formats the edge server decodes (16-bit mm raster, 12-bit YUV420), with the
-decode and hole fill fused into one kernel.
+decode + ingest in one kernel (K0) for all of a tick's cameras, followed by
+the hole fill (K1) of the pixels K0 listed.
 
 ``synthesize(virtual_camera, mvd_frame, ...)`` is the one-call convenience
 the north star names.
@@ -87,7 +88,7 @@ class EdgeRenderer:
                   depth_out: Optional[torch.Tensor] = None,
                   validity_out: Optional[torch.Tensor] = None) -> None:
         """Live frame as the 16-bit mm raster + validity sidecar (mvdio.py:132):
-        fused mm decode + bilateral hole fill + ingest."""
+        mm decode + ingest (K0), then the bilateral hole fill (K1)."""
         self._bind()
         rgb_t = _dev.upload(rgb, np.uint8)
         mm_t = _dev.upload(mm, np.uint16)
@@ -98,7 +99,7 @@ class EdgeRenderer:
         self.ingested.add(cid)
 
     def ingest_mm_many(self, frames: Mapping, hole_closing: bool = True) -> None:
-        """``{cam_id: (rgb, mm, validity)}`` in one fused launch (one grid layer
+        """``{cam_id: (rgb, mm, validity)}`` in one K0 launch (one grid layer
         per camera) — the form a render tick uses for its reference cameras."""
         self._bind()
         items = list(frames.items())
