@@ -390,10 +390,15 @@ def run_ours(args):
             return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).to(dev)
         return a
 
-    staged = []
+    # each frame lives in one flat buffer, so a multi-GPU step replicates it
+    # with a single broadcast
+    staged, flats = [], []
     for fr in frames:
-        staged.append({cid: (on_dev(fr[cid].rgb), on_dev(fr[cid].mm), on_dev(fr[cid].validity))
-                       for cid in fr})
+        order = sorted(fr)
+        flat, vs = D.pack_frame([on_dev(a) for cid in order
+                                 for a in (fr[cid].rgb, fr[cid].mm, fr[cid].validity)], dev)
+        flats.append(flat)
+        staged.append({cid: tuple(vs[3 * i:3 * i + 3]) for i, cid in enumerate(order)})
     k = wl.rig[0].intrinsics
     H, W = k.height, k.width
     vmax = max(len(v) for v in views)
@@ -407,9 +412,9 @@ def run_ours(args):
         vi = views[s % len(views)] if args.config == "c3" else views[0]
         fr = staged[fi]
         if bcast:
-            # the live MVD frame arrives at rank 0; one NCCL broadcast per
-            # tensor replicates it over NVLink (the path's only exchange)
-            D.broadcast_frame([t for cid in cams for t in fr[cid]])
+            # the live MVD frame arrives at rank 0; one NCCL broadcast of its
+            # packed buffer replicates it over NVLink (the path's only exchange)
+            D.broadcast_frame([flats[fi]])
         need = sorted({c for v in vi for c in wl.refs[v]})
         e.ingest_mm_many({cid: fr[cid] for cid in need}, hole_closing=True)
         e.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=o)

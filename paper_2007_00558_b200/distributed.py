@@ -6,10 +6,10 @@ per-pixel collective:
 
 * ``shard`` — contiguous block of views (c2, c4) or round-robin frames (c3)
   for a rank;
-* ``broadcast_frame`` — the one real exchange: the live MVD frame (RGB + u16
-  depth + validity per camera, 6 B/px) arriving at one rank is replicated to
-  all ranks with one NCCL broadcast per tensor over NVLink (gloo on CPU for
-  the host tests);
+* ``pack_frame`` / ``broadcast_frame`` — the one real exchange: the live MVD
+  frame (RGB + u16 depth + validity per camera, 6 B/px) arriving at one rank,
+  packed into one flat buffer, is replicated to all ranks with a single NCCL
+  broadcast over NVLink (gloo on CPU for the host tests);
 * ``max_over_ranks`` — device-timed step times reduced with MAX, the only
   honest multi-GPU clock.
 
@@ -55,6 +55,25 @@ def shard(n_items: int, world_size: int, rank: int, mode: str = "block") -> List
     base, extra = divmod(n_items, world_size)
     start = rank * base + min(rank, extra)
     return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+def pack_frame(tensors: Sequence[torch.Tensor], device=None):
+    """Copy a frame's tensors into ONE flat byte buffer (16-byte aligned
+    slices) and return (flat, views): the views have the tensors' dtypes and
+    shapes, so the frame is replicated with a single broadcast of `flat`."""
+    sizes = [t.numel() * t.element_size() for t in tensors]
+    offs, total = [], 0
+    for n in sizes:
+        offs.append(total)
+        total += (n + 15) // 16 * 16
+    dev = tensors[0].device if device is None else device
+    flat = torch.empty(total, dtype=torch.uint8, device=dev)
+    views = []
+    for t, o, n in zip(tensors, offs, sizes):
+        v = flat[o:o + n].view(t.dtype).view(t.shape)
+        v.copy_(t)
+        views.append(v)
+    return flat, views
 
 
 def broadcast_frame(tensors: Sequence[torch.Tensor], src: int = 0) -> None:

@@ -255,12 +255,17 @@ import torch
 from paper_2007_00558_b200 import distributed as D
 rank, ws, _ = D.init("gloo")
 # the frame arrives at rank 0; every rank must end with identical bytes
-frame = [torch.zeros(6, 8, 3, dtype=torch.uint8), torch.zeros(6, 8, dtype=torch.int16)]
+frame = [torch.zeros(6, 8, 3, dtype=torch.uint8), torch.zeros(6, 8, dtype=torch.int16),
+         torch.zeros(6, 8, dtype=torch.uint8)]
 if rank == 0:
     g = torch.Generator().manual_seed(1)
     frame[0].copy_(torch.randint(0, 256, (6, 8, 3), generator=g, dtype=torch.uint8))
     frame[1].copy_(torch.randint(0, 30000, (6, 8), generator=g, dtype=torch.int16))
-D.broadcast_frame(frame)
+    frame[2].copy_(torch.randint(0, 3, (6, 8), generator=g, dtype=torch.uint8))
+# packed into one flat buffer, replicated by a single broadcast (bench.py)
+flat, frame = D.pack_frame(frame)
+D.broadcast_frame([flat])
+assert frame[1].dtype == torch.int16 and frame[0].shape == (6, 8, 3)
 mine = D.shard(64, ws, rank)
 total = D.sum_over_ranks(len(mine))
 slow = D.max_over_ranks(0.5 + rank)
