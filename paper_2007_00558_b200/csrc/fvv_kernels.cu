@@ -192,6 +192,53 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
 #pragma unroll
     for (int q = 0; q < 4; ++q) nh += (val[q] == FVV_INVALID);
 
+    // outputs first: K1 later rewrites the pixels it fills, so the stores
+    // need not wait for the candidate test below
+    if (row_ok) {
+        uint32_t tex[4];
+        float wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t flags;
+            if (p.color_valid) {
+                flags = (xb + q < p.W && p.color_valid[rowbase + xb + q]) ? kFlagLiveValid : 0u;
+            } else {
+                flags = (val[q] == FVV_VALID ? kFlagLiveValid : 0u) |
+                        (val[q] == FVV_BACKGROUND ? kFlagLiveBackground : 0u);
+            }
+            tex[q] = (uint32_t)g[q].x | ((uint32_t)g[q].y << 8) | ((uint32_t)g[q].z << 16) |
+                     (flags << 24);
+            wd[q] = (val[q] == FVV_VALID) ? z[q] : 0.0f;
+        }
+        if (vec) {
+            const size_t i0 = rowbase + xb;
+            if (p.texel) *reinterpret_cast<uint4 *>(p.texel + i0) = make_uint4(tex[0], tex[1], tex[2], tex[3]);
+            if (p.warp_depth) *reinterpret_cast<float4 *>(p.warp_depth + i0) = make_float4(wd[0], wd[1], wd[2], wd[3]);
+            if (p.depth_out) *reinterpret_cast<float4 *>(p.depth_out + i0) = make_float4(z[0], z[1], z[2], z[3]);
+            if (p.validity_out)
+                *reinterpret_cast<uint32_t *>(p.validity_out + i0) =
+                    (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
+                    ((uint32_t)val[3] << 24);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (xb + q >= p.W) break;
+                const size_t i = rowbase + xb + q;
+                if (p.texel) p.texel[i] = tex[q];
+                if (p.warp_depth) p.warp_depth[i] = wd[q];
+                if (p.depth_out) p.depth_out[i] = z[q];
+                if (p.validity_out) p.validity_out[i] = val[q];
+                if (p.codes_out) p.codes_out[i] = (uint16_t)code[q];
+            }
+        }
+    }
+    if (p.n_holes) {
+        const int m = __reduce_add_sync(0xffffffffu, nh);
+        if (lane == 0 && m) atomicAdd(&s_holes, m);
+        __syncthreads();
+        if (tid == 0 && s_holes) atomicAdd(p.n_holes, s_holes);
+    }
+
     if (R > 0 && __syncthreads_or(nh)) {
         // K1 candidates: Invalid pixels with >= min_valid Valid pixels in
         // their window (depthproc.py:218). Only the validity of the tile and
@@ -302,52 +349,9 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
             base += __popc(cm[q]);
         }
     }
-
-    if (row_ok) {
-        uint32_t tex[4];
-        float wd[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t flags;
-            if (p.color_valid) {
-                flags = (xb + q < p.W && p.color_valid[rowbase + xb + q]) ? kFlagLiveValid : 0u;
-            } else {
-                flags = (val[q] == FVV_VALID ? kFlagLiveValid : 0u) |
-                        (val[q] == FVV_BACKGROUND ? kFlagLiveBackground : 0u);
-            }
-            tex[q] = (uint32_t)g[q].x | ((uint32_t)g[q].y << 8) | ((uint32_t)g[q].z << 16) |
-                     (flags << 24);
-            wd[q] = (val[q] == FVV_VALID) ? z[q] : 0.0f;
-        }
-        if (vec) {
-            const size_t i0 = rowbase + xb;
-            if (p.texel) *reinterpret_cast<uint4 *>(p.texel + i0) = make_uint4(tex[0], tex[1], tex[2], tex[3]);
-            if (p.warp_depth) *reinterpret_cast<float4 *>(p.warp_depth + i0) = make_float4(wd[0], wd[1], wd[2], wd[3]);
-            if (p.depth_out) *reinterpret_cast<float4 *>(p.depth_out + i0) = make_float4(z[0], z[1], z[2], z[3]);
-            if (p.validity_out)
-                *reinterpret_cast<uint32_t *>(p.validity_out + i0) =
-                    (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
-                    ((uint32_t)val[3] << 24);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (xb + q >= p.W) break;
-                const size_t i = rowbase + xb + q;
-                if (p.texel) p.texel[i] = tex[q];
-                if (p.warp_depth) p.warp_depth[i] = wd[q];
-                if (p.depth_out) p.depth_out[i] = z[q];
-                if (p.validity_out) p.validity_out[i] = val[q];
-                if (p.codes_out) p.codes_out[i] = (uint16_t)code[q];
-            }
-        }
-    }
-    if (p.n_holes) {
-        const int m = __reduce_add_sync(0xffffffffu, nh);
-        if (lane == 0 && m) atomicAdd(&s_holes, m);
-        __syncthreads();
-        if (tid == 0 && s_holes) atomicAdd(p.n_holes, s_holes);
-    }
 }
+
+
 
 // K1 proper: the joint-bilateral fill (depthproc.py:196-222) of the
 // candidates k_preprocess listed, one thread per candidate, reading the
