@@ -65,6 +65,9 @@ struct fvv_ctx {
     CUtensorMap kmap;
     const void *kmap_base = nullptr;
     long long kmap_pitch = 0, kmap_rows = 0, kmap_n = 0, kmap_per = 0;
+    // K2 -> K3 FG tile occupancy (TileFlags), 0xFF-initialised
+    uint8_t *tflag = nullptr;
+    size_t tflag_cap = 0;
     // K1 candidate list (camera << 26 | pixel) + its length
     uint32_t *cand = nullptr;
     int *ncand = nullptr;
@@ -397,6 +400,31 @@ double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
     return 1.0 / (std::sqrt((dx * dx + dy * dy) + dz * dz) + eps);
 }
 
+// FG tile occupancy for n FG contributions of a W x H view on K3's fast
+// path (r == 1, 3 x 3 crack window): stale entries only cost K3 work
+// (flags are compared with the view's generation), so the buffer is filled
+// with 0xFF once per growth and never cleared.
+int tile_flags(fvv_ctx *ctx, int n, int W, int H, WarpParams &wp, ResolveParams &rp) {
+    TileFlags tf{};
+    tf.n_fg = n;
+    tf.tile_w = FVV_TF_W;
+    tf.tile_h = FVV_TF_H;
+    tf.ntx = (W + tf.tile_w - 1) / tf.tile_w;
+    tf.nty = (H + tf.tile_h - 1) / tf.tile_h;
+    const size_t need = (size_t)n * tf.ntx * tf.nty * kTileFlagStride;
+    if (need > ctx->tflag_cap) {
+        CK(cudaFree(ctx->tflag));
+        ctx->tflag = nullptr;
+        CK(cudaMalloc(&ctx->tflag, need));
+        CK(cudaMemsetAsync(ctx->tflag, 0xFF, need, ctx->stream));
+        ctx->tflag_cap = need;
+    }
+    tf.flag = ctx->tflag;
+    wp.tf = tf;
+    rp.tf = tf;
+    return FVV_OK;
+}
+
 // One view from n reference slots: K2 over 2n contributions, then K3.
 int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const double *weights,
                 int n, const fvv_synth_cfg &cfg, uint8_t *rgb_out, uint8_t *prov_out,
@@ -483,6 +511,9 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     if (r == 1 && resolve_uses_tma() &&
         (rc = canvas_tensor_map(ctx, ctx->cn, virt.width, virt.height, r, rp)))
         return rc;
+    if (FVV_K3_SKIP && r == 1 && cfg.crack_fill_window == 3 &&
+        (rc = tile_flags(ctx, n, virt.width, virt.height, wp, rp)))
+        return rc;
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, maxpx, ctx->stream));
     LAUNCH_K(FVV_K_RESOLVE, launch_resolve(rp, ctx->stream));
     if (ip.rgb) {
@@ -541,6 +572,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
                     (void *)ctx->rice.changed})
         cudaFree(q);
     cudaFree(ctx->cand);
+    cudaFree(ctx->tflag);
     cudaFree(ctx->ncand);
     cudaFree(ctx->iprov);
     cudaFree(ctx->idepth);

@@ -567,15 +567,30 @@ __device__ __forceinline__ double proj_rint(double f, double x, double z, double
 
 constexpr int K2_THREADS = 128, K2_PX = 4;
 
+// FG tile flags (TileFlags). Every CTA warping a view's FG region stores into
+// the same few flags, and same-sector stores serialise in L2: flags are spread
+// kTileFlagStride (8) bytes apart, one store per run of a tile per warp. At c4
+// (4K, L2-thrashing canvases) packed bytes cost K2 +35%, 8-byte spacing +15%;
+// a read-before-store (L1) or coarser 64/128-px flag tiles were slower still.
+__device__ __forceinline__ uint8_t *tile_flag(const TileFlags &tf, int k, int t) {
+    return tf.flag + ((size_t)k * tf.ntx * tf.nty + t) * kTileFlagStride;
+}
+
+__device__ __forceinline__ void mark_tile(uint8_t *f, uint8_t gen8) { *f = gen8; }
+
 __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_constant__ WarpParams p) {
     const WarpContrib &c = p.c[blockIdx.z];
     const int Ws = c.src.W, Hs = c.src.H;
     const int sv = blockIdx.y;
     const int u0 = (blockIdx.x * K2_THREADS + threadIdx.x) * K2_PX;
-    if (sv >= Hs || u0 >= Ws) return;
+    if (sv >= Hs) return;
+    // lanes past the row end stay for the warp shuffle below (no pixels)
     const size_t row = (size_t)sv * Ws;
     float d[K2_PX];
-    if ((Ws & 3) == 0) {
+    if (u0 >= Ws) {
+#pragma unroll
+        for (int q = 0; q < K2_PX; ++q) d[q] = 0.0f;
+    } else if ((Ws & 3) == 0) {
         const float4 v = __ldcs(reinterpret_cast<const float4 *>(c.depth + row + u0));
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
     } else {
@@ -586,6 +601,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
     const int Wd = p.dst.W, Hd = p.dst.H, P = p.pitch;
     const double lo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
     const double ry = __ldg(c.ry + sv);
+    const bool fgk = p.tf.flag && (int)blockIdx.z < p.tf.n_fg;
+    const uint8_t gen8 = (uint8_t)(p.gen_hi >> kGenShift);
+    int first_t = -1, last_t = -1;
     double zq[K2_PX];
     unsigned stored = 0;
 #pragma unroll
@@ -610,8 +628,29 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
         const size_t cell = (size_t)((int)vr + r) * P + (size_t)((int)ur + r);
         atomicMin((unsigned long long *)(c.canvas + cell),
                   (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
+        if (fgk) {
+            // the K3 tile of the target (padding columns/rows clamp to the edge
+            // tiles, whose neighbourhood check covers them); a plain store
+            // (no read-back on the critical path), once per tile change
+            const int tx = min(max((int)ur, 0) / p.tf.tile_w, p.tf.ntx - 1);
+            const int ty = min(max((int)vr, 0) / p.tf.tile_h, p.tf.nty - 1);
+            const int t = ty * p.tf.ntx + tx;
+            if (t != last_t) {
+                // the thread's first tile is stored after the loop, unless the
+                // previous lane's run already ended in it
+                if (first_t < 0) first_t = t;
+                else mark_tile(tile_flag(p.tf, blockIdx.z, t), gen8);
+                last_t = t;
+            }
+        }
         zq[q] = z;
         stored |= 1u << q;
+    }
+    if (fgk) {
+        // lanes hold consecutive source pixels: one store per run of a tile
+        const int prev = __shfl_up_sync(0xffffffffu, last_t, 1);
+        if (first_t >= 0 && ((threadIdx.x & 31) == 0 || first_t != prev))
+            mark_tile(tile_flag(p.tf, blockIdx.z, first_t), gen8);
     }
     // the exact z of every scattering source, so K3 reads a winner's depth
     // instead of re-deriving it: one 32-byte run per thread where all four
@@ -974,6 +1013,8 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 constexpr int FTY = FVV_K3_TY, FNT = TX * FTY;                   // fast-path tile: 32 x FTY
 constexpr int FKR = FTY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36 (FTY = 8)
 constexpr int FBR = FTY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+// a key span of TX + 4 (FTY + 4) pixels meets at most 3 flag tiles per axis
+static_assert(2 * FVV_TF_W >= TX + 3 && 2 * FVV_TF_H >= FTY + 3, "flag tiles too small");
 constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
@@ -1243,7 +1284,51 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     const size_t plane = (size_t)Wd * Hd;
     const uint64_t gen = p.gen;
     const int ntot = p.n_fg + p.n_bg;
-    const int nitems = ntot;
+    // the contributions this tile resolves, in reference order: every BG
+    // contribution, and the FG ones K2 flagged near this tile (all of them
+    // when debug rasters are requested)
+    __shared__ int8_t s_item[2 * FVV_MAX_REFS];
+    __shared__ int s_nitems;
+    if (tid < 32) {
+        bool act = false;
+        if (tid < ntot) {
+            act = DBG || !p.tf.flag || tid >= p.n_fg;
+            if (!act) {
+                // the flag tiles covering the staged key tile (target pixels
+                // x0-2 .. x0+TX+1, y0-2 .. y0+FTY+1; K2 clamps the canvas
+                // padding into the edge tiles)
+                // (at most 3 x 3 tiles, static_assert below); the nine loads are independent
+                // (clamped duplicates are harmless), so they cost one round trip
+                const int fx0 = max(x0 - 2, 0) / p.tf.tile_w;
+                const int fx1 = min((x0 + TX + 1) / p.tf.tile_w, p.tf.ntx - 1);
+                const int fy0 = max(y0 - 2, 0) / p.tf.tile_h;
+                const int fy1 = min((y0 + FTY + 1) / p.tf.tile_h, p.tf.nty - 1);
+                uint8_t f[9];
+#pragma unroll
+                for (int e = 0; e < 9; ++e) {
+                    const int tx2 = min(fx0 + e % 3, fx1), ty2 = min(fy0 + e / 3, fy1);
+                    f[e] = *tile_flag(p.tf, tid, ty2 * p.tf.ntx + tx2);
+                }
+#pragma unroll
+                for (int e = 0; e < 9; ++e) act |= f[e] == (uint8_t)gen;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, act);
+        if (act) s_item[__popc(m & ((1u << tid) - 1u))] = (int8_t)tid;
+        if (tid == 0) s_nitems = __popc(m);
+    }
+    __syncthreads();
+    const int nitems = s_nitems;
+    if (nitems == 0) {
+        // no BG contribution and no FG key near the tile: all holes
+        if (inimg) {
+            if (p.rgb_out)
+                for (int ch = 0; ch < 3; ++ch) p.rgb_out[pix * 3 + ch] = (uint8_t)rgb_u8(p.hole[ch]);
+            if (p.prov_out) p.prov_out[pix] = 0;
+            if (p.depth_out) p.depth_out[pix] = 0.0f;
+        }
+        return;
+    }
     // virtual-camera rays of the tile's columns and rows (pixel_rays,
     // core.py:224-227), once per CTA
     if (tid < TX) sray[tid] = ddiv(dsub((double)(x0 + tid), dst.cx), dst.fx);
@@ -1263,7 +1348,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         if (tid == 0 && q < nitems) {
             uint64_t *bar = &s_bar[q % NBUF];
             mbar_expect_tx(bar, FKEYS * sizeof(uint64_t));
-            tma_load_3d(sk + (q % NBUF) * FKEYS, &p.kmap, x0, y0 - 1, q, bar);
+            tma_load_3d(sk + (q % NBUF) * FKEYS, &p.kmap, x0, y0 - 1, s_item[q], bar);
         }
     };
     auto wait_keys = [&](int q) {
@@ -1274,7 +1359,8 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     wait_keys(0);
 #else
     auto stage = [&](int q) {
-        if (q < nitems) stage_keys(sk + (q % NBUF) * FKEYS, p.c[q].canvas, x0, y0, P, Hc, tid);
+        if (q < nitems)
+            stage_keys(sk + (q % NBUF) * FKEYS, p.c[s_item[q]].canvas, x0, y0, P, Hc, tid);
         cp_async_commit();  // (possibly empty) group per item keeps the accounting uniform
     };
 
@@ -1283,7 +1369,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     cp_async_wait<NBUF - 1>();
     __syncthreads();
 #endif
-    int any_next = resolve_cells<DBG>(p.c[0], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
+    int any_next = resolve_cells<DBG>(p.c[s_item[0]], Wd, Hd, sk, swk, sst, gen, x0, y0, tid);
 
     bool fv = false, bv = false;
     uint32_t fgc = 0, bgc = 0;   // rounded merged layer colours (R | G << 8 | B << 16)
@@ -1291,7 +1377,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     uint32_t vmask = 0;
 #pragma unroll 1
     for (int q = 0; q < nitems; ++q) {
-        const int k = q;
+        const int k = s_item[q];
         const bool fgl = k < p.n_fg;
         const int j = fgl ? k : k - p.n_fg;
         // keys of q+1 must have landed (groups q+1 done, q+2 may pend); cells of q
@@ -1312,7 +1398,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         // cells of q+1 (other warps' per-pixel work of q overlaps it)
         any_next = 0;
         if (q + 1 < nitems)
-            any_next = resolve_cells<DBG>(p.c[q + 1], Wd, Hd, sk + ((q + 1) % NBUF) * FKEYS,
+            any_next = resolve_cells<DBG>(p.c[s_item[q + 1]], Wd, Hd, sk + ((q + 1) % NBUF) * FKEYS,
                                           swk + ((q + 1) & 1) * FCELLS,
                                           sst + ((q + 1) & 1) * FCELLS, gen, x0, y0, tid);
         const ResolveContrib &c = p.c[k];
@@ -1367,7 +1453,8 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             if (p.dbg.contrib_stage) p.dbg.contrib_stage[o] = st;
         }
         // -- end of a layer: mix_layer (synthesis.py:261-292)
-        const bool last = fgl ? (k == p.n_fg - 1) : (k == ntot - 1);
+        // the last resolved contribution of its layer
+        const bool last = q + 1 == nitems || (fgl && s_item[q + 1] >= p.n_fg);
         if (last) {
             const int n = j + 1;
             const int kb = k - j;
@@ -1425,7 +1512,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             }
         }
         // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
-        if (k == ntot - 1 && inimg) {
+        if (q + 1 == nitems && inimg) {
             const uint32_t hole = rgb_u8(p.hole[0]) | (rgb_u8(p.hole[1]) << 8) |
                                   (rgb_u8(p.hole[2]) << 16);
             const uint32_t oc = fv ? fgc : (bv ? bgc : hole);
@@ -1483,6 +1570,7 @@ static void launch_fast_r(const ResolveParams &p, bool dbg, dim3 grid, cudaStrea
 
 
 bool resolve_uses_tma() { return FVV_K3_TMA != 0; }
+int resolve_tile_rows() { return FTY; }
 
 cudaError_t launch_resolve(const ResolveParams &p, cudaStream_t s) {
     dim3 grid((p.dst.W + TX - 1) / TX, (p.dst.H + TY - 1) / TY);

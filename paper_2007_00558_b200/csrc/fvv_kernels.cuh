@@ -78,12 +78,36 @@ struct WarpContrib {
 // ptr[cy * pitch + cx], where ptr = allocation + 1 + k * per and pitch is even
 // and >= Wd+2r+1, so that tile rows starting at image column x0 (a multiple
 // of 32) are 16-byte aligned for cp.async staging.
+// FG tile occupancy: for contributions k < n_fg, K2 stores the view's
+// generation into tflag[k * ntx * nty + tile] of every K3 tile (tile_w x
+// tile_h target pixels) a source lands in; K3 skips an FG contribution for
+// a tile none of whose 3 x 3 neighbour tiles is flagged (its key tile,
+// halo included, holds no key of this view). Null: no flags.
+#ifndef FVV_TF_STRIDE
+#define FVV_TF_STRIDE 8
+#endif
+constexpr int kTileFlagStride = FVV_TF_STRIDE;  // bytes per flag
+#ifndef FVV_TF_W
+#define FVV_TF_W 32   // flag tile width (target pixels)
+#endif
+#ifndef FVV_TF_H
+#define FVV_TF_H 8    // flag tile height
+#endif
+#ifndef FVV_K3_SKIP
+#define FVV_K3_SKIP 1
+#endif
+struct TileFlags {
+    uint8_t *flag;
+    int n_fg, ntx, nty, tile_w, tile_h;
+};
+
 struct WarpParams {
     DevCam dst;
     int r;
     int pitch;
     int n;
     uint64_t gen_hi;         // generation code << 57
+    TileFlags tf;
     WarpContrib c[2 * FVV_MAX_REFS];
 };
 
@@ -109,6 +133,7 @@ struct ResolveParams {
     int r, window, need;
     int pitch;
     uint64_t gen;            // generation code (0..127)
+    TileFlags tf;            // FG tile occupancy written by K2 (fast path, non-debug)
     int n_fg, n_bg;
     double band_rel;
     double hole[3];
@@ -163,5 +188,6 @@ cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s);
 int take_extra_launches();  // kernels beyond one issued by the last launcher call
 cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
 size_t resolve_smem_bytes(int maxr);
+int resolve_tile_rows();  // K3 fast-path tile height (the tile width is 32)
 
 }  // namespace fvv

@@ -358,3 +358,31 @@ def test_full_4k_edge_server_path_vs_c_oracle(cuda):
     img = r.render([v], [refs])[0].cpu().numpy()
     o_rgb, _ = CO.es_view(v, frames)
     np.testing.assert_array_equal(img, o_rgb)
+
+
+@pytest.mark.parametrize("name", ["syn_c1_s8.npz", "syn_c2_s8_v3.npz"])
+@pytest.mark.parametrize("density", [0.005, 0.05])
+def test_sparse_foreground_tile_skip_bit_exact(cuda, name, density):
+    """K3 skips an FG contribution on tiles whose key span K2 did not flag
+    (TileFlags): isolated FG specks put keys in tile halos and corners, where
+    a missed flag would drop a splat or a crack median. The skip path (plain
+    render) must equal the oracle and the all-contributions debug render."""
+    from paper_2007_00558_b200 import synthesis as S
+
+    _, case = _case(name)
+    rng = np.random.default_rng(7)
+    for a in case.arrays:
+        fg = a["live_validity"] == 1
+        keep = rng.random(fg.shape) < density
+        keep |= np.roll(keep, 1, 0) | np.roll(keep, 1, 1)   # 2x2 specks
+        a["live_validity"] = np.where(fg & ~keep, 0, a["live_validity"]).astype(
+            a["live_validity"].dtype)
+    frame, prov = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig(),
+                                    return_provenance=True)
+    o_rgb, o_prov, _ = O.synthesize_view(case.virtual, case.oracle_refs(), debug=True)
+    np.testing.assert_array_equal(frame.pixels, o_rgb)
+    np.testing.assert_array_equal(prov, o_prov)
+    dframe, _ = S.synthesize_view_debug(case.virtual, case.inputs(), case.refs,
+                                        S.SynthesisConfig())
+    np.testing.assert_array_equal(frame.pixels, dframe.pixels)
+    assert (o_prov == 2).any(), "no foreground survived: the case tests nothing"
