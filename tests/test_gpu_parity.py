@@ -372,11 +372,10 @@ def test_sparse_foreground_tile_skip_bit_exact(cuda, name, density):
     _, case = _case(name)
     rng = np.random.default_rng(7)
     for a in case.arrays:
-        fg = a["live_validity"] == 1
+        fg = a["live_validity"] == 0                          # Validity.VALID
         keep = rng.random(fg.shape) < density
         keep |= np.roll(keep, 1, 0) | np.roll(keep, 1, 1)   # 2x2 specks
-        a["live_validity"] = np.where(fg & ~keep, 0, a["live_validity"]).astype(
-            a["live_validity"].dtype)
+        a["live_validity"] = np.where(fg & ~keep, 1, a["live_validity"]).astype(np.uint8)
     frame, prov = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig(),
                                     return_provenance=True)
     o_rgb, o_prov, _ = O.synthesize_view(case.virtual, case.oracle_refs(), debug=True)
@@ -386,3 +385,50 @@ def test_sparse_foreground_tile_skip_bit_exact(cuda, name, density):
                                         S.SynthesisConfig())
     np.testing.assert_array_equal(frame.pixels, dframe.pixels)
     assert (o_prov == 2).any(), "no foreground survived: the case tests nothing"
+
+
+def test_foreground_keys_only_in_neighbour_tiles(cuda):
+    """Crafted identity view (target pixel == source pixel): FG keys lie only
+    in the tiles left of / above / diagonal to a 32x8 K3 tile, in the L shape
+    that makes the tile's corner pixel a 5-of-8 FG splat, plus lone halo-2
+    keys. The tile must still resolve that contribution (its flag check
+    covers the whole staged key span x0-2 .. x0+33, y0-2 .. y0+9).
+    The composite cannot show such a splat (its fetch needs valid source
+    pixels, which would put keys in the tile), so this checks the rasters
+    against the oracle and that the splat winners exist."""
+    from _helpers import Case
+    from paper_2007_00558_b200 import synthesis as S
+    from paper_2007_00558_b200.types import CameraCalibration, CameraIntrinsics, CameraPose
+
+    W, H = 128, 40
+    cam = CameraCalibration(1, CameraIntrinsics(100.0, 100.0, 63.0, 19.0, W, H),
+                            CameraPose(np.eye(3), np.zeros(3)))
+    rng = np.random.default_rng(3)
+    rgb = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+    live_v = np.ones((H, W), np.uint8)                 # INVALID
+    live_d = np.zeros((H, W), np.float32)
+    for x0 in (32, 64, 96):
+        for y0 in (8, 16, 24, 32):
+            # ring of (x0, y0) outside its tile: (x0-1, y0-1..y0+1), (x0, y0-1), (x0+1, y0-1)
+            for (x, y) in ((x0 - 1, y0 - 1), (x0, y0 - 1), (x0 + 1, y0 - 1),
+                           (x0 - 1, y0), (x0 - 1, y0 + 1)):
+                live_v[y, x] = 0
+                live_d[y, x] = 2.0 + 0.01 * (x % 7)
+    live_v[4, 61] = 0            # halo-2 keys of the tiles to the right / below
+    live_d[4, 61] = 3.0
+    live_v[14, 90] = 0
+    live_d[14, 90] = 3.0
+    bg_v = np.ones((H, W), np.uint8)
+    bg_d = np.zeros((H, W), np.float32)
+    case = Case(cam, [1], [dict(calib=cam, rgb=rgb, live_depth=live_d, live_validity=live_v,
+                                bg_depth=bg_d, bg_validity=bg_v)])
+    frame, prov = S.synthesize_view(cam, case.inputs(), [1], S.SynthesisConfig(),
+                                    return_provenance=True)
+    o_rgb, o_prov, _ = O.synthesize_view(cam, case.oracle_refs(), debug=True)
+    np.testing.assert_array_equal(prov, o_prov)
+    np.testing.assert_array_equal(frame.pixels, o_rgb)
+    # the corner cells do take an FG splat winner (debug rasters: every
+    # contribution resolved); their backward fetch lands on Invalid source
+    # pixels, so the composite leaves them holes, like the oracle
+    _, b = S.synthesize_view_debug(cam, case.inputs(), [1], S.SynthesisConfig())
+    assert (b.fg_contributions[0].winner[8::8, 32::32] >= 0).all()
