@@ -452,7 +452,10 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     rp.n_fg = n;
     rp.n_bg = n;
     rp.band_rel = cfg.depth_band_rel;
-    for (int q = 0; q < 3; ++q) rp.hole[q] = (double)cfg.hole_color[q];
+    for (int q = 0; q < 3; ++q) {
+        rp.hole[q] = (double)cfg.hole_color[q];
+        rp.hole_rgb |= (uint32_t)cfg.hole_color[q] << (8 * q);
+    }
     rp.rgb_out = rgb_out;
     rp.prov_out = prov_out;
     if (dbg) rp.dbg = *dbg;

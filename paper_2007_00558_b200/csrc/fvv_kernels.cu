@@ -1081,8 +1081,16 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // composite's per-channel conversion: np.clip(np.round(v), 0, 255) -> uint8
 // (half-even rint, synthesis.py:312)
+// One F2I: cvt.rni rounds half to even like rint, .sat clamps to 0..255
+// and NaN converts to 0 (what fmin(fmax(rint(NaN), 0), 255) gives).
 __device__ __forceinline__ uint32_t rgb_u8(double v) {
+#if FVV_RGB_CVT
+    unsigned short r;
+    asm("cvt.rni.sat.u8.f64 %0, %1;" : "=h"(r) : "d"(v));
+    return r;
+#else
     return (uint32_t)fmin(fmax(rint(v), 0.0), 255.0);
+#endif
 }
 
 // exact f64 z of a winner index: the value K2 computed and stored for it
@@ -1323,7 +1331,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         // no BG contribution and no FG key near the tile: all holes
         if (inimg) {
             if (p.rgb_out)
-                for (int ch = 0; ch < 3; ++ch) p.rgb_out[pix * 3 + ch] = (uint8_t)rgb_u8(p.hole[ch]);
+                for (int ch = 0; ch < 3; ++ch) p.rgb_out[pix * 3 + ch] = (uint8_t)(p.hole_rgb >> (8 * ch));
             if (p.prov_out) p.prov_out[pix] = 0;
             if (p.depth_out) p.depth_out[pix] = 0.0f;
         }
@@ -1513,9 +1521,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         }
         // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
         if (q + 1 == nitems && inimg) {
-            const uint32_t hole = rgb_u8(p.hole[0]) | (rgb_u8(p.hole[1]) << 8) |
-                                  (rgb_u8(p.hole[2]) << 16);
-            const uint32_t oc = fv ? fgc : (bv ? bgc : hole);
+            const uint32_t oc = fv ? fgc : (bv ? bgc : p.hole_rgb);
             if (p.rgb_out) {
                 uint8_t *o = p.rgb_out + pix * 3;
                 o[0] = (uint8_t)oc;

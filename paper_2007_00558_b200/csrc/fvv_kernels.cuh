@@ -83,6 +83,9 @@ struct WarpContrib {
 // tile_h target pixels) a source lands in; K3 skips an FG contribution for
 // a tile none of whose 3 x 3 neighbour tiles is flagged (its key tile,
 // halo included, holds no key of this view). Null: no flags.
+#ifndef FVV_RGB_CVT
+#define FVV_RGB_CVT 1
+#endif
 #ifndef FVV_TF_STRIDE
 #define FVV_TF_STRIDE 8
 #endif
@@ -137,6 +140,7 @@ struct ResolveParams {
     int n_fg, n_bg;
     double band_rel;
     double hole[3];
+    uint32_t hole_rgb;       // hole[] as composite's u8 R | G << 8 | B << 16
     uint8_t *rgb_out;        // H*W*3 (may be null)
     uint8_t *prov_out;       // H*W (may be null)
     // extensions outside the reference (off in parity mode, fvv_synth_cfg):
