@@ -1297,6 +1297,23 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     // when debug rasters are requested)
     __shared__ int8_t s_item[2 * FVV_MAX_REFS];
     __shared__ int s_nitems;
+#if FVV_K3_TMA
+    // key tiles by TMA: thread 0 arms buffer q % NBUF's mbarrier and issues
+    // the box; canvas column x0-1 .. x0+34 is tensor x = x0 .. x0+35 (the
+    // allocation's +1 offset), out-of-canvas boxes are zero-filled (they only
+    // feed out-of-image cells, which are never resolved)
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(&s_bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    auto stage = [&](int q, int n) {
+        if (tid == 0 && q < n) {
+            uint64_t *bar = &s_bar[q % NBUF];
+            mbar_expect_tx(bar, FKEYS * sizeof(uint64_t));
+            tma_load_3d(sk + (q % NBUF) * FKEYS, &p.kmap, x0, y0 - 1, s_item[q], bar);
+        }
+    };
+#endif
     if (tid < 32) {
         bool act = false;
         if (tid < ntot) {
@@ -1304,9 +1321,9 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             if (!act) {
                 // the flag tiles covering the staged key tile (target pixels
                 // x0-2 .. x0+TX+1, y0-2 .. y0+FTY+1; K2 clamps the canvas
-                // padding into the edge tiles)
-                // (at most 3 x 3 tiles, static_assert below); the nine loads are independent
-                // (clamped duplicates are harmless), so they cost one round trip
+                // padding into the edge tiles): at most 3 x 3 (static_assert
+                // above); the nine loads are independent (clamped duplicates
+                // are harmless), so they cost one round trip
                 const int fx0 = max(x0 - 2, 0) / p.tf.tile_w;
                 const int fx1 = min((x0 + TX + 1) / p.tf.tile_w, p.tf.ntx - 1);
                 const int fy0 = max(y0 - 2, 0) / p.tf.tile_h;
@@ -1324,6 +1341,18 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         const unsigned m = __ballot_sync(0xffffffffu, act);
         if (act) s_item[__popc(m & ((1u << tid) - 1u))] = (int8_t)tid;
         if (tid == 0) s_nitems = __popc(m);
+#if FVV_K3_TMA
+        // the first key tiles go out before the CTA barrier
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NBUF; ++q) stage(q, __popc(m));
+#endif
+    } else if (tid < 32 + TX + FTY) {
+        // virtual-camera rays of the tile's columns and rows (pixel_rays,
+        // core.py:224-227), once per CTA, while warp 0 picks the contributions
+        const int t = tid - 32;
+        if (t < TX) sray[t] = ddiv(dsub((double)(x0 + t), dst.cx), dst.fx);
+        else sray[t] = ddiv(dsub((double)(y0 + t - TX), dst.cy), dst.fy);
     }
     __syncthreads();
     const int nitems = s_nitems;
@@ -1337,33 +1366,10 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         }
         return;
     }
-    // virtual-camera rays of the tile's columns and rows (pixel_rays,
-    // core.py:224-227), once per CTA
-    if (tid < TX) sray[tid] = ddiv(dsub((double)(x0 + tid), dst.cx), dst.fx);
-    else if (tid < TX + FTY) sray[tid] = ddiv(dsub((double)(y0 + tid - TX), dst.cy), dst.fy);
-
 #if FVV_K3_TMA
-    // key tiles by TMA: thread 0 arms buffer q % NBUF's mbarrier and issues
-    // the box; canvas column x0-1 .. x0+34 is tensor x = x0 .. x0+35 (the
-    // allocation's +1 offset), out-of-canvas boxes are zero-filled (they only
-    // feed out-of-image cells, which are never resolved)
-    if (tid == 0) {
-        for (int b = 0; b < NBUF; ++b) mbar_init(&s_bar[b], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    auto stage = [&](int q) {
-        if (tid == 0 && q < nitems) {
-            uint64_t *bar = &s_bar[q % NBUF];
-            mbar_expect_tx(bar, FKEYS * sizeof(uint64_t));
-            tma_load_3d(sk + (q % NBUF) * FKEYS, &p.kmap, x0, y0 - 1, s_item[q], bar);
-        }
-    };
     auto wait_keys = [&](int q) {
         if (q < nitems) mbar_wait(&s_bar[q % NBUF], (unsigned)((q / NBUF) & 1));
     };
-#pragma unroll
-    for (int q = 0; q < NBUF; ++q) stage(q);
     wait_keys(0);
 #else
     auto stage = [&](int q) {
@@ -1396,7 +1402,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         // keys of q+NBUF into the buffer item q's cells phase used (all reads of
         // it by the generic proxy are ordered before the barrier above)
         if (tid == 0) fence_proxy_async();
-        stage(q + NBUF);
+        stage(q + NBUF, nitems);
 #else
         cp_async_wait<NBUF - 2>();
         const int any = __syncthreads_or(any_next);
