@@ -1168,8 +1168,10 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
     return any;
 }
 
-// crack median of a hole pixel from its 8 neighbours' winner keys (rare path,
-// kept out of line so the unrolled kernel stays small)
+// crack median of a hole pixel from its 8 neighbours' winner keys. About 8 %
+// of (pixel, contribution) pairs at c1, ~2.5 lanes per warp that enters it;
+// a CTA crack queue (one warp resolving all of an item's cracks after an
+// extra barrier, layer mixes deferred) was 16 % slower.
 #ifndef FVV_K3_CRACK_NOINLINE
 #define FVV_K3_CRACK_NOINLINE 0
 #endif
@@ -1389,6 +1391,62 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     uint32_t fgc = 0, bgc = 0;   // rounded merged layer colours (R | G << 8 | B << 16)
     float fgz = 0.0f, bgz = 0.0f;
     uint32_t vmask = 0;
+    // -- end of a layer: mix_layer (synthesis.py:261-292) over the layer's
+    // valid contributions (kb = its first contribution index)
+    auto mix = [&](bool fgl, int kb) {
+        // valid contributions only, in ascending (reference) order
+        double zmin = INFINITY;
+        for (unsigned m = vmask; m; m &= m - 1) {
+            const int qq = __ffs(m) - 1;
+            const double zj = sres[(qq * 4 + 3) * FNT + tid];
+            if (zj < zmin) zmin = zj;
+        }
+        const double thr = dadd(zmin, dmul(p.band_rel, zmin));
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
+        for (unsigned m = vmask; m; m &= m - 1) {
+            const int qq = __ffs(m) - 1;
+            const double zj = sres[(qq * 4 + 3) * FNT + tid];
+            if (zj <= thr) {
+                const double w = ANG ? swt[qq * FNT + tid] : p.c[kb + qq].weight;
+                a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * FNT + tid]));
+                a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * FNT + tid]));
+                a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * FNT + tid]));
+                if (DBG || p.depth_out) ad = dadd(ad, dmul(w, zj));
+                aw = dadd(aw, w);
+            }
+        }
+        const bool mv = aw > 0.0;
+        double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+        if (mv) {
+            const double ra = rcp_nr(aw);
+            m0 = div_rcp(a0, aw, ra);
+            m1 = div_rcp(a1, aw, ra);
+            m2 = div_rcp(a2, aw, ra);
+        }
+        const float mz = (p.depth_out && mv) ? (float)ddiv(ad, aw) : 0.0f;
+        if (fgl) {
+            // composite needs only the FG layer's rounded colour (it wins
+            // wherever valid, synthesis.py:309-312): one packed register
+            fv = mv;
+            fgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
+            fgz = mz;
+        } else {
+            bv = mv;
+            bgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
+            bgz = mz;
+        }
+        vmask = 0;
+        if (DBG && inimg) {
+            const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
+            if (p.dbg.merged_color) {
+                p.dbg.merged_color[o * 3 + 0] = m0;
+                p.dbg.merged_color[o * 3 + 1] = m1;
+                p.dbg.merged_color[o * 3 + 2] = m2;
+            }
+            if (p.dbg.merged_depth) p.dbg.merged_depth[o] = mv ? ddiv(ad, aw) : 0.0;
+            if (p.dbg.merged_valid) p.dbg.merged_valid[o] = mv ? 1 : 0;
+        }
+    };
 #pragma unroll 1
     for (int q = 0; q < nitems; ++q) {
         const int k = s_item[q];
@@ -1434,7 +1492,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
                 z = winner_z(c, dst, idx);
                 win = (int)idx;
             } else {
-                // crack median (synthesis.py:90-125), rare: out of line
+                // crack median (synthesis.py:90-125)
                 int stc = st;
                 z = crack_z(c, dst, W, bi, &stc);
                 st = (uint8_t)stc;
@@ -1466,77 +1524,21 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             if (p.dbg.contrib_winner) p.dbg.contrib_winner[o] = win;
             if (p.dbg.contrib_stage) p.dbg.contrib_stage[o] = st;
         }
-        // -- end of a layer: mix_layer (synthesis.py:261-292)
-        // the last resolved contribution of its layer
+        // the last resolved contribution of its layer ends it
         const bool last = q + 1 == nitems || (fgl && s_item[q + 1] >= p.n_fg);
-        if (last) {
-            const int n = j + 1;
-            const int kb = k - j;
-            // valid contributions only, in ascending (reference) order
-            double zmin = INFINITY;
-            for (unsigned m = vmask; m; m &= m - 1) {
-                const int qq = __ffs(m) - 1;
-                const double zj = sres[(qq * 4 + 3) * FNT + tid];
-                if (zj < zmin) zmin = zj;
-            }
-            const double thr = dadd(zmin, dmul(p.band_rel, zmin));
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
-            for (unsigned m = vmask; m; m &= m - 1) {
-                const int qq = __ffs(m) - 1;
-                const double zj = sres[(qq * 4 + 3) * FNT + tid];
-                if (zj <= thr) {
-                    const double w = ANG ? swt[qq * FNT + tid] : p.c[kb + qq].weight;
-                    a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * FNT + tid]));
-                    a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * FNT + tid]));
-                    a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * FNT + tid]));
-                    if (DBG || p.depth_out) ad = dadd(ad, dmul(w, zj));
-                    aw = dadd(aw, w);
-                }
-            }
-            const bool mv = aw > 0.0;
-            double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-            if (mv) {
-                const double ra = rcp_nr(aw);
-                m0 = div_rcp(a0, aw, ra);
-                m1 = div_rcp(a1, aw, ra);
-                m2 = div_rcp(a2, aw, ra);
-            }
-            const float mz = (p.depth_out && mv) ? (float)ddiv(ad, aw) : 0.0f;
-            if (fgl) {
-                // composite needs only the FG layer's rounded colour (it wins
-                // wherever valid, synthesis.py:309-312): one packed register
-                fv = mv;
-                fgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
-                fgz = mz;
-            } else {
-                bv = mv;
-                bgc = rgb_u8(m0) | (rgb_u8(m1) << 8) | (rgb_u8(m2) << 16);
-                bgz = mz;
-            }
-            vmask = 0;
-            if (DBG && inimg) {
-                const size_t o = (size_t)(fgl ? 0 : 1) * plane + pix;
-                if (p.dbg.merged_color) {
-                    p.dbg.merged_color[o * 3 + 0] = m0;
-                    p.dbg.merged_color[o * 3 + 1] = m1;
-                    p.dbg.merged_color[o * 3 + 2] = m2;
-                }
-                if (p.dbg.merged_depth) p.dbg.merged_depth[o] = mv ? ddiv(ad, aw) : 0.0;
-                if (p.dbg.merged_valid) p.dbg.merged_valid[o] = mv ? 1 : 0;
-            }
+        if (last) mix(fgl, k - j);
+    }
+    // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
+    if (inimg) {
+        const uint32_t oc = fv ? fgc : (bv ? bgc : p.hole_rgb);
+        if (p.rgb_out) {
+            uint8_t *o = p.rgb_out + pix * 3;
+            o[0] = (uint8_t)oc;
+            o[1] = (uint8_t)(oc >> 8);
+            o[2] = (uint8_t)(oc >> 16);
         }
-        // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
-        if (q + 1 == nitems && inimg) {
-            const uint32_t oc = fv ? fgc : (bv ? bgc : p.hole_rgb);
-            if (p.rgb_out) {
-                uint8_t *o = p.rgb_out + pix * 3;
-                o[0] = (uint8_t)oc;
-                o[1] = (uint8_t)(oc >> 8);
-                o[2] = (uint8_t)(oc >> 16);
-            }
-            if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
-            if (p.depth_out) p.depth_out[pix] = fv ? fgz : (bv ? bgz : 0.0f);
-        }
+        if (p.prov_out) p.prov_out[pix] = fv ? 2 : (bv ? 1 : 0);
+        if (p.depth_out) p.depth_out[pix] = fv ? fgz : (bv ? bgz : 0.0f);
     }
 #if !FVV_K3_TMA
     cp_async_wait<0>();
