@@ -407,10 +407,8 @@ double host_weight(const fvv_camera &a, const fvv_camera &b, double eps) {
 int tile_flags(fvv_ctx *ctx, int n, int W, int H, WarpParams &wp, ResolveParams &rp) {
     TileFlags tf{};
     tf.n_fg = n;
-    tf.tile_w = FVV_TF_W;
-    tf.tile_h = FVV_TF_H;
-    tf.ntx = (W + tf.tile_w - 1) / tf.tile_w;
-    tf.nty = (H + tf.tile_h - 1) / tf.tile_h;
+    tf.ntx = (W + kTileFlagW - 1) / kTileFlagW;
+    tf.nty = (H + kTileFlagH - 1) / kTileFlagH;
     const size_t need = (size_t)n * tf.ntx * tf.nty * kTileFlagStride;
     if (need > ctx->tflag_cap) {
         CK(cudaFree(ctx->tflag));

@@ -632,8 +632,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_consta
             // the K3 tile of the target (padding columns/rows clamp to the edge
             // tiles, whose neighbourhood check covers them); a plain store
             // (no read-back on the critical path), once per tile change
-            const int tx = min(max((int)ur, 0) / p.tf.tile_w, p.tf.ntx - 1);
-            const int ty = min(max((int)vr, 0) / p.tf.tile_h, p.tf.nty - 1);
+            const int tx = min(max((int)ur, 0) / kTileFlagW, p.tf.ntx - 1);
+            const int ty = min(max((int)vr, 0) / kTileFlagH, p.tf.nty - 1);
             const int t = ty * p.tf.ntx + tx;
             if (t != last_t) {
                 // the thread's first tile is stored after the loop, unless the
@@ -1326,10 +1326,10 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
                 // padding into the edge tiles): at most 3 x 3 (static_assert
                 // above); the nine loads are independent (clamped duplicates
                 // are harmless), so they cost one round trip
-                const int fx0 = max(x0 - 2, 0) / p.tf.tile_w;
-                const int fx1 = min((x0 + TX + 1) / p.tf.tile_w, p.tf.ntx - 1);
-                const int fy0 = max(y0 - 2, 0) / p.tf.tile_h;
-                const int fy1 = min((y0 + FTY + 1) / p.tf.tile_h, p.tf.nty - 1);
+                const int fx0 = max(x0 - 2, 0) / kTileFlagW;
+                const int fx1 = min((x0 + TX + 1) / kTileFlagW, p.tf.ntx - 1);
+                const int fy0 = max(y0 - 2, 0) / kTileFlagH;
+                const int fy1 = min((y0 + FTY + 1) / kTileFlagH, p.tf.nty - 1);
                 uint8_t f[9];
 #pragma unroll
                 for (int e = 0; e < 9; ++e) {

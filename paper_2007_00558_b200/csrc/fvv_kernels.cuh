@@ -79,8 +79,8 @@ struct WarpContrib {
 // and >= Wd+2r+1, so that tile rows starting at image column x0 (a multiple
 // of 32) are 16-byte aligned for cp.async staging.
 // FG tile occupancy: for contributions k < n_fg, K2 stores the view's
-// generation into tflag[k * ntx * nty + tile] of every K3 tile (tile_w x
-// tile_h target pixels) a source lands in; K3 skips an FG contribution for
+// generation into tflag[k * ntx * nty + tile] of every flag tile (kTileFlagW x
+// kTileFlagH target pixels) a source lands in; K3 skips an FG contribution for
 // a tile none of whose 3 x 3 neighbour tiles is flagged (its key tile,
 // halo included, holds no key of this view). Null: no flags.
 #ifndef FVV_RGB_CVT
@@ -96,12 +96,13 @@ constexpr int kTileFlagStride = FVV_TF_STRIDE;  // bytes per flag
 #ifndef FVV_TF_H
 #define FVV_TF_H 8    // flag tile height
 #endif
+constexpr int kTileFlagW = FVV_TF_W, kTileFlagH = FVV_TF_H;
 #ifndef FVV_K3_SKIP
 #define FVV_K3_SKIP 1
 #endif
 struct TileFlags {
     uint8_t *flag;
-    int n_fg, ntx, nty, tile_w, tile_h;
+    int n_fg, ntx, nty;      // flag tiles are kTileFlagW x kTileFlagH target pixels
 };
 
 struct WarpParams {
