@@ -568,9 +568,12 @@ def run_ours(args):
     dom = max(kern, key=lambda n: prof[n][0])
     dom_bytes = per_kernel.get(dom)
     # ncu DRAM bytes per launch of the same kernel, from the committed capture
+    # (tools/round_bench.sh: the default c1 step, reference mixing), so only
+    # for that configuration
+    captured = args.config == "c1" and not args.extensions
     traffic = None
     tfile = ROOT / "profiles" / "r01_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and captured:
         kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
               "resolve": "k_resolve_fast"}.get(dom)
         traffic = json.loads(tfile.read_text()).get(kn)
@@ -585,7 +588,7 @@ def run_ours(args):
     # peak of 4 warp instructions per clock per SM (one per sub-partition)
     issue = None
     ifile = ROOT / "profiles" / "r01_inst.json"
-    if ifile.exists() and dom_bytes:
+    if ifile.exists() and dom_bytes and captured:
         kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
               "resolve": "k_resolve_fast"}.get(dom)
         inst = json.loads(ifile.read_text()).get(kn)
