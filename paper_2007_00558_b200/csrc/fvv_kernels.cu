@@ -60,7 +60,11 @@ cudaError_t launch_rays(const DevCam &c, double *rx, double *ry, cudaStream_t s)
 #ifndef FVV_PRE_MINB
 #define FVV_PRE_MINB 4
 #endif
-constexpr int PX = 128, PY = 8, PMAXR = 4;  // tile: 8 rows x 128 px, 4 px per thread
+#ifndef FVV_PRE_ROWS
+#define FVV_PRE_ROWS 2
+#endif
+// tile: PY rows x 128 px; a thread owns 4 px of PROWS rows
+constexpr int PROWS = FVV_PRE_ROWS, PX = 128, PY = 8 * PROWS, PMAXR = 4;
 constexpr int PSC = PX + 2 * PMAXR, PSR = PY + 2 * PMAXR;
 
 // 12-bit code at (iy, ix) from the folded/interleaved YUV420 raster
@@ -131,70 +135,93 @@ __device__ __forceinline__ uchar4 load_rgb(const PreprocCore &p, size_t i) {
     return make_uchar4(c[0], c[1], c[2], 0);
 }
 
-// K0 + K1 + ingest. Each thread owns 4 consecutive pixels of one row; a warp
-// owns a 128-px row segment (coalesced 8/4/12-byte loads, 16-byte stores).
-// The 5x5 joint-bilateral fill (depthproc.py:171-224) only runs when the
-// tile holds an Invalid pixel: then the 2-px halo is staged in shared memory
-// (zero-padded like scenegen._shift2d: outside pixels are never Valid).
+// K0 + K1 + ingest. Each thread owns 4 consecutive pixels of PROWS rows
+// (8 apart); a warp owns 128-px row segments (coalesced 8/4/12-byte loads,
+// 16-byte stores), all rows' loads issued before any is used so twice the
+// bytes are in flight per thread (the kernel streams from HBM and is bound by
+// memory-level parallelism). The 5x5 joint-bilateral fill
+// (depthproc.py:171-224) only runs when the tile holds an Invalid pixel: then
+// the 2-px halo is staged in shared memory (zero-padded like
+// scenegen._shift2d: outside pixels are never Valid).
 __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_constant__ PreprocBatch batch) {
     const PreprocCore &p = batch.cam[blockIdx.z];
     const BilateralParams &bl = batch.bil;
     __shared__ __align__(8) uint8_t sv[PSR * PSC + 8];
     __shared__ int s_holes, s_base;
-    __shared__ int s_wcnt[PY];
+    __shared__ int s_wcnt[8];
 
     const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
     if (x0 >= p.W || y0 >= p.H) return;  // batch grids cover the largest camera
-    const int iy = y0 + ty, xb = x0 + lane * 4;
+    const int xb = x0 + lane * 4;
     const int R = bl.radius;
     const int SC = PX + 2 * R;
     if (tid == 0) s_holes = 0;
 
-    float z[4];
-    uint8_t val[4];
-    uchar4 g[4];
-    uint32_t code[4] = {0, 0, 0, 0};
-    const bool row_ok = iy < p.H;
-    const size_t rowbase = (size_t)iy * p.W;
-    const bool vec = row_ok && xb + 3 < p.W && (p.W & 3) == 0 && p.src == kSrcMM && p.rgb &&
-                     p.validity;
-    if (vec) {
-        // 16-B aligned vector path (W % 4 == 0; torch/cudaMalloc bases are 256-B aligned)
-        const size_t i0 = rowbase + xb;
-        const uint2 m = __ldcs(reinterpret_cast<const uint2 *>(p.mm + i0));
-        const uint32_t v4 = __ldcs(reinterpret_cast<const uint32_t *>(p.validity + i0));
-        const uint32_t *c3 = reinterpret_cast<const uint32_t *>(p.rgb + i0 * 3);
-        const uint32_t ca = __ldcs(c3), cb = __ldcs(c3 + 1), cc = __ldcs(c3 + 2);
-        const uint32_t mm4[4] = {m.x & 0xFFFFu, m.x >> 16, m.y & 0xFFFFu, m.y >> 16};
+    // phase 1: every row's vector loads (raw words only, to keep registers
+    // for more bytes in flight)
+    bool vec[PROWS];
+    uint2 rm[PROWS];
+    uint32_t rv[PROWS], rc[PROWS][3];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            val[q] = (uint8_t)(v4 >> (8 * q));
-            decode_mm(mm4[q], val[q], z[q]);
-        }
-        g[0] = make_uchar4(ca & 255, (ca >> 8) & 255, (ca >> 16) & 255, 0);
-        g[1] = make_uchar4(ca >> 24, cb & 255, (cb >> 8) & 255, 0);
-        g[2] = make_uchar4((cb >> 16) & 255, cb >> 24, cc & 255, 0);
-        g[3] = make_uchar4((cc >> 8) & 255, (cc >> 16) & 255, cc >> 24, 0);
-    } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            z[q] = 0.0f;
-            val[q] = 0xFF;
-            g[q] = make_uchar4(0, 0, 0, 0);
-            if (row_ok && xb + q < p.W) {
-                load_depth(p, iy, xb + q, z[q], val[q], &code[q]);
-                g[q] = load_rgb(p, rowbase + xb + q);
-            }
+    for (int r = 0; r < PROWS; ++r) {
+        const int iy = y0 + ty + 8 * r;
+        vec[r] = iy < p.H && xb + 3 < p.W && (p.W & 3) == 0 && p.src == kSrcMM && p.rgb &&
+                 p.validity;
+        if (vec[r]) {
+            // 16-B aligned vector path (W % 4 == 0; torch/cudaMalloc bases are 256-B aligned)
+            const size_t i0 = (size_t)iy * p.W + xb;
+            rm[r] = __ldcs(reinterpret_cast<const uint2 *>(p.mm + i0));
+            rv[r] = __ldcs(reinterpret_cast<const uint32_t *>(p.validity + i0));
+            const uint32_t *c3 = reinterpret_cast<const uint32_t *>(p.rgb + i0 * 3);
+            rc[r][0] = __ldcs(c3);
+            rc[r][1] = __ldcs(c3 + 1);
+            rc[r][2] = __ldcs(c3 + 2);
         }
     }
+    // phase 2: decode, write the outputs (K1 later rewrites the pixels it
+    // fills, so the stores need not wait for the candidate test below) and
+    // keep each row's decoded validity (packed) for that test
+    uint32_t vp[PROWS];
     int nh = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) nh += (val[q] == FVV_INVALID);
-
-    // outputs first: K1 later rewrites the pixels it fills, so the stores
-    // need not wait for the candidate test below
-    if (row_ok) {
+    for (int r = 0; r < PROWS; ++r) {
+        const int iy = y0 + ty + 8 * r;
+        const size_t rowbase = (size_t)iy * p.W;
+        float z[4];
+        uint8_t val[4];
+        uchar4 g[4];
+        uint32_t code[4] = {0, 0, 0, 0};
+        if (vec[r]) {
+            const uint32_t mm4[4] = {rm[r].x & 0xFFFFu, rm[r].x >> 16, rm[r].y & 0xFFFFu,
+                                     rm[r].y >> 16};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                val[q] = (uint8_t)(rv[r] >> (8 * q));
+                decode_mm(mm4[q], val[q], z[q]);
+            }
+            const uint32_t ca = rc[r][0], cb = rc[r][1], cc = rc[r][2];
+            g[0] = make_uchar4(ca & 255, (ca >> 8) & 255, (ca >> 16) & 255, 0);
+            g[1] = make_uchar4(ca >> 24, cb & 255, (cb >> 8) & 255, 0);
+            g[2] = make_uchar4((cb >> 16) & 255, cb >> 24, cc & 255, 0);
+            g[3] = make_uchar4((cc >> 8) & 255, (cc >> 16) & 255, cc >> 24, 0);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                z[q] = 0.0f;
+                val[q] = 0xFF;
+                g[q] = make_uchar4(0, 0, 0, 0);
+                if (iy < p.H && xb + q < p.W) {
+                    load_depth(p, iy, xb + q, z[q], val[q], &code[q]);
+                    g[q] = load_rgb(p, rowbase + xb + q);
+                }
+            }
+        }
+        vp[r] = (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
+                ((uint32_t)val[3] << 24);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nh += (val[q] == FVV_INVALID);
+        if (iy >= p.H) continue;
         uint32_t tex[4];
         float wd[4];
 #pragma unroll
@@ -210,15 +237,12 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                      (flags << 24);
             wd[q] = (val[q] == FVV_VALID) ? z[q] : 0.0f;
         }
-        if (vec) {
+        if (vec[r]) {
             const size_t i0 = rowbase + xb;
             if (p.texel) *reinterpret_cast<uint4 *>(p.texel + i0) = make_uint4(tex[0], tex[1], tex[2], tex[3]);
             if (p.warp_depth) *reinterpret_cast<float4 *>(p.warp_depth + i0) = make_float4(wd[0], wd[1], wd[2], wd[3]);
             if (p.depth_out) *reinterpret_cast<float4 *>(p.depth_out + i0) = make_float4(z[0], z[1], z[2], z[3]);
-            if (p.validity_out)
-                *reinterpret_cast<uint32_t *>(p.validity_out + i0) =
-                    (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
-                    ((uint32_t)val[3] << 24);
+            if (p.validity_out) *reinterpret_cast<uint32_t *>(p.validity_out + i0) = vp[r];
         } else {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -247,16 +271,18 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
         // k_fill drains densely after this kernel (a tile holds a few dozen of
         // them, so filling them here would idle most of its lanes).
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sv[(ty + R) * SC + lane * 4 + q + R] = val[q];
+        for (int r = 0; r < PROWS; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sv[(ty + 8 * r + R) * SC + lane * 4 + q + R] = (uint8_t)(vp[r] >> (8 * q));
         const int SR = PY + 2 * R;
         // block-uniform choice (a thread's own `vec` is false on rows / columns
         // past the image, which must not change how the halo is split up)
         const bool hvec = R == 2 && (p.W & 3) == 0 && p.src == kSrcMM && p.validity;
         const int ring = hvec ? 0 : SR * SC - PY * PX;
         if (hvec) {
-            // halo validity with 16-byte-group loads: rows y0-2, y0-1, y0+8,
-            // y0+9 as 34 aligned 4-px groups each (columns x0-4 .. x0+131),
-            // then the 2-px side columns of the 8 tile rows
+            // halo validity with 16-byte-group loads: rows y0-2, y0-1, y0+PY,
+            // y0+PY+1 as 34 aligned 4-px groups each (columns x0-4 .. x0+131),
+            // then the 2-px side columns of the PY tile rows
             if (tid < 4 * 34) {
                 const int hr = tid / 34, gq = tid - hr * 34;
                 const int ry = hr < 2 ? hr : PY + hr;  // smem row
@@ -301,38 +327,43 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
             sv[ry * SC + rx] = vv;
         }
         __syncthreads();
-        unsigned cm[4];
+        unsigned cm[PROWS][4];
+        int wc = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            bool cand = false;
-            const int x = lane * 4 + q;  // tile column; window columns x..x+2R in smem
-            if (val[q] == FVV_INVALID) {
-                int cnt = 0;
-                if (R == 2) {
-                    // 5-byte window = 4 + 1 bytes out of two aligned words (Valid == 0)
-                    for (int dy = -2; dy <= 2; ++dy) {
-                        const int o = (ty + 2 + dy) * SC + x;
-                        const uint32_t *w = reinterpret_cast<const uint32_t *>(sv) + (o >> 2);
-                        const uint64_t span = (((uint64_t)w[1] << 32) | w[0]) >> (8 * (o & 3));
-                        cnt += __popc(__vcmpeq4((uint32_t)span, 0u)) / 8 +
-                               (((uint32_t)(span >> 32) & 0xFFu) == 0u);
+        for (int r = 0; r < PROWS; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bool cand = false;
+                const int x = lane * 4 + q;  // tile column; window columns x..x+2R in smem
+                const int row = ty + 8 * r;  // tile row
+                if (((vp[r] >> (8 * q)) & 0xFFu) == FVV_INVALID) {
+                    int cnt = 0;
+                    if (R == 2) {
+                        // 5-byte window = 4 + 1 bytes out of two aligned words (Valid == 0)
+                        for (int dy = -2; dy <= 2; ++dy) {
+                            const int o = (row + 2 + dy) * SC + x;
+                            const uint32_t *w = reinterpret_cast<const uint32_t *>(sv) + (o >> 2);
+                            const uint64_t span = (((uint64_t)w[1] << 32) | w[0]) >> (8 * (o & 3));
+                            cnt += __popc(__vcmpeq4((uint32_t)span, 0u)) / 8 +
+                                   (((uint32_t)(span >> 32) & 0xFFu) == 0u);
+                        }
+                    } else {
+                        for (int dy = -R; dy <= R; ++dy)
+                            for (int dx = -R; dx <= R; ++dx)
+                                cnt += sv[(row + R + dy) * SC + x + R + dx] == FVV_VALID;
                     }
-                } else {
-                    for (int dy = -R; dy <= R; ++dy)
-                        for (int dx = -R; dx <= R; ++dx)
-                            cnt += sv[(ty + R + dy) * SC + x + R + dx] == FVV_VALID;
+                    cand = cnt >= bl.min_valid;
                 }
-                cand = cnt >= bl.min_valid;
+                cm[r][q] = __ballot_sync(0xffffffffu, cand);
+                wc += __popc(cm[r][q]);
             }
-            cm[q] = __ballot_sync(0xffffffffu, cand);
-        }
         // one global atomic per tile (a single list counter is hit by every
         // tile with candidates): warp counts -> tile prefix -> list slots
-        if (lane == 0) s_wcnt[ty] = __popc(cm[0]) + __popc(cm[1]) + __popc(cm[2]) + __popc(cm[3]);
+        if (lane == 0) s_wcnt[ty] = wc;
         __syncthreads();
         if (tid == 0) {
             int tot = 0;
-            for (int w = 0; w < PY; ++w) {
+            for (int w = 0; w < 8; ++w) {
                 const int c = s_wcnt[w];
                 s_wcnt[w] = tot;
                 tot += c;
@@ -342,12 +373,15 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
         __syncthreads();
         int base = s_base + s_wcnt[ty];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((cm[q] >> lane) & 1u)
-                batch.cand[base + __popc(cm[q] & ((1u << lane) - 1u))] =
-                    ((uint32_t)blockIdx.z << 26) | (uint32_t)(rowbase + xb + q);
-            base += __popc(cm[q]);
-        }
+        for (int r = 0; r < PROWS; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if ((cm[r][q] >> lane) & 1u)
+                    batch.cand[base + __popc(cm[r][q] & ((1u << lane) - 1u))] =
+                        ((uint32_t)blockIdx.z << 26) |
+                        (uint32_t)((size_t)(y0 + ty + 8 * r) * p.W + xb + q);
+                base += __popc(cm[r][q]);
+            }
     }
 }
 
