@@ -69,8 +69,9 @@ def parse():
     ap.add_argument("--pipelines", type=int, default=None,
                     help="frames in flight: steps alternate over this many private renderers "
                          "on their own CUDA streams, so one frame's decode/fill (K0/K1) "
-                         "overlaps another's warp/resolve (K2/K3); default 2, and 1 for c0 "
-                         "whose 0.1 ms steps are bound by the host's launch calls")
+                         "overlaps another's warp/resolve (K2/K3); default 3 for c1/c3 (one "
+                         "ingest per view), 2 for c2/c4, and 1 for c0 whose 0.1 ms steps "
+                         "are bound by the host's launch calls")
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
@@ -83,7 +84,7 @@ def parse():
     if args.frames is None:
         args.frames = 300 if args.config == "c3" else 4
     if args.pipelines is None:
-        args.pipelines = 1 if args.config == "c0" else 2
+        args.pipelines = {"c0": 1, "c1": 3, "c3": 3}.get(args.config, 2)
     return args
 
 
