@@ -1,28 +1,43 @@
-import torch, time
-dev=torch.device('cuda')
-for mb in (4, 37.3, 112):
-    n=int(mb*1e6)
-    h=torch.empty(n,dtype=torch.uint8).pin_memory(); d=torch.empty(n,dtype=torch.uint8,device=dev)
-    for _ in range(3): d.copy_(h,non_blocking=True)
+"""PCIe probe: H2D / D2H bandwidth of pinned copies by size, and one c1
+frame (3 cameras x RGB + mm + validity, 37.3 MB) as 9 copies vs one packed
+copy. Used to size the e2e path (bench.py e2e, engine.FrameUploader)."""
+import torch
+
+dev = torch.device("cuda")
+
+
+def rate(fn, nbytes, reps=30):
+    for _ in range(5):
+        fn()
     torch.cuda.synchronize()
-    s=torch.cuda.Event(enable_timing=True); e=torch.cuda.Event(enable_timing=True)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(20): d.copy_(h,non_blocking=True)
-    e.record(); torch.cuda.synchronize()
-    ms=s.elapsed_time(e)/20
-    print(f"H2D {mb} MB: {n/ms/1e6:.1f} GB/s")
-    s.record()
-    for _ in range(20): h.copy_(d,non_blocking=True)
-    e.record(); torch.cuda.synchronize()
-    ms=s.elapsed_time(e)/20
-    print(f"D2H {mb} MB: {n/ms/1e6:.1f} GB/s")
-# concurrent H2D + D2H
-n=int(37.3e6); h=torch.empty(n,dtype=torch.uint8).pin_memory(); d=torch.empty(n,dtype=torch.uint8,device=dev)
-h2=torch.empty(n//6,dtype=torch.uint8).pin_memory(); d2=torch.empty(n//6,dtype=torch.uint8,device=dev)
-s1=torch.cuda.Stream(); s2=torch.cuda.Stream()
-torch.cuda.synchronize(); t=time.perf_counter()
-for _ in range(20):
-    with torch.cuda.stream(s1): d.copy_(h,non_blocking=True)
-    with torch.cuda.stream(s2): h2.copy_(d2,non_blocking=True)
-torch.cuda.synchronize(); dt=(time.perf_counter()-t)/20
-print(f"concurrent 37.3MB H2D + 6.2MB D2H: {dt*1e3:.3f} ms/iter -> H2D {n/dt/1e9:.1f} GB/s")
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return nbytes / (s.elapsed_time(e) / reps) / 1e6
+
+
+for mb in (2, 4, 8, 37.3, 112):
+    n = int(mb * 1e6)
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    print(f"H2D {mb:6} MB: {rate(lambda: d.copy_(h, non_blocking=True), n):6.1f} GB/s   "
+          f"D2H: {rate(lambda: h.copy_(d, non_blocking=True), n):6.1f} GB/s")
+N = 1920 * 1080
+sizes = [3 * N, 2 * N, N] * 3
+hs = [torch.empty(s, dtype=torch.uint8).pin_memory() for s in sizes]
+ds = [torch.empty(s, dtype=torch.uint8, device=dev) for s in sizes]
+tot = sum(sizes)
+
+
+def nine():
+    for d, h in zip(ds, hs):
+        d.copy_(h, non_blocking=True)
+
+
+hp = torch.empty(tot, dtype=torch.uint8).pin_memory()
+dp = torch.empty(tot, dtype=torch.uint8, device=dev)
+print(f"c1 frame as 9 copies: {rate(nine, tot):6.1f} GB/s; "
+      f"packed: {rate(lambda: dp.copy_(hp, non_blocking=True), tot):6.1f} GB/s")
