@@ -4,9 +4,11 @@
 //                        and warp depth, list the hole-fill candidates
 //   K1  k_fill_g8/k_fill joint-bilateral fill of the listed candidates
 //   K2  k_forward_warp   forward 3-D warp, one 64-bit atomicMin per source
-//                        pixel into a padded keyed z canvas, exact z kept
-//   K3  k_resolve_fast   per 32x8 target tile and per contribution: splat
-//       (k_resolve_generic for other splat radii / crack windows)
+//                        pixel into a padded keyed z canvas, exact z kept;
+//                        FG contributions flag the target tiles they reach
+//   K3  k_resolve_fast   per 32x8 target tile and per contribution (BG ones
+//       (k_resolve_generic  and the flagged FG ones): splat
+//        for other splat radii / crack windows)
 //                        ring + FG cull + crack median in shared memory, f64
 //                        backward projection, masked bilinear fetch; then the
 //                        two layer mixes and the FG-over-BG composite -> RGB8
