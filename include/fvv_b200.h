@@ -254,6 +254,25 @@ int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *stream
                            const int32_t *heights, uint8_t *const *planes_out,
                            uint32_t *adlers_out, int32_t *status_out);
 
+/* ---- MVD disk container rasters (mvdio.py) -------------
+ * The container's files (PNG colour, u16le mm depth, JSON sidecar with the
+ * validity run-length code) are read and written by the host; these are the
+ * per-pixel parts. Device pointers. */
+/* core.depth_to_millimeters (core.py:246-255): Valid pixels ->
+ * clip(rint(f32(depth * 1000)), 1, 65535), all others 0. */
+int fvv_encode_mm(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                  int32_t height, uint16_t *mm_out);
+/* mvdio.rle_decode (mvdio.py:43-52) after the host checked the runs cover
+ * exactly n pixels (the reference's ValueError): run r = codes[r] over
+ * [ends[r-1], ends[r]) (ends = cumulative run lengths). */
+int fvv_rle_decode(fvv_ctx *ctx, const uint8_t *codes, const int64_t *ends, int64_t n_runs,
+                   int64_t n, uint8_t *out);
+/* mvdio.rle_encode (mvdio.py:34-40): the starts and codes of the runs of
+ * flat[0..n) in order (starts_out / codes_out hold up to n entries);
+ * *n_runs_out (host) after the call, which synchronises. */
+int fvv_rle_encode(fvv_ctx *ctx, const uint8_t *flat, int64_t n, int64_t *starts_out,
+                   uint8_t *codes_out, int64_t *n_runs_out);
+
 /* ---- session path: resident camera slots, batched views ---------------------
  * The edge server keeps a slot per rig camera: its calibration, its static
  * BG model (uploaded once, pipeline.py:445) and its latest live frame. */

@@ -23,6 +23,8 @@ What it restates, function by function (each cites the reference line):
 * ``correct_depth``        depthproc.correct_depth          depthproc.py:67-84
 * ``bg_train`` / ``classify_fg``  depthproc BG model         depthproc.py:121-149
 * ``remove_bg_depth``      depthproc.remove_bg_depth        depthproc.py:152-164
+* ``depth_to_millimeters`` core.depth_to_millimeters        core.py:246-255
+* ``rle_encode`` / ``rle_decode``  mvdio validity sidecar   mvdio.py:34-52
 
 Differences from the reference, all deliberate and mirrored by the kernels:
 
@@ -709,3 +711,38 @@ def decompress_plane(data: bytes, offset: int, shape):
 def encode_lossless_payload(y, u, v) -> bytes:
     """encode_lossless's CODEC_PRED_RICE payload (depthcodec.py:437-438)."""
     return b"".join(compress_plane(p) for p in (y, u, v))
+
+
+# ---------------------------------------------------------------------------
+# MVD disk container rasters (mvdio.py, core.py)
+
+
+def depth_to_millimeters(depth: np.ndarray, validity: np.ndarray) -> np.ndarray:
+    """core.py:246-255 (``encode_mm`` above, with f32 input): Valid pixels ->
+    clip(round(f32 depth * 1000), 1, 65535) (the product stays float32 under
+    numpy 2's promotion of the Python scalar; np.round is half-to-even);
+    every other pixel 0."""
+    return encode_mm(np.asarray(depth, dtype=np.float32), np.asarray(validity))
+
+
+def rle_encode(flat: np.ndarray):
+    """mvdio.py:34-40: [[code, run], ...] over the flattened raster; a run
+    starts at 0 and wherever a value differs from its predecessor."""
+    flat = np.asarray(flat).ravel()
+    if flat.size == 0:
+        return []
+    starts = np.concatenate([[0], np.flatnonzero(flat[1:] != flat[:-1]) + 1])
+    ends = np.concatenate([starts[1:], [flat.size]])
+    return [[int(flat[a]), int(b - a)] for a, b in zip(starts, ends)]
+
+
+def rle_decode(runs, size: int) -> np.ndarray:
+    """mvdio.py:43-52: the runs must cover exactly ``size`` pixels."""
+    out = np.empty(size, dtype=np.uint8)
+    pos = 0
+    for code, n in runs:
+        out[pos:pos + n] = code
+        pos += n
+    if pos != size:
+        raise ValueError(f"RLE covers {pos} pixels, expected {size}")
+    return out

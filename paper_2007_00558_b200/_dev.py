@@ -7,7 +7,7 @@ import torch
 
 # uint16 rasters travel as int16 (same bytes; torch's uint16 support is partial)
 _DT = {np.uint8: torch.uint8, np.uint16: torch.int16, np.int32: torch.int32,
-       np.float32: torch.float32, np.float64: torch.float64}
+       np.int64: torch.int64, np.float32: torch.float32, np.float64: torch.float64}
 
 
 def device() -> torch.device:

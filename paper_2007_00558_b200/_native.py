@@ -38,7 +38,8 @@ EXPORTS = (
     "fvv_correct_depth", "fvv_bg_train", "fvv_classify_fg", "fvv_remove_bg_depth",
     "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode", "fvv_slots_ingest_mm",
     "fvv_set_range_weights", "fvv_rice_stream_bound", "fvv_rice_encode_plane",
-    "fvv_rice_decode_plane", "fvv_rice_decode_planes",
+    "fvv_rice_decode_plane", "fvv_rice_decode_planes", "fvv_encode_mm", "fvv_rle_decode",
+    "fvv_rle_encode",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -122,6 +123,9 @@ _SIGS = {
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_void_p), C.POINTER(C.c_uint32),
                                 C.POINTER(C.c_int32)], C.c_int),
+    "fvv_encode_mm": ([_VP, _VP, _VP, _I32, _I32, _VP], C.c_int),
+    "fvv_rle_decode": ([_VP, _VP, _VP, C.c_int64, C.c_int64, _VP], C.c_int),
+    "fvv_rle_encode": ([_VP, _VP, C.c_int64, _VP, _VP, C.POINTER(C.c_int64)], C.c_int),
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
                          C.c_int),

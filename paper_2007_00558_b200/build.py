@@ -10,7 +10,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-SOURCES = ("fvv_kernels.cu", "fvv_capture.cu", "fvv_codec.cu", "fvv_capi.cu")
+SOURCES = ("fvv_kernels.cu", "fvv_capture.cu", "fvv_codec.cu", "fvv_mvd.cu", "fvv_capi.cu")
 LIB = PKG / "libfvvb200.so"
 ARCH = ("-gencode", "arch=compute_100a,code=sm_100a")
 

@@ -13,6 +13,7 @@
 #include "fvv_capture.cuh"
 #include "fvv_codec.cuh"
 #include "fvv_kernels.cuh"
+#include "fvv_mvd.cuh"
 
 using namespace fvv;
 
@@ -74,6 +75,8 @@ struct fvv_ctx {
     size_t cand_cap = 0;
     // MED + Rice plane codec scratch
     RiceScratch rice;
+    // MVD container validity run-length encoder scratch
+    RleScratch rle;
     // K1 range-weight table for range_sigma (kRangeTableLen doubles)
     double *range_w = nullptr;
     double range_sigma = -1.0;
@@ -566,6 +569,8 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
+    cudaFree(ctx->rle.block);
+    cudaFree(ctx->rle.n_runs);
     for (void *q : {(void *)ctx->rice.zz, (void *)ctx->rice.res, (void *)ctx->rice.skew,
                     (void *)ctx->rice.block,
                     (void *)ctx->rice.costs, (void *)ctx->rice.total, (void *)ctx->rice.entry,
@@ -876,6 +881,56 @@ int fvv_capture_encode(fvv_ctx *ctx, const float *depth, const uint8_t *validity
 int64_t fvv_rice_stream_bound(int32_t width, int32_t height) {
     if (width < 0 || height < 0) return -1;
     return rice_stream_bound(width, height);
+}
+
+// ---------------------------------------------------------------------------
+// MVD disk container rasters (mvdio.py, core.py:246-255)
+
+int fvv_encode_mm(fvv_ctx *ctx, const float *depth, const uint8_t *validity, int32_t width,
+                  int32_t height, uint16_t *mm_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(width >= 0 && height >= 0 && depth && validity && mm_out, "encode_mm: bad arguments");
+    if (!width || !height) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_encode_mm(depth, validity, (long long)width * height, mm_out,
+                                           ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_rle_decode(fvv_ctx *ctx, const uint8_t *codes, const int64_t *ends, int64_t n_runs,
+                   int64_t n, uint8_t *out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(n >= 0 && n_runs >= 0 && (n == 0 || (n_runs > 0 && codes && ends && out)),
+         "rle_decode: bad arguments");
+    if (!n) return FVV_OK;
+    LAUNCH_K(FVV_K_OTHER, launch_rle_decode(codes, reinterpret_cast<const long long *>(ends),
+                                            n_runs, n, out, ctx->stream));
+    return FVV_OK;
+}
+
+int fvv_rle_encode(fvv_ctx *ctx, const uint8_t *flat, int64_t n, int64_t *starts_out,
+                   uint8_t *codes_out, int64_t *n_runs_out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    NEED(n >= 0 && n_runs_out && (n == 0 || (flat && starts_out && codes_out)),
+         "rle_encode: bad arguments");
+    const size_t nb = (size_t)((n + kRlePx - 1) / kRlePx);
+    if (nb + 1 > ctx->rle.cap || !ctx->rle.n_runs) {
+        CK(cudaFree(ctx->rle.block));
+        ctx->rle.block = nullptr;
+        CK(cudaMalloc(&ctx->rle.block, (nb + 1) * sizeof(unsigned long long)));
+        if (!ctx->rle.n_runs) CK(cudaMalloc(&ctx->rle.n_runs, sizeof(long long)));
+        ctx->rle.cap = nb + 1;
+    }
+    LAUNCH(launch_rle_encode(flat, n, reinterpret_cast<long long *>(starts_out), codes_out,
+                             ctx->rle, ctx->stream));
+    ctx->launches += n > 0 ? 2 : 0;   // k_rle_count, k_rle_scan, k_rle_write
+    long long nr = 0;
+    CK(cudaMemcpyAsync(&nr, ctx->rle.n_runs, sizeof(nr), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *n_runs_out = nr;
+    return FVV_OK;
 }
 
 int fvv_rice_encode_plane(fvv_ctx *ctx, const uint8_t *plane, int32_t width, int32_t height,

@@ -22,7 +22,11 @@ What is rebound:
   module's codec then builds and raises the reference's own types
   (EncodedFrame, Yuv420Image, DisparityMap12, DecodeError,
   UnsupportedCodecError), so callers that catch or isinstance-check them
-  keep working.
+  keep working;
+* with ``FVV_SHIM_MVDIO=1`` the MVD disk container (``fvv.mvdio``:
+  ``rle_encode`` / ``rle_decode`` / ``MvdWriter`` / ``MvdReader``, and the
+  ``MvdWriter`` that pipeline.py:32 imported); the reader returns this
+  package's frame types, which carry the same attributes.
 """
 
 from __future__ import annotations
@@ -71,6 +75,15 @@ def install() -> types.ModuleType:
         for name in ("unpack_yuv420", "dequantize12", "quantize12", "pack_yuv420",
                      "encode_lossless", "decode_lossless"):
             setattr(ref_codec, name, getattr(ours_codec, name))
+    if os.environ.get("FVV_SHIM_MVDIO") == "1":
+        import fvv.mvdio as ref_mvd
+
+        from . import mvdio as ours_mvd
+
+        for name in ("rle_encode", "rle_decode", "MvdWriter", "MvdReader"):
+            setattr(ref_mvd, name, getattr(ours_mvd, name))
+        if "fvv.pipeline" in sys.modules:   # pipeline.py:32 binds MvdWriter at import
+            sys.modules["fvv.pipeline"].MvdWriter = ours_mvd.MvdWriter
     installed["synthesis"] = mod
     return mod
 

@@ -291,13 +291,65 @@ def silhouette_case():
     print("silhouette ok: holes", int((degraded.validity == 1).sum()))
 
 
+def mvd_case():
+    """A small MVD disk container written by the reference's own MvdWriter
+    (mvdio.py:55-98): 2 cameras x 2 sequence numbers of a 48x32 rig render,
+    depth degraded with holes (all three validity codes present) and a row of
+    depths on half-millimetre boundaries; plus what the reference's MvdReader
+    reads back and its rle_encode / depth_to_millimeters of each frame."""
+    import shutil
+
+    import fvv.mvdio as rmvd
+
+    root = OUT / "mvd"
+    if root.exists():
+        shutil.rmtree(root)
+    rig = rscene.build_camera_arc(9, 0.270, 60.0, width=48, height=32)
+    scene = rscene.make_scene("simple")
+    out = {}
+    with rmvd.MvdWriter(root, 30.0, 48, 32) as w:
+        for cam in (2, 5):
+            for seq in (0, 7):
+                mvd, fg = rscene.render_with_mask(scene, rig[cam], seq / 30.0)
+                d = rscene.degrade_depth(mvd.depth, rscene.DepthErrorSpec(0.0, 1.0, hole_width=1),
+                                         seed=cam * 10 + seq, fg_mask=fg)
+                depth, val = d.depth.copy(), d.validity.copy()
+                val[0, :6] = [0, 1, 2, 2, 1, 0]
+                depth[0, :6] = [1.5, 0.0, 0.0, 0.0, 0.0, 2.25]
+                depth[1, :8] = (np.arange(8, dtype=np.float32) + np.float32(1234.5)) / 1000
+                val[1, :8] = 0
+                frame = rc.MvdFrame(camera_id=cam, color=mvd.color,
+                                    depth=rc.DepthFrame(48, 32, depth, val, mvd.depth.timestamp_us))
+                w.write_frame(seq, frame)
+                key = f"c{cam}_s{seq}"
+                out[key + "_depth_in"] = depth
+                out[key + "_validity_in"] = val
+                out[key + "_mm"] = rc.depth_to_millimeters(frame.depth)
+                out[key + "_rle"] = np.asarray(rmvd.rle_encode(val), dtype=np.int64)
+    r = rmvd.MvdReader(root)
+    for cam in r.cameras:
+        for seq in r.sequences(cam):
+            f = r.read_frame(cam, seq)
+            key = f"c{cam}_s{seq}"
+            out[key + "_rgb"] = f.color.pixels
+            out[key + "_depth"] = f.depth.depth
+            out[key + "_validity"] = f.depth.validity
+            out[key + "_ts"] = np.int64(f.timestamp_us)
+    np.savez_compressed(OUT / "mvd.npz", **out)
+    print("mvd ok:", sorted(p.name for p in root.rglob("*") if p.is_file())[:6], "...")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["mvd"]:
+        mvd_case()
+        sys.exit(0)
     if sys.argv[1:] == ["rice"]:
         rice_case()
         sys.exit(0)
     if sys.argv[1:] == ["silhouette"]:
         silhouette_case()
         sys.exit(0)
+    mvd_case()
     silhouette_case()
     rice_case()
     capture_case()

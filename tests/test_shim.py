@@ -61,3 +61,26 @@ print("OK")
                          cwd="/tmp")
     assert out.returncode == 0, out.stderr
     assert "OK" in out.stdout
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference package not present on this host")
+def test_shim_rebinds_mvd_container_on_request():
+    code = r"""
+import os
+os.environ["FVV_SHIM_MVDIO"] = "1"
+import fvv.pipeline
+from paper_2007_00558_b200 import pytest_shim, mvdio as ours
+pytest_shim.install()
+import fvv.mvdio
+for n in ("rle_encode", "rle_decode", "MvdWriter", "MvdReader"):
+    assert getattr(fvv.mvdio, n) is getattr(ours, n), n
+assert fvv.pipeline.MvdWriter is ours.MvdWriter
+print("OK")
+"""
+    env = {"PYTHONPATH": f"{REF_SRC}:{ROOT}", "PYTHONDONTWRITEBYTECODE": "1",
+           "PATH": "/usr/bin:/bin"}
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd="/tmp")
+    assert out.returncode == 0, out.stderr
+    assert "OK" in out.stdout
+
