@@ -1292,6 +1292,9 @@ __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst
     return true;
 }
 
+#ifndef FVV_K3_MIXUNROLL
+#define FVV_K3_MIXUNROLL 1
+#endif
 #ifndef FVV_K3_NBUF
 #define FVV_K3_NBUF 2
 #endif
@@ -1432,15 +1435,27 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     auto mix = [&](bool fgl, int kb) {
         // valid contributions only, in ascending (reference) order
         double zmin = INFINITY;
+#if FVV_K3_MIXUNROLL
+#pragma unroll
+        for (int qq = 0; qq < MAXR; ++qq) {
+            if (!((vmask >> qq) & 1u)) continue;
+#else
         for (unsigned m = vmask; m; m &= m - 1) {
             const int qq = __ffs(m) - 1;
+#endif
             const double zj = sres[(qq * 4 + 3) * FNT + tid];
             if (zj < zmin) zmin = zj;
         }
         const double thr = dadd(zmin, dmul(p.band_rel, zmin));
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, ad = 0.0, aw = 0.0;
+#if FVV_K3_MIXUNROLL
+#pragma unroll
+        for (int qq = 0; qq < MAXR; ++qq) {
+            if (!((vmask >> qq) & 1u)) continue;
+#else
         for (unsigned m = vmask; m; m &= m - 1) {
             const int qq = __ffs(m) - 1;
+#endif
             const double zj = sres[(qq * 4 + 3) * FNT + tid];
             if (zj <= thr) {
                 const double w = ANG ? swt[qq * FNT + tid] : p.c[kb + qq].weight;
