@@ -19,6 +19,7 @@
 // in fvv_common.cuh and oracle/fvv_oracle.py.
 
 #include <atomic>
+#include <type_traits>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -1049,6 +1050,14 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 constexpr int FTY = FVV_K3_TY, FNT = TX * FTY;                   // fast-path tile: 32 x FTY
 constexpr int FKR = FTY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36 (FTY = 8)
 constexpr int FBR = FTY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+// 32-bit winner cells from this many contributions per layer on (default:
+// always). They save 2.7 KB of shared memory, which keeps 5 CTAs/SM with a
+// 4-reference sres (c4: K3 1,078 -> 943 us) and trims K3 at c1 by 3 %.
+#ifndef FVV_K3_W32_FROM
+#define FVV_K3_W32_FROM 1
+#endif
+template <int MAXR>
+using WinnerT = typename std::conditional<(MAXR >= FVV_K3_W32_FROM), uint32_t, uint64_t>::type;
 // a key span of TX + 4 (FTY + 4) pixels meets at most 3 flag tiles per axis
 static_assert(2 * FVV_TF_W >= TX + 3 && 2 * FVV_TF_H >= FTY + 3, "flag tiles too small");
 constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
@@ -1135,8 +1144,25 @@ __device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam
     return __ldg(c.zsrc + idx);
 }
 
-__device__ __forceinline__ double key_z(const ResolveContrib &c, const DevCam &dst, uint64_t w) {
-    return w == kEmpty ? INFINITY : winner_z(c, dst, (uint32_t)(w & ((1ull << c.b) - 1)));
+// A cell's winner as K3 keeps it in shared memory: the whole 64-bit key, or
+// (WT = uint32_t, for the wider contribution counts, whose mixes need the
+// shared memory) just its source index — the key's depth bits only order the
+// z-buffer, the exact z comes from zsrc. All ones = no winner either way.
+template <typename WT>
+__device__ __forceinline__ WT w_pack(uint64_t key, int b) {
+    if (sizeof(WT) == 8) return (WT)key;
+    return key == kEmpty ? (WT)~0u : (WT)(key & ((1ull << b) - 1));
+}
+template <typename WT>
+__device__ __forceinline__ bool w_none(WT w) { return w == (WT)~(WT)0; }
+template <typename WT>
+__device__ __forceinline__ uint32_t w_idx(WT w, int b) {
+    return sizeof(WT) == 8 ? (uint32_t)((uint64_t)w & ((1ull << b) - 1)) : (uint32_t)w;
+}
+
+template <typename WT>
+__device__ __forceinline__ double key_z(const ResolveContrib &c, const DevCam &dst, WT w) {
+    return w_none(w) ? INFINITY : winner_z(c, dst, w_idx(w, c.b));
 }
 
 __device__ __forceinline__ void cswap(double &a, double &b) {
@@ -1147,9 +1173,9 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
 
 // Phase "cells" of one contribution: splat policy + FG cull (synthesis.py:
 // 207-219) for the 10x34 cells around the tile -> winner key (kEmpty = none).
-template <bool DBG>
+template <bool DBG, typename WT>
 __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, int Hd,
-                                             const uint64_t *K, uint64_t *swk, uint8_t *sst,
+                                             const uint64_t *K, WT *swk, uint8_t *sst,
                                              uint64_t gen, int x0, int y0, int tid) {
     int any = 0;
 #pragma unroll
@@ -1198,7 +1224,7 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
             }
             any |= w != kEmpty;
         }
-        swk[i] = w;
+        swk[i] = w_pack<WT>(w, c.b);
         if (DBG) sst[i] = sq;
     }
     return any;
@@ -1211,17 +1237,18 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
 #ifndef FVV_K3_CRACK_NOINLINE
 #define FVV_K3_CRACK_NOINLINE 0
 #endif
+template <typename WT>
 #if FVV_K3_CRACK_NOINLINE
 __device__ __noinline__
 #else
 __device__ __forceinline__
 #endif
 double crack_z(const ResolveContrib &c, const DevCam &dst,
-                                       const uint64_t *W, int bi, int *stage) {
-    const uint64_t k0 = W[bi - FBC - 1], k1 = W[bi - FBC], k2 = W[bi - FBC + 1], k3 = W[bi - 1],
-                   k4 = W[bi + 1], k5 = W[bi + FBC - 1], k6 = W[bi + FBC], k7 = W[bi + FBC + 1];
-    const int cnt = (k0 != kEmpty) + (k1 != kEmpty) + (k2 != kEmpty) + (k3 != kEmpty) +
-                    (k4 != kEmpty) + (k5 != kEmpty) + (k6 != kEmpty) + (k7 != kEmpty);
+                                       const WT *W, int bi, int *stage) {
+    const WT k0 = W[bi - FBC - 1], k1 = W[bi - FBC], k2 = W[bi - FBC + 1], k3 = W[bi - 1],
+             k4 = W[bi + 1], k5 = W[bi + FBC - 1], k6 = W[bi + FBC], k7 = W[bi + FBC + 1];
+    const int cnt = !w_none(k0) + !w_none(k1) + !w_none(k2) + !w_none(k3) + !w_none(k4) +
+                    !w_none(k5) + !w_none(k6) + !w_none(k7);
     if (cnt < 5) return INFINITY;
     double v0 = key_z(c, dst, k0), v1 = key_z(c, dst, k1), v2 = key_z(c, dst, k2),
            v3 = key_z(c, dst, k3), v4 = key_z(c, dst, k4), v5 = key_z(c, dst, k5),
@@ -1316,7 +1343,8 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[NBUF];                // TMA completion per buffer
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
-    uint64_t *swk = sk + NBUF * FKEYS;                           // [2][FCELLS] winner keys
+    using WT = WinnerT<MAXR>;
+    WT *swk = reinterpret_cast<WT *>(sk + NBUF * FKEYS);          // [2][FCELLS] winners
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][FNT]
     double *sray = sres + MAXR * 4 * FNT;                         // [TX] rx, [FTY] ry
     double *swt = sray + TX + FTY;                                // [MAXR][FNT] weights (ANG)
@@ -1525,7 +1553,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
                                           swk + ((q + 1) & 1) * FCELLS,
                                           sst + ((q + 1) & 1) * FCELLS, gen, x0, y0, tid);
         const ResolveContrib &c = p.c[k];
-        const uint64_t *W = swk + (q & 1) * FCELLS;
+        const WT *W = swk + (q & 1) * FCELLS;
         double z = INFINITY;
         int win = -1;
         uint8_t st = kStageNone;
@@ -1536,10 +1564,10 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         // there unless every intermediate raster is requested (DBG)
         if (any && inimg && (DBG || fgl || !fv)) {
             const int bi = (ty + 1) * FBC + tx + 1;
-            const uint64_t wk = W[bi];
+            const WT wk = W[bi];
             if (DBG) st = sst[(q & 1) * FCELLS + bi];
-            if (wk != kEmpty) {
-                const uint32_t idx = (uint32_t)(wk & ((1ull << c.b) - 1));
+            if (!w_none(wk)) {
+                const uint32_t idx = w_idx(wk, c.b);
                 z = winner_z(c, dst, idx);
                 win = (int)idx;
             } else {
@@ -1610,7 +1638,7 @@ static void raise_smem(K kernel, size_t bytes, std::atomic<uint64_t> &done) {
 
 template <int MAXR, bool ANG>
 static size_t fast_smem() {
-    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(uint64_t) +
+    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(WinnerT<MAXR>) +
            (size_t)MAXR * 4 * FNT * sizeof(double) + (TX + FTY) * sizeof(double) +
            (ANG ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
 }
