@@ -615,7 +615,13 @@ __device__ __forceinline__ uint8_t *tile_flag(const TileFlags &tf, int k, int t)
 
 __device__ __forceinline__ void mark_tile(uint8_t *f, uint8_t gen8) { *f = gen8; }
 
-__global__ void __launch_bounds__(K2_THREADS) k_forward_warp(const __grid_constant__ WarpParams p) {
+// 12 CTAs of 128 threads per SM (40 registers, a few bytes of spill): K2
+// is issue-bound with its atomics' latency to hide; 46 registers (10 CTAs)
+// measured 68.1 us at c1, 40 registers 66.1, 32 registers (16 CTAs) 68.2.
+#ifndef FVV_K2_MINB
+#define FVV_K2_MINB 12
+#endif
+__global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const __grid_constant__ WarpParams p) {
     const WarpContrib &c = p.c[blockIdx.z];
     const int Ws = c.src.W, Hs = c.src.H;
     const int sv = blockIdx.y;
