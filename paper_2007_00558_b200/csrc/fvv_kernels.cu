@@ -1372,6 +1372,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     // when debug rasters are requested)
     __shared__ int8_t s_item[2 * FVV_MAX_REFS];
     __shared__ int s_nitems;
+    __shared__ int s_needbg;   // some in-image pixel's merged FG layer is invalid
 #if FVV_K3_TMA
     // key tiles by TMA: thread 0 arms buffer q % NBUF's mbarrier and issues
     // the box; canvas column x0-1 .. x0+34 is tensor x = x0 .. x0+35 (the
@@ -1415,7 +1416,10 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         }
         const unsigned m = __ballot_sync(0xffffffffu, act);
         if (act) s_item[__popc(m & ((1u << tid) - 1u))] = (int8_t)tid;
-        if (tid == 0) s_nitems = __popc(m);
+        if (tid == 0) {
+            s_nitems = __popc(m);
+            s_needbg = 0;
+        }
 #if FVV_K3_TMA
         // the first key tiles go out before the CTA barrier
         __syncwarp();
@@ -1542,6 +1546,11 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
 #if FVV_K3_TMA
         wait_keys(q + 1);
         const int any = __syncthreads_or(any_next);
+        // every in-image pixel has a valid merged FG layer: the BG layer cannot
+        // change the composite (FG wins wherever valid, synthesis.py:309-311),
+        // so the tile skips its BG contributions (no key tile is in flight:
+        // q+1's landed above, q+2's is issued below)
+        if (!DBG && !fgl && q > 0 && s_item[q - 1] < p.n_fg && !s_needbg) break;
         // keys of q+NBUF into the buffer item q's cells phase used (all reads of
         // it by the generic proxy are ordered before the barrier above)
         if (tid == 0) fence_proxy_async();
@@ -1549,6 +1558,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
 #else
         cp_async_wait<NBUF - 2>();
         const int any = __syncthreads_or(any_next);
+        if (!DBG && !fgl && q > 0 && s_item[q - 1] < p.n_fg && !s_needbg) break;
         // keys of q+NBUF into the buffer item q's cells phase (iteration q-1) used
         stage(q + NBUF);
 #endif
@@ -1611,7 +1621,10 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
         }
         // the last resolved contribution of its layer ends it
         const bool last = q + 1 == nitems || (fgl && s_item[q + 1] >= p.n_fg);
-        if (last) mix(fgl, k - j);
+        if (last) {
+            mix(fgl, k - j);
+            if (!DBG && fgl && inimg && !fv) s_needbg = 1;
+        }
     }
     // -- end of a tile: composite (synthesis.py:295-318): hole, BG, FG; rint, clip
     if (inimg) {

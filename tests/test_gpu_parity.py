@@ -432,3 +432,30 @@ def test_foreground_keys_only_in_neighbour_tiles(cuda):
     # pixels, so the composite leaves them holes, like the oracle
     _, b = S.synthesize_view_debug(cam, case.inputs(), [1], S.SynthesisConfig())
     assert (b.fg_contributions[0].winner[8::8, 32::32] >= 0).all()
+
+
+@pytest.mark.parametrize("name", ["syn_c1_s8.npz", "syn_c2_s8_v3.npz"])
+def test_dense_foreground_bg_skip_bit_exact(cuda, name):
+    """Live pixels classified Background turned Valid (foreground): most K3
+    tiles then have a valid merged FG layer at every pixel and skip their BG
+    contributions; the few holes left still take the BG layer. Equal to the
+    oracle and to the all-contributions debug render."""
+    from paper_2007_00558_b200 import synthesis as S
+
+    _, case = _case(name)
+    for a in case.arrays:
+        # Background-classified live pixels carry no live depth: give them the
+        # BG model's depth and make them foreground
+        bgc = (a["live_validity"] == 2) & (a["bg_validity"] == 0) & (a["bg_depth"] > 0)
+        bgc[:, int(0.7 * bgc.shape[1]):] = False   # the right part keeps its BG layer
+        a["live_depth"] = np.where(bgc, a["bg_depth"], a["live_depth"]).astype(np.float32)
+        a["live_validity"] = np.where(bgc, 0, a["live_validity"]).astype(np.uint8)
+    frame, prov = S.synthesize_view(case.virtual, case.inputs(), case.refs, S.SynthesisConfig(),
+                                    return_provenance=True)
+    o_rgb, o_prov, _ = O.synthesize_view(case.virtual, case.oracle_refs(), debug=True)
+    np.testing.assert_array_equal(frame.pixels, o_rgb)
+    np.testing.assert_array_equal(prov, o_prov)
+    dframe, _ = S.synthesize_view_debug(case.virtual, case.inputs(), case.refs,
+                                        S.SynthesisConfig())
+    np.testing.assert_array_equal(frame.pixels, dframe.pixels)
+    assert (o_prov == 2).mean() > 0.5 and (o_prov == 1).mean() > 0.05
