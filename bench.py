@@ -543,7 +543,7 @@ def run_ours(args):
         e2e = {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
                "h2d_bytes_per_step": (b1 - b0) // args.steps,
                "d2h_bytes_per_step": (dl.bytes - d0) // args.steps,
-               "api": "FrameUploader (pinned H2D, copy stream) -> EdgeRenderer.ingest_mm_many + "
+               "api": "FrameUploader (pinned H2D, two copy streams) -> EdgeRenderer.ingest_mm_many + "
                       "render (C ABI fvv_slots_ingest_mm, fvv_render_views) -> "
                       "ResultDownloader (D2H, copy stream), double-buffered",
                "ms_per_step": ms2 / args.steps}

@@ -211,9 +211,14 @@ class FrameUploader:
     copy + compute in series.
     """
 
-    def __init__(self, example_frame: Mapping, depth: int = 2, device=None):
+    def __init__(self, example_frame: Mapping, depth: int = 2, device=None, lanes: int = None):
         self.dev = _dev.device() if device is None else torch.device(device)
         self.stream = torch.cuda.Stream(self.dev)
+        # copies spread over `lanes` streams so one copy's setup overlaps
+        # another's transfer (FVV_UPLOAD_LANES overrides; 1 = one stream)
+        import os
+        lanes = int(os.environ.get("FVV_UPLOAD_LANES", lanes or 2))
+        self.extra = [torch.cuda.Stream(self.dev) for _ in range(max(lanes, 1) - 1)]
         self.depth = depth
         self.bufs = [{cid: tuple(torch.empty(tuple(t.shape), dtype=t.dtype, device=self.dev)
                                  for t in ts) for cid, ts in example_frame.items()}
@@ -225,15 +230,23 @@ class FrameUploader:
 
     def put(self, frame: Mapping) -> int:
         slot = self.n % self.depth
-        with torch.cuda.stream(self.stream):
+        streams = [self.stream] + self.extra
+        for st in streams:
             if self.free[slot] is not None:
-                self.stream.wait_event(self.free[slot])
-            for cid, ts in frame.items():
-                for dst, src in zip(self.bufs[slot][cid], ts):
+                st.wait_event(self.free[slot])
+        i = 0
+        for cid, ts in frame.items():
+            for dst, src in zip(self.bufs[slot][cid], ts):
+                with torch.cuda.stream(streams[i % len(streams)]):
                     dst.copy_(src, non_blocking=True)
-                    self.bytes += src.numel() * src.element_size()
-            ev = torch.cuda.Event()
-            ev.record(self.stream)
+                i += 1
+                self.bytes += src.numel() * src.element_size()
+        for st in self.extra:   # the ticket's event covers every lane
+            ev_l = torch.cuda.Event()
+            ev_l.record(st)
+            self.stream.wait_event(ev_l)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
         self.done[slot] = ev
         self.n += 1
         return self.n - 1
