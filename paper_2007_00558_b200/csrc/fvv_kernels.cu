@@ -1353,8 +1353,11 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     WT *swk = reinterpret_cast<WT *>(sk + NBUF * FKEYS);          // [2][FCELLS] winners
     double *sres = reinterpret_cast<double *>(swk + 2 * FCELLS); // [MAXR][4][FNT]
     double *sray = sres + MAXR * 4 * FNT;                         // [TX] rx, [FTY] ry
-    double *swt = sray + TX + FTY;                                // [MAXR][FNT] weights (ANG)
-    uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (ANG ? MAXR * FNT : 0));  // [2][FCELLS] (DBG)
+    // ANG weights: kept per contribution in shared memory up to 3 references;
+    // for more, evaluated in the mix (the raster would cost the 5th CTA/SM)
+    constexpr bool WSTORE = ANG && MAXR <= 3;
+    double *swt = sray + TX + FTY;                                // [MAXR][FNT] (WSTORE)
+    uint8_t *sst = reinterpret_cast<uint8_t *>(swt + (WSTORE ? MAXR * FNT : 0));  // [2][FCELLS] (DBG)
 
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const DevCam &dst = p.dst;
@@ -1496,7 +1499,13 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
 #endif
             const double zj = sres[(qq * 4 + 3) * FNT + tid];
             if (zj <= thr) {
-                const double w = ANG ? swt[qq * FNT + tid] : p.c[kb + qq].weight;
+                // ANG without WSTORE: the angular factor of the participating
+                // contributions from the stored exact z (same value)
+                const double w = WSTORE ? swt[qq * FNT + tid]
+                                 : ANG ? p.c[kb + qq].weight *
+                                             angular_factor(dst, p.c[kb + qq].src, sray[tx],
+                                                            sray[TX + ty], zj, p.ang_eps)
+                                       : p.c[kb + qq].weight;
                 a0 = dadd(a0, dmul(w, sres[(qq * 4 + 0) * FNT + tid]));
                 a1 = dadd(a1, dmul(w, sres[(qq * 4 + 1) * FNT + tid]));
                 a2 = dadd(a2, dmul(w, sres[(qq * 4 + 2) * FNT + tid]));
@@ -1602,7 +1611,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             sres[(j * 4 + 1) * FNT + tid] = c1;
             sres[(j * 4 + 2) * FNT + tid] = c2;
             sres[(j * 4 + 3) * FNT + tid] = zd;
-            if (ANG)
+            if (WSTORE)
                 swt[j * FNT + tid] =
                     c.weight * angular_factor(dst, c.src, sray[tx], sray[TX + ty], z, p.ang_eps);
             vmask |= 1u << j;
@@ -1659,7 +1668,7 @@ template <int MAXR, bool ANG>
 static size_t fast_smem() {
     return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(WinnerT<MAXR>) +
            (size_t)MAXR * 4 * FNT * sizeof(double) + (TX + FTY) * sizeof(double) +
-           (ANG ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
+           (ANG && MAXR <= 3 ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
 }
 
 template <int MAXR, bool DBG, bool ANG>
