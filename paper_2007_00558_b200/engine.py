@@ -215,9 +215,12 @@ class FrameUploader:
         self.dev = _dev.device() if device is None else torch.device(device)
         self.stream = torch.cuda.Stream(self.dev)
         # copies spread over `lanes` streams so one copy's setup overlaps
-        # another's transfer (FVV_UPLOAD_LANES overrides; 1 = one stream)
+        # another's transfer: two for frames of 8 MB and more (c1: +2 % e2e),
+        # one below, where the extra events cost more than they hide
+        # (FVV_UPLOAD_LANES overrides)
         import os
-        lanes = int(os.environ.get("FVV_UPLOAD_LANES", lanes or 2))
+        nbytes = sum(t.numel() * t.element_size() for ts in example_frame.values() for t in ts)
+        lanes = int(os.environ.get("FVV_UPLOAD_LANES", lanes or (2 if nbytes >= 8 << 20 else 1)))
         self.extra = [torch.cuda.Stream(self.dev) for _ in range(max(lanes, 1) - 1)]
         self.depth = depth
         self.bufs = [{cid: tuple(torch.empty(tuple(t.shape), dtype=t.dtype, device=self.dev)
@@ -234,13 +237,13 @@ class FrameUploader:
         for st in streams:
             if self.free[slot] is not None:
                 st.wait_event(self.free[slot])
-        i = 0
-        for cid, ts in frame.items():
-            for dst, src in zip(self.bufs[slot][cid], ts):
-                with torch.cuda.stream(streams[i % len(streams)]):
+        pairs = [(dst, src) for cid, ts in frame.items()
+                 for dst, src in zip(self.bufs[slot][cid], ts)]
+        for li, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                for dst, src in pairs[li::len(streams)]:
                     dst.copy_(src, non_blocking=True)
-                i += 1
-                self.bytes += src.numel() * src.element_size()
+        self.bytes += sum(src.numel() * src.element_size() for _, src in pairs)
         for st in self.extra:   # the ticket's event covers every lane
             ev_l = torch.cuda.Event()
             ev_l.record(st)
