@@ -380,7 +380,8 @@ int canvas_tensor_map(fvv_ctx *ctx, int n, int W, int H, int r, ResolveParams &r
         if (!enc) return fail(ctx, FVV_ECUDA, "cuTensorMapEncodeTiled unavailable");
         const cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)rows, (cuuint64_t)n};
         const cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)per * 8};
-        const cuuint32_t box[3] = {36, 12, 1};
+        // K3's key tile: the 32 x FTY tile plus a 2-cell ring
+        const cuuint32_t box[3] = {32 + 4, (cuuint32_t)resolve_tile_rows() + 4, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         const CUresult e = enc(&ctx->kmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, ctx->canvas, dims,
                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
