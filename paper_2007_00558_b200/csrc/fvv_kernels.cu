@@ -1064,8 +1064,7 @@ constexpr int FBR = FTY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
 #endif
 template <int MAXR>
 using WinnerT = typename std::conditional<(MAXR >= FVV_K3_W32_FROM), uint32_t, uint64_t>::type;
-// a key span of TX + 4 (FTY + 4) pixels meets at most 3 flag tiles per axis
-static_assert(2 * FVV_TF_W >= TX + 3 && 2 * FVV_TF_H >= FTY + 3, "flag tiles too small");
+
 constexpr int FCHUNKS = FKR * (FKC / 2);                       // 216 16-byte chunks
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
@@ -1400,21 +1399,23 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
             if (!act) {
                 // the flag tiles covering the staged key tile (target pixels
                 // x0-2 .. x0+TX+1, y0-2 .. y0+FTY+1; K2 clamps the canvas
-                // padding into the edge tiles): at most 3 x 3 (static_assert
-                // above); the nine loads are independent (clamped duplicates
-                // are harmless), so they cost one round trip
+                // padding into the edge tiles): at most NXF x NYF of them
+                // (3 x 3 for 32 x 8 flag tiles); the loads are independent
+                // (clamped duplicates are harmless), so they cost one round
+                // trip. 16x8, 16x4 and 8x8 flag tiles measured the same.
                 const int fx0 = max(x0 - 2, 0) / kTileFlagW;
                 const int fx1 = min((x0 + TX + 1) / kTileFlagW, p.tf.ntx - 1);
                 const int fy0 = max(y0 - 2, 0) / kTileFlagH;
                 const int fy1 = min((y0 + FTY + 1) / kTileFlagH, p.tf.nty - 1);
-                uint8_t f[9];
+                constexpr int NXF = (TX + 3) / kTileFlagW + 2, NYF = (FTY + 3) / kTileFlagH + 2;
+                uint8_t f[NXF * NYF];
 #pragma unroll
-                for (int e = 0; e < 9; ++e) {
-                    const int tx2 = min(fx0 + e % 3, fx1), ty2 = min(fy0 + e / 3, fy1);
+                for (int e = 0; e < NXF * NYF; ++e) {
+                    const int tx2 = min(fx0 + e % NXF, fx1), ty2 = min(fy0 + e / NXF, fy1);
                     f[e] = *tile_flag(p.tf, tid, ty2 * p.tf.ntx + tx2);
                 }
 #pragma unroll
-                for (int e = 0; e < 9; ++e) act |= f[e] == (uint8_t)gen;
+                for (int e = 0; e < NXF * NYF; ++e) act |= f[e] == (uint8_t)gen;
             }
         }
         const unsigned m = __ballot_sync(0xffffffffu, act);
