@@ -1056,6 +1056,8 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 constexpr int FTY = FVV_K3_TY, FNT = TX * FTY;                   // fast-path tile: 32 x FTY
 constexpr int FKR = FTY + 4, FKC = TX + 4, FKEYS = FKR * FKC;  // 12 x 36 (FTY = 8)
 constexpr int FBR = FTY + 2, FBC = TX + 2, FCELLS = FBR * FBC;  // 10 x 34
+// each key buffer is a TMA destination: 128-byte aligned (FTY = 4 or 8)
+static_assert(FKEYS * sizeof(uint64_t) % 128 == 0, "K3 key buffers must stay 128-byte aligned");
 // 32-bit winner cells from this many contributions per layer on (default:
 // always). They save 2.7 KB of shared memory, which keeps 5 CTAs/SM with a
 // 4-reference sres (c4: K3 1,078 -> 943 us) and trims K3 at c1 by 3 %.
