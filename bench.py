@@ -20,8 +20,12 @@ models + 100 MB of z canvases per step footprint > 126 MB L2).
   --impl reference   the CPU oracle port (oracle/) on the host cores, same
          workload, each step = one view per worker process
 
-Multi-GPU (torchrun): each rank renders its own views from frames staged on
-its own GPU (weak scaling, no collective in the timed region).
+Multi-GPU: ``--gpus N`` launches N ranks itself (torch.distributed.run on
+127.0.0.1) unless it already runs under torchrun. c0/c1 run N replicas; c2/c4
+shard the frame's views in contiguous blocks, the frame replicated by one
+NCCL broadcast per step on a comm stream overlapped with the previous frame's
+render; c3 shards the stream's frames round-robin, each rank generating only
+its own. Device time is the max over ranks (``rank_ms`` lists them all).
 """
 
 from __future__ import annotations
@@ -75,6 +79,9 @@ def parse():
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="launcher/sharding check without GPU work (CPU, gloo): every rank "
+                         "reports the views/frames it owns; rank 0 prints one JSON line")
     ap.add_argument("--gen", default="auto", choices=("auto", "host", "gpu"),
                     help="input generator: numpy ray caster on the host, or scenes_gpu in "
                          "HBM (auto: gpu for c3/c4, whose host generation takes minutes)")
@@ -92,7 +99,18 @@ def parse():
 # workload
 
 
+def my_frames(args):
+    """c3: the stream's frames this rank owns (round-robin)."""
+    from paper_2007_00558_b200.distributed import shard, world
+
+    rank, ws, _ = world()
+    n = max(args.frames, ws)
+    return n, shard(n, ws, rank, "cyclic")
+
+
 def build_workload(args):
+    """The config's rig, views and frames. c3: each rank ray-casts only the
+    frames it owns (``frames[i]`` is stream frame ``my_frames()[1][i]``)."""
     name = args.config
     if args.gen == "gpu":
         import torch
@@ -101,9 +119,9 @@ def build_workload(args):
 
         dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
         if name == "c3":
-            ws = int(os.environ.get("WORLD_SIZE", 1))
-            return scenes_gpu.make_workload("c3", seed=args.seed, n_frames=max(args.frames, ws),
-                                            dev=dev)
+            n, mine = my_frames(args)
+            return scenes_gpu.make_workload("c3", seed=args.seed, n_frames=n, dev=dev,
+                                            frame_ids=mine)
         return scenes_gpu.make_workload(name, seed=args.seed, n_views=args.views,
                                         cameras="all" if name in ("c2", "c4") else "refs",
                                         dev=dev)
@@ -114,8 +132,8 @@ def build_workload(args):
     elif name in ("c2", "c4"):
         wl = scenes.make_workload(name, seed=args.seed, n_views=args.views, cameras="all")
     else:
-        ws = int(os.environ.get("WORLD_SIZE", 1))
-        wl = scenes.make_workload("c3", seed=args.seed, n_frames=max(args.frames, ws))
+        n, mine = my_frames(args)
+        wl = scenes.make_workload("c3", seed=args.seed, n_frames=n, frame_ids=mine)
     return wl
 
 
@@ -326,6 +344,70 @@ def run_reference(args):
 # GPU arm
 
 
+def run_e2e(args, wl, eng, frames, views, dev, stream):
+    """``e2e``: the same metric through the public host-memory API,
+    ``engine.EdgeStream`` — every step's live inputs start in pinned host
+    memory (16-bit mm + validity sidecar + RGB of the step's reference
+    cameras), its rendered views end in pinned host memory; the H2D of step
+    s+1 and the D2H of step s-1 overlap step s (double-buffered, the device
+    output buffers rotate so a view is never overwritten while downloaded)."""
+    import torch
+
+    from paper_2007_00558_b200 import distributed as D
+    from paper_2007_00558_b200.engine import EdgeStream
+
+    def pinned(a):
+        a = host_array(a)
+        return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory()
+
+    # at most 8 distinct host frames rotate (c3's 300 would pin 11 GB)
+    host = [{cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm, fr[cid].validity))
+             for cid in fr} for fr in frames[:8]]
+
+    def step_views(s):
+        # c3: the e2e run cycles over the frames that have host copies
+        return views[s % len(host)] if args.config == "c3" else views[0]
+
+    def step_frame(s):
+        need = sorted({c for v in step_views(s) for c in wl.refs[v]})
+        return {cid: host[s % len(host)][cid] for cid in need}
+
+    es = EdgeStream(eng, max(len(v) for v in views), depth=2)
+
+    def run(start, n):
+        nv_ = 0
+        for s in range(start, start + n):
+            vi = step_views(s)
+            es.submit(step_frame(s), [wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi])
+            nv_ += len(vi)
+        es.dl.wait_into(stream)
+        return nv_
+
+    run(0, args.warmup)
+    es.flush()
+    torch.cuda.synchronize()
+    D.barrier()
+    b0, d0 = es.h2d_bytes, es.d2h_bytes
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for up in es.ups.values():
+        up.stream.wait_event(e0)
+    es.dl.stream.wait_event(e0)
+    nv2 = run(args.warmup, args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    es.flush()
+    ms2 = D.max_over_ranks(e0.elapsed_time(e1))
+    return {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
+            "h2d_bytes_per_step": (es.h2d_bytes - b0) // args.steps,
+            "d2h_bytes_per_step": (es.d2h_bytes - d0) // args.steps,
+            "api": "engine.EdgeStream.submit: pinned H2D (FrameUploader, two copy streams) -> "
+                   "EdgeRenderer.ingest_mm_many + render (C ABI fvv_slots_ingest_mm, "
+                   "fvv_render_views) -> D2H (ResultDownloader, rotating device buffers), "
+                   "double-buffered",
+            "ms_per_step": ms2 / args.steps}
+
+
 def run_ours(args):
     import torch
 
@@ -360,9 +442,10 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     if args.config == "c3":
-        # frames sharded round-robin over ranks; view f is rendered from frame f
-        mine = D.shard(len(wl.frames), ws, rank, "cyclic")
-        frames = [wl.frames[f] for f in mine]
+        # frames sharded round-robin over ranks (each rank generated only its
+        # own); view f is rendered from frame f
+        _, mine = my_frames(args)
+        frames = list(wl.frames)
         views = [[f] for f in mine]
     else:
         frames = frame_variants(wl, args.frames, args.seed + 1)
@@ -407,18 +490,42 @@ def run_ours(args):
     out = outs[0]
 
     bcast = ws > 1 and args.config in ("c2", "c4")
+    # the live MVD frame arrives at rank 0; one NCCL broadcast of its packed
+    # buffer replicates it over NVLink (the path's only exchange). It runs on
+    # a comm stream: frame k+1's broadcast overlaps frame k's render, which
+    # waits only for its own frame's broadcast (event); a frame's buffer is
+    # re-filled only after the render that read it (event).
+    comm = torch.cuda.Stream(dev) if bcast else None
+    landed, read_done = {}, {}
+    if bcast and len(staged) < 2:
+        raise SystemExit("c2/c4 multi-GPU needs --frames >= 2 (broadcast double buffering)")
+
+    def issue_broadcast(fi):
+        if fi in read_done:
+            comm.wait_event(read_done.pop(fi))
+        with torch.cuda.stream(comm):
+            D.broadcast_frame([flats[fi]])
+            ev = torch.cuda.Event()
+            ev.record(comm)
+        landed[fi] = ev
 
     def run_step(s, e, o):
         fi = s % len(staged)
         vi = views[s % len(views)] if args.config == "c3" else views[0]
         fr = staged[fi]
+        cur = torch.cuda.current_stream(dev)
         if bcast:
-            # the live MVD frame arrives at rank 0; one NCCL broadcast of its
-            # packed buffer replicates it over NVLink (the path's only exchange)
-            D.broadcast_frame([flats[fi]])
+            if fi not in landed:
+                issue_broadcast(fi)
+            cur.wait_event(landed.pop(fi))
+            issue_broadcast((s + 1) % len(staged))
         need = sorted({c for v in vi for c in wl.refs[v]})
         e.ingest_mm_many({cid: fr[cid] for cid in need}, hole_closing=True)
         e.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=o)
+        if bcast:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            read_done[fi] = ev
         return len(vi)
 
     def step(s):
@@ -451,7 +558,8 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     D.barrier()
     clk = clocks.stop() if clocks else None
-    ms_max = D.max_over_ranks(ms)
+    rank_ms = D.gather_over_ranks(ms)
+    ms_max = max(rank_ms)
     total_views = D.sum_over_ranks(nviews)
     value = total_views / (ms_max / 1e3)
 
@@ -463,92 +571,10 @@ def run_ours(args):
     prof = eng.ctx.profile_read()
     eng.ctx.profile(False)
 
-    # e2e: public API with host buffers. Every step's live inputs start in
-    # pinned host memory and its rendered views end in pinned host memory;
-    # FrameUploader / ResultDownloader (engine.py) run those copies on their
-    # own streams, double-buffered, so the H2D of step s+1 overlaps step s.
+    # e2e: public API with host buffers (run_e2e)
     e2e = None
     if not args.no_e2e:
-        from paper_2007_00558_b200.engine import FrameUploader, ResultDownloader
-
-        def step_views(s):
-            # c3: the e2e run cycles over the frames that have host copies
-            return views[s % len(host)] if args.config == "c3" else views[0]
-
-        def step_cams(s):
-            return sorted({c for v in step_views(s) for c in wl.refs[v]})
-
-        def pinned(a):
-            a = host_array(a)
-            return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory()
-
-        # at most 8 distinct host frames rotate (c3's 300 would pin 11 GB)
-        host = []
-        for fr in frames[:8]:
-            host.append({cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm,
-                                                        fr[cid].validity))
-                         for cid in fr})
-
-        def host_frame(s):
-            fr = host[s % len(host)]
-            return {cid: fr[cid] for cid in step_cams(s)}
-
-        if args.config == "c3":
-            # frames carry different camera sets: one uploader per camera set
-            ups = {}
-            for s in range(len(host)):
-                key = tuple(step_cams(s))
-                if key not in ups:
-                    ups[key] = FrameUploader(host_frame(s), depth=2, device=dev)
-            uploader_for = lambda s: ups[tuple(step_cams(s))]  # noqa: E731
-        else:
-            up0 = FrameUploader(host_frame(0), depth=2, device=dev)
-            uploader_for = lambda s: up0  # noqa: E731
-        dl = ResultDownloader(out.shape, depth=2, device=dev)
-
-        def e2e_run(start, n):
-            nv_ = 0
-            ticket = uploader_for(start).put(host_frame(start))
-            for s in range(start, start + n):
-                nxt = uploader_for(s + 1).put(host_frame(s + 1)) if s + 1 < start + n else None
-                up = uploader_for(s)
-                fr = up.get(ticket)
-                vi = step_views(s)
-                eng.ingest_mm_many({cid: fr[cid] for cid in step_cams(s)}, hole_closing=True)
-                eng.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=out)
-                up.release(ticket)
-                dl.put(out[:len(vi)])
-                nv_ += len(vi)
-                ticket = nxt
-            dl.wait_into(stream)
-            return nv_
-
-        e2e_run(0, args.warmup)
-        torch.cuda.synchronize()
-        D.barrier()
-        ups_all = set(map(id, [uploader_for(s) for s in range(len(host))]))
-        b0 = sum(u.bytes for u in {id(uploader_for(s)): uploader_for(s)
-                                    for s in range(len(host))}.values())
-        d0 = dl.bytes
-        e0.record(stream)
-        for s in range(len(host)):
-            uploader_for(s).stream.wait_event(e0)
-        dl.stream.wait_event(e0)
-        nv2 = e2e_run(args.warmup, args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        b1 = sum(u.bytes for u in {id(uploader_for(s)): uploader_for(s)
-                                    for s in range(len(host))}.values())
-        ms2 = D.max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
-               "h2d_bytes_per_step": (b1 - b0) // args.steps,
-               "d2h_bytes_per_step": (dl.bytes - d0) // args.steps,
-               "api": "FrameUploader (pinned H2D, two copy streams) -> EdgeRenderer.ingest_mm_many + "
-                      "render (C ABI fvv_slots_ingest_mm, fvv_render_views) -> "
-                      "ResultDownloader (D2H, copy stream), double-buffered",
-               "ms_per_step": ms2 / args.steps}
-        del ups_all
-
+        e2e = run_e2e(args, wl, eng, frames, views, dev, stream)
     if rank != 0:
         return 0
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
@@ -607,7 +633,8 @@ def run_ours(args):
     pipe = value / ws * b_view / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "ms_per_view":
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "rank_ms": rank_ms, "rank_views": D.gather_over_ranks(nviews), "ms_per_view":
             ms_max / max(nviews, 1), "higher_is_better": True, "scaling": "weak",
         # 30 ms max synthesis time, 1080p, 3 refs
         "vs_baseline": (value / ws) / (1000.0 / 30.0) if args.config == "c1" else None, "dtype": "f64", "data": "synthetic",
@@ -640,10 +667,60 @@ def run_ours(args):
     return 0
 
 
+def self_launch(args) -> int:
+    """``--gpus N`` without a torchrun environment: launch N ranks (one
+    process per GPU) with torch.distributed.run on 127.0.0.1, exactly as the
+    driver's scaling run does; rank 0's JSON line is this run's output."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_launch_check(args) -> int:
+    """Ranks, world size and the work each rank owns, without any GPU work
+    (tests/test_host.py runs it on CPU with gloo)."""
+    from paper_2007_00558_b200 import distributed as D
+
+    rank, ws, local = D.init("gloo")
+    if args.config == "c3":
+        n, mine = my_frames(args)
+        unit = "frames"
+    else:
+        wl = scenes.make_workload(args.config, seed=args.seed, n_views=args.views,
+                                  render_frames=False)
+        n = len(wl.virtuals)
+        mine = D.shard(n, ws, rank) if args.config in ("c2", "c4") else list(range(n))
+        unit = "views"
+    owned = D.gather_over_ranks(float(len(mine)))
+    first = D.gather_over_ranks(float(mine[0]) if mine else -1.0)
+    ranks = D.gather_over_ranks(float(rank))
+    D.barrier()
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": ws, "ranks": [int(r) for r in ranks],
+                          "config": args.config, "unit": unit, "total": n,
+                          f"{unit}_per_rank": [int(x) for x in owned],
+                          "first_per_rank": [int(x) for x in first]}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1 and args.impl == "ours":
+        return self_launch(args)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
+    if args.launch_check:
+        return run_launch_check(args)
     return run_ours(args)
 
 

@@ -277,6 +277,9 @@ int fvv_rle_encode(fvv_ctx *ctx, const uint8_t *flat, int64_t n, int64_t *starts
  * The edge server keeps a slot per rig camera: its calibration, its static
  * BG model (uploaded once, pipeline.py:445) and its latest live frame. */
 int fvv_slot_set_camera(fvv_ctx *ctx, int32_t slot, const fvv_camera *cam);
+/* Forget a slot's BG model and live frame (a renderer taking over a slot
+ * must supply both again before rendering from it: "missing inputs"). */
+int fvv_slot_reset(fvv_ctx *ctx, int32_t slot);
 int fvv_slot_set_bg(fvv_ctx *ctx, int32_t slot, const float *bg_depth,
                     const uint8_t *bg_validity);
 /* Live frame from f32 depth + validity (MvdFrame / DepthFrame); hole_closing

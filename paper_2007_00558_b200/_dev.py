@@ -47,3 +47,19 @@ def ptr(t) -> int | None:
 def host(t: torch.Tensor, dtype=None) -> np.ndarray:
     a = t.cpu().numpy()
     return a.view(dtype) if dtype is not None else a
+
+
+def check_out(t, dtype, what: str, shape=None, dev: int | None = None) -> None:
+    """An output tensor the library writes: CUDA, ``dtype``, contiguous, and
+    (when given) exactly ``shape``; else ValueError before any kernel runs."""
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise ValueError(f"{what} must be a CUDA tensor")
+    want = device() if dev is None else torch.device("cuda", dev)
+    if t.device != want:
+        raise ValueError(f"{what} is on {t.device}, the renderer on {want}")
+    if t.dtype != dtype:
+        raise ValueError(f"{what} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what} has shape {tuple(t.shape)}, expected {tuple(shape)}")

@@ -39,7 +39,7 @@ EXPORTS = (
     "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode", "fvv_slots_ingest_mm",
     "fvv_set_range_weights", "fvv_rice_stream_bound", "fvv_rice_encode_plane",
     "fvv_rice_decode_plane", "fvv_rice_decode_planes", "fvv_encode_mm", "fvv_rle_decode",
-    "fvv_rle_encode",
+    "fvv_rle_encode", "fvv_slot_reset",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -97,6 +97,7 @@ _SIGS = {
                       C.c_int),
     "fvv_slot_set_camera": ([_VP, _I32, C.POINTER(FvvCamera)], C.c_int),
     "fvv_slot_set_bg": ([_VP, _I32, _VP, _VP], C.c_int),
+    "fvv_slot_reset": ([_VP, _I32], C.c_int),
     "fvv_slot_ingest": ([_VP, _I32, _VP, _VP, _VP, _I32], C.c_int),
     "fvv_slot_ingest_mm": ([_VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP], C.c_int),
     "fvv_slot_ingest_yuv": ([_VP, _I32, _VP, _VP, _VP, _VP, _D, _D, _I32, _VP, _VP], C.c_int),
@@ -212,7 +213,22 @@ class Context:
         self.h = h
         self.device = int(device)
         self._range_sigma = None
+        self._free_slots = list(range(MAX_SLOTS))
         self.range_weights(_DEFAULT_SIGMA_RANGE)
+
+    def alloc_slots(self, n: int):
+        """Reserve ``n`` camera slots of this context (lowest free ids), or
+        None when fewer than ``n`` are free. Renderers sharing a context hold
+        disjoint slots, so one never renders another's frames."""
+        with _lock:
+            if n > len(self._free_slots):
+                return None
+            got, self._free_slots = self._free_slots[:n], self._free_slots[n:]
+            return got
+
+    def free_slots(self, slots) -> None:
+        with _lock:
+            self._free_slots = sorted(set(self._free_slots) | set(slots))
 
     def range_weights(self, sigma_range: float) -> None:
         """Make K1's resident range-weight table the np.exp one for sigma_range."""

@@ -190,10 +190,13 @@ int slot_alloc(fvv_ctx *ctx, Slot &s, const fvv_camera &cam) {
 int slot_camera(fvv_ctx *ctx, Slot &s, const fvv_camera &cam) {
     if (s.has_cam && memcmp(&s.cam, &cam, sizeof(cam)) == 0) return FVV_OK;
     if (s.has_cam && s.cam.width == cam.width && s.cam.height == cam.height) {
-        // same size: only the calibration changed; keep buffers, refresh rays
+        // same size: only the calibration changed; keep buffers, refresh
+        // rays. The slot's BG model and live frame belonged to the old
+        // calibration: a render now needs new ones ("missing inputs").
         s.cam = cam;
         s.dev = to_dev(cam);
         LAUNCH(launch_rays(s.dev, s.rays, s.rays + cam.width, ctx->stream));
+        s.has_bg = s.has_frame = false;
         return FVV_OK;
     }
     return slot_alloc(ctx, s, cam);
@@ -1012,6 +1015,14 @@ int fvv_slot_set_camera(fvv_ctx *ctx, int32_t slot, const fvv_camera *cam) {
     if (slot < 0 || slot >= FVV_MAX_SLOTS) return fail(ctx, FVV_EINVAL, "slot %d out of range", slot);
     if ((rc = check_cam(ctx, cam, "slot"))) return rc;
     return slot_camera(ctx, ctx->slots[slot], *cam);
+}
+
+int fvv_slot_reset(fvv_ctx *ctx, int32_t slot) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (slot < 0 || slot >= FVV_MAX_SLOTS) return fail(ctx, FVV_EINVAL, "slot %d out of range", slot);
+    ctx->slots[slot].has_bg = ctx->slots[slot].has_frame = false;
+    return FVV_OK;
 }
 
 int fvv_slot_set_bg(fvv_ctx *ctx, int32_t slot, const float *bg_depth, const uint8_t *bg_validity) {

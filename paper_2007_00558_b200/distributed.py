@@ -105,6 +105,18 @@ def sum_over_ranks(value: float) -> float:
     return float(t.item())
 
 
+def gather_over_ranks(value: float) -> List[float]:
+    """``value`` of every rank, in rank order (a list of one without a group)."""
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(value)]
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
 def barrier() -> None:
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()

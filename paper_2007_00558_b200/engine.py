@@ -35,25 +35,61 @@ class EdgeRenderer:
                  private: bool = False):
         """``private=True`` gives the renderer its own library context (own
         slots, canvases and stream binding), so several renderers can work on
-        different frames concurrently on different CUDA streams; the default
-        shares the device's context."""
-        if private:
-            import torch
-
-            self.ctx = _native.Context(torch.cuda.current_device() if device is None else device)
-        else:
-            self.ctx = _native.context(device)
+        different frames concurrently on different CUDA streams. The default
+        shares the device's context (and its z canvases) but reserves its own
+        camera slots in it, so renderers never see each other's frames; when
+        the shared context has too few free slots, a private one is made."""
         self.cfg = cfg or SynthesisConfig()
         self.rig = list(rig)
         self.by_id = {c.id: c for c in self.rig}
+        if len(self.by_id) != len(self.rig):
+            raise ValueError("camera ids of the rig must be unique")
         if len(self.rig) > _native.MAX_SLOTS:
             raise ValueError(f"at most {_native.MAX_SLOTS} cameras per renderer")
-        self.slot = {c.id: i for i, c in enumerate(self.rig)}
+        dev = torch.cuda.current_device() if device is None else device
+        slots = None
+        if not private:
+            self.ctx = _native.context(dev)
+            slots = self.ctx.alloc_slots(len(self.rig))
+        if slots is None:
+            self.ctx = _native.Context(dev)
+            slots = self.ctx.alloc_slots(len(self.rig))
+        self._slots = slots
+        self.slot = {c.id: s for c, s in zip(self.rig, slots)}
         for c in self.rig:
             self.ctx.call("fvv_slot_set_camera", self.slot[c.id], C.byref(_native.camera(c)))
+            self.ctx.call("fvv_slot_reset", self.slot[c.id])
         self.ingested = set()
         for cid, bg in (bg_models or {}).items():
             self.set_bg_model(cid, bg)
+
+    def close(self) -> None:
+        """Give the renderer's camera slots back to its context."""
+        slots, self._slots = getattr(self, "_slots", None), None
+        if slots:
+            self.ctx.free_slots(slots)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- argument checks (the kernels read/write W*H elements of the slot's
+    # calibration: a short raster must fail here, as ValueError, like the
+    # reference's frame validation, core.py:96-126)
+
+    def _hw(self, cid):
+        k = self.by_id[cid].intrinsics
+        return int(k.height), int(k.width)
+
+    def _check(self, a, cid, what: str, channels: Optional[int] = None):
+        H, W = self._hw(cid)
+        shape = (H, W) if channels is None else (H, W, channels)
+        got = tuple(getattr(a, "shape", np.shape(a)))
+        if got != shape:
+            raise ValueError(f"camera {cid}: {what} has shape {got}, its calibration needs {shape}")
+        return a
 
     def _bind(self):
         self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
@@ -68,8 +104,11 @@ class EdgeRenderer:
     def set_bg_model(self, cid, depth, validity=None) -> None:
         """Static background depth model of camera ``cid`` (DepthFrame or arrays)."""
         self._bind()
+        self._slot(cid)
         if validity is None:
             depth, validity = depth.depth, depth.validity
+        self._check(depth, cid, "background depth")
+        self._check(validity, cid, "background validity")
         d = _dev.upload(depth, np.float32)
         v = _dev.upload(validity, np.uint8)
         self.ctx.call("fvv_slot_set_bg", self._slot(cid), d.data_ptr(), v.data_ptr())
@@ -77,6 +116,10 @@ class EdgeRenderer:
     def ingest(self, cid, color, depth, hole_closing: bool = True) -> None:
         """Live ColorFrame + DepthFrame of camera ``cid`` (pipeline.py:514-524)."""
         self._bind()
+        self._slot(cid)
+        self._check(getattr(color, "pixels", color), cid, "colour", 3)
+        self._check(depth.depth, cid, "depth")
+        self._check(depth.validity, cid, "validity")
         rgb = _dev.upload(getattr(color, "pixels", color), np.uint8)
         d = _dev.upload(depth.depth, np.float32)
         v = _dev.upload(depth.validity, np.uint8)
@@ -90,6 +133,16 @@ class EdgeRenderer:
         """Live frame as the 16-bit mm raster + validity sidecar (mvdio.py:132):
         mm decode + ingest (K0), then the bilateral hole fill (K1)."""
         self._bind()
+        self._slot(cid)
+        self._check(rgb, cid, "colour", 3)
+        self._check(mm, cid, "mm raster")
+        if validity is not None:
+            self._check(validity, cid, "validity")
+        for o, what in ((depth_out, "depth_out"), (validity_out, "validity_out")):
+            if o is not None:
+                self._check(o, cid, what)
+                _dev.check_out(o, torch.float32 if what == "depth_out" else torch.uint8, what,
+                               dev=self.ctx.device)
         rgb_t = _dev.upload(rgb, np.uint8)
         mm_t = _dev.upload(mm, np.uint16)
         v_t = None if validity is None else _dev.upload(validity, np.uint8)
@@ -110,6 +163,11 @@ class EdgeRenderer:
             return
         keep = []
         for cid, (rgb, mm, val) in items:
+            self._slot(cid)
+            self._check(rgb, cid, "colour", 3)
+            self._check(mm, cid, "mm raster")
+            if val is not None:
+                self._check(val, cid, "validity")
             keep.append((_dev.upload(rgb, np.uint8), _dev.upload(mm, np.uint16),
                          None if val is None else _dev.upload(val, np.uint8)))
         arr = C.c_void_p * n
@@ -122,6 +180,14 @@ class EdgeRenderer:
     def ingest_yuv(self, cid, rgb, y, u, v, depth_range, hole_closing: bool = True) -> None:
         """Live frame as the 12-bit YUV420 depth raster (pipeline.py:469-472)."""
         self._bind()
+        self._slot(cid)
+        H, W = self._hw(cid)
+        self._check(rgb, cid, "colour", 3)
+        self._check(y, cid, "Y plane")
+        for a, what in ((u, "U plane"), (v, "V plane")):
+            if tuple(np.shape(a) if not hasattr(a, "shape") else a.shape) != (H // 2, W // 2):
+                raise ValueError(f"camera {cid}: {what} has shape {tuple(a.shape)}, its "
+                                 f"calibration needs {(H // 2, W // 2)}")
         t = [_dev.upload(a, np.uint8) for a in (rgb, y, u, v)]
         self.ctx.call("fvv_slot_ingest_yuv", self._slot(cid), *[x.data_ptr() for x in t],
                       float(depth_range.z_near), float(depth_range.z_far),
@@ -172,8 +238,14 @@ class EdgeRenderer:
         refs, weights = self.plan(virtuals, refs)
         n, k = len(virtuals), len(refs[0])
         W, H = int(virtuals[0].intrinsics.width), int(virtuals[0].intrinsics.height)
+        if any((int(v.intrinsics.width), int(v.intrinsics.height)) != (W, H) for v in virtuals):
+            raise ValueError("every view of a batch needs the same image size")
         if out is None:
             out = _dev.empty((n, H, W, 3), np.uint8)
+        else:
+            _dev.check_out(out, torch.uint8, "out", (n, H, W, 3), self.ctx.device)
+        if provenance is not None:
+            _dev.check_out(provenance, torch.uint8, "provenance", (n, H, W), self.ctx.device)
         cams = (_native.FvvCamera * n)(*[_native.camera(v) for v in virtuals])
         slots = (C.c_int32 * (n * k))(*[self.slot[c] for r in refs for c in r])
         wts = (C.c_double * (n * k))(*[w for ws in weights for w in ws])
@@ -191,11 +263,32 @@ class EdgeRenderer:
         return ColorFrame(W, H, img[0].cpu().numpy())
 
 
+_SESSION: list = []   # [(key, pinned objects, renderer)] of the last synthesize() call
+
+
+def _session_key(rig, bg_models, cfg):
+    cams = tuple((c.id, bytes(_native.camera(c))) for c in rig)
+    return cams, tuple((cid, id(bg)) for cid, bg in sorted(bg_models.items())), cfg
+
+
 def synthesize(virtual_camera, mvd_frame: Mapping, refs=None, cfg: Optional[SynthesisConfig] = None,
                *, rig: Sequence, bg_models: Mapping, hole_closing: bool = True) -> ColorFrame:
     """North-star convenience call: ``mvd_frame`` maps camera id -> MvdFrame;
-    ``refs=None`` selects ``cfg.reference_count`` nearest cameras."""
-    r = EdgeRenderer(rig, bg_models, cfg)
+    ``refs=None`` selects ``cfg.reference_count`` nearest cameras.
+
+    Consecutive calls with the same rig, the same BG-model objects and the
+    same config reuse one session (resident slots, BG models uploaded once,
+    pipeline.py:445); the held BG objects keep their ids from being reused."""
+    cfg = cfg or SynthesisConfig()
+    key = _session_key(rig, bg_models, cfg)
+    if _SESSION and _SESSION[0][0] == key:
+        r = _SESSION[0][2]
+    else:
+        if _SESSION:
+            _SESSION.pop()[2].close()
+        r = EdgeRenderer(rig, bg_models, cfg)
+        _SESSION.append((key, (list(rig), dict(bg_models)), r))
+    r.ingested = set()
     return r.synthesize(virtual_camera, mvd_frame, refs, hole_closing=hole_closing)
 
 
@@ -205,7 +298,9 @@ class FrameUploader:
     ``put(frame)`` enqueues the pinned-host -> HBM copies of one frame
     (``{cam_id: (rgb u8 HxWx3, mm int16/uint16 HxW, validity u8 HxW)}``) on a
     dedicated stream and returns a ticket; ``get(ticket)`` makes the current
-    (compute) stream wait for those copies and returns the device tensors.
+    (compute) stream wait for those copies and returns the device tensors;
+    ``release(ticket)`` marks the point on the compute stream after which the
+    buffers may be overwritten by the copy ``depth`` puts later.
     With ``depth`` >= 2 the upload of frame t+1 overlaps the synthesis of
     frame t, so a PCIe-fed edge server is bounded by the link, not by
     copy + compute in series.
@@ -267,38 +362,138 @@ class FrameUploader:
 
 
 class ResultDownloader:
-    """Device -> pinned-host copies of rendered views on a separate stream."""
+    """Device -> pinned-host copies of rendered views on a separate stream.
 
-    def __init__(self, shape, depth: int = 2, device=None):
+    Render into ``next_buffer()`` (the current stream first waits until the
+    download that last read that device buffer is finished, so a view is
+    never overwritten while it is being copied out — the displayed frame of
+    pipeline.py:546-547,762-763), then ``put`` it. Host results rotate over
+    ``depth`` pinned buffers: ``on_done(host_view, tag)`` is called for each
+    result once its copy has finished (before its host buffer is reused, or
+    at ``flush``).
+    """
+
+    def __init__(self, shape, depth: int = 2, device=None, on_done=None):
         self.dev = _dev.device() if device is None else torch.device(device)
         self.stream = torch.cuda.Stream(self.dev)
         self.host = [torch.empty(tuple(shape), dtype=torch.uint8).pin_memory()
                      for _ in range(depth)]
+        self.bufs = [torch.empty(tuple(shape), dtype=torch.uint8, device=self.dev)
+                     for _ in range(depth)]
         self.depth = depth
         self.n = 0
         self.bytes = 0
-        self.events = [None] * depth
+        self.copied = [None] * depth       # D2H of the slot's device + host buffers done
+        self.pending = [None] * depth      # (host view, tag) not yet handed to on_done
+        self.on_done = on_done
 
-    def put(self, views: torch.Tensor) -> torch.Tensor:
-        """Queue the copy of ``views`` (after the current stream's work);
-        returns the pinned host tensor it lands in (valid after ``sync``)."""
+    def next_buffer(self) -> torch.Tensor:
+        """The device buffer the next ``put`` downloads; safe to write on the
+        current stream from now on."""
         slot = self.n % self.depth
+        if self.copied[slot] is not None:
+            torch.cuda.current_stream(self.dev).wait_event(self.copied[slot])
+        return self.bufs[slot]
+
+    def _retire(self, slot) -> None:
+        if self.copied[slot] is not None:
+            self.copied[slot].synchronize()
+        if self.pending[slot] is not None:
+            view, tag = self.pending[slot]
+            self.pending[slot] = None
+            if self.on_done is not None:
+                self.on_done(view, tag)
+
+    def put(self, views: torch.Tensor, tag=None) -> torch.Tensor:
+        """Queue the copy of ``views`` (after the current stream's work);
+        returns the pinned host tensor it lands in (valid once the copy is
+        done: ``on_done``, ``flush``, or ``depth`` puts later). ``views`` not
+        taken from ``next_buffer()``: the current stream waits for the copy
+        before running anything else, so it cannot be overwritten early."""
+        slot = self.n % self.depth
+        self._retire(slot)                 # host slot about to be reused
+        cur = torch.cuda.current_stream(self.dev)
         ready = torch.cuda.Event()
-        ready.record(torch.cuda.current_stream(self.dev))
+        ready.record(cur)
+        own = views.untyped_storage().data_ptr() == self.bufs[slot].untyped_storage().data_ptr()
         with torch.cuda.stream(self.stream):
-            if self.events[slot] is not None:
-                self.events[slot].synchronize()
             self.stream.wait_event(ready)
             dst = self.host[slot][:views.shape[0]]
             dst.copy_(views, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.stream)
-        self.events[slot] = ev
+        if not own:
+            views.record_stream(self.stream)
+            cur.wait_event(ev)
+        self.copied[slot] = ev
+        self.pending[slot] = (dst, tag)
         self.bytes += views.numel()
         self.n += 1
         return dst
 
+    def flush(self) -> None:
+        """Wait for every queued download and hand the results to on_done."""
+        for i in range(self.n - self.depth, self.n):
+            if i >= 0:
+                self._retire(i % self.depth)
+
     def wait_into(self, stream) -> None:
-        for ev in self.events:
+        for ev in self.copied:
             if ev is not None:
                 stream.wait_event(ev)
+
+
+class EdgeStream:
+    """The edge server fed from host memory (the e2e path of bench.py):
+    frames of pinned host rasters in, rendered views in pinned host memory
+    out, with the H2D copies of frame t+1 and the D2H copy of view t-1
+    overlapping frame t's decode/fill/warp/resolve on the renderer's stream.
+
+    ``submit(frame, virtuals, refs)`` takes ``{cam_id: (rgb, mm, validity)}``
+    (the 16-bit mm raster + validity sidecar, mvdio.py:132) and runs one
+    render tick (pipeline.py:514-547): upload, ``ingest_mm_many`` (K0 + K1),
+    ``render`` (K2 + K3), download. ``on_view(host_views, tag)`` receives each
+    tick's views once they are in host memory (pipeline.py:762-763
+    ``on_display``); ``flush()`` drains the last ones.
+    """
+
+    def __init__(self, renderer: "EdgeRenderer", max_views: int, depth: int = 2,
+                 on_view=None, hole_closing: bool = True):
+        self.r = renderer
+        dev = torch.device("cuda", renderer.ctx.device)
+        self.dev = dev
+        k = renderer.rig[0].intrinsics
+        self.dl = ResultDownloader((max_views, int(k.height), int(k.width), 3), depth, dev,
+                                   on_done=on_view)
+        self.depth = depth
+        self.ups = {}
+        self.hole_closing = hole_closing
+
+    def _uploader(self, frame):
+        key = tuple((cid, tuple(tuple(t.shape) for t in ts)) for cid, ts in sorted(frame.items()))
+        up = self.ups.get(key)
+        if up is None:
+            up = self.ups[key] = FrameUploader(dict(sorted(frame.items())), self.depth, self.dev)
+        return up
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(u.bytes for u in self.ups.values())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.dl.bytes
+
+    def submit(self, frame: Mapping, virtuals: Sequence, refs=None, tag=None) -> torch.Tensor:
+        up = self._uploader(frame)
+        ticket = up.put(dict(sorted(frame.items())))
+        fr = up.get(ticket)
+        self.r.ingest_mm_many(fr, hole_closing=self.hole_closing)
+        n = len(virtuals)
+        out = self.dl.next_buffer()[:n]
+        self.r.render(virtuals, refs, out=out)
+        up.release(ticket)
+        return self.dl.put(out, tag)
+
+    def flush(self) -> None:
+        self.dl.flush()

@@ -9,8 +9,7 @@ What is rebound:
 
 * ``fvv.synthesis`` — every public name of :mod:`paper_2007_00558_b200.synthesis`
   (synthesize_view, synthesize_view_debug, warp_layer, mix_layer, composite,
-  view_psnr, border_mask, the config/contribution types); the reference's
-  ``write_debug_bundle`` (disk I/O, out of scope) is kept;
+  write_debug_bundle, view_psnr, border_mask, the config/contribution types);
 * ``fvv.pipeline.synthesis`` — the module global ``EdgeServer.render_tick``
   reaches through ``synthesize_with_config`` (pipeline.py:546, 569-570);
 * ``fvv.depthproc.bilateral_close_holes`` (called at pipeline.py:518-519);
@@ -37,7 +36,8 @@ import types
 
 _OVERRIDE = ("SynthesisConfig", "LayerContribution", "MergedLayer", "CameraStreamInputs",
              "DebugBundle", "warp_layer", "mix_layer", "composite", "synthesize_view",
-             "synthesize_view_debug", "view_psnr", "border_mask", "LAYER_FG", "LAYER_BG")
+             "synthesize_view_debug", "write_debug_bundle", "view_psnr", "border_mask",
+             "LAYER_FG", "LAYER_BG")
 installed = {}
 
 
@@ -75,6 +75,9 @@ def install() -> types.ModuleType:
         for name in ("unpack_yuv420", "dequantize12", "quantize12", "pack_yuv420",
                      "encode_lossless", "decode_lossless"):
             setattr(ref_codec, name, getattr(ours_codec, name))
+        # one byte-codec registry: codecs registered through either module
+        # (depthcodec.register_codec, depthcodec.py:416-421) serve both
+        ours_codec._COMPRESSORS = ref_codec._COMPRESSORS
     if os.environ.get("FVV_SHIM_MVDIO") == "1":
         import fvv.mvdio as ref_mvd
 
@@ -88,5 +91,21 @@ def install() -> types.ModuleType:
     return mod
 
 
+def launches() -> int:
+    """GPU kernels launched so far by this process's library contexts."""
+    from . import _native
+
+    return sum(c.launches() for c in _native._contexts.values())
+
+
 def pytest_configure(config):  # pragma: no cover - exercised through pytest -p
     install()
+
+
+def pytest_unconfigure(config):  # pragma: no cover - exercised through pytest -p
+    # FVV_SHIM_REPORT=<path>: record how many kernels the run launched, the
+    # evidence that the reference's tests exercised the GPU backend
+    path = os.environ.get("FVV_SHIM_REPORT")
+    if path:
+        with open(path, "w") as fh:
+            fh.write(f"{launches()}\n")

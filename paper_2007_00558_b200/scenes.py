@@ -241,33 +241,61 @@ def _random_in_view(rng, anchor: np.ndarray, d_lo: float, d_hi: float, hspan: fl
     return anchor + d * direction
 
 
+def _rig_clearance(c: np.ndarray, arc_radius: float) -> float:
+    """Distance from ``c`` to the circle the rig's cameras sit on (radius
+    ``arc_radius`` around the world y axis, at y = 0)."""
+    return math.hypot(math.hypot(c[0], c[2]) - arc_radius, c[1])
+
+
 def make_scene(seed: int, n_planes: int, n_spheres: int, plane_dist, sphere_dist,
                sphere_radius, arc_radius: float, ground_y: Optional[float] = None,
                plane_half=(0.4, 1.4), hspan: float = 22.0, vspan: float = 10.0,
-               motion: bool = False) -> Scene:
+               motion: bool = False, near: bool = False) -> Scene:
+    """Seeded planes (static BG) and spheres (FG) at the given distances from
+    the rig's central camera.
+
+    ``near=True`` is the placement for object ranges that start close to the
+    rig (BASELINE.json c1-c4: "0.5-6 m", "0.5-8 m"): a plane's half-sizes are
+    ``plane_half`` x its distance (a constant angular size, so a plane 0.5 m
+    from the camera is a small card rather than a wall over the whole view),
+    a sphere's radius is at most 0.35 x its distance, and an object is
+    re-drawn (up to 64 times) while it would reach within 0.45 m of the
+    camera arc (where rig and jittered virtual cameras sit)."""
     rng = np.random.default_rng(seed)
     anchor = np.array([0.0, 0.0, -arc_radius])
     quads = []
     for _ in range(n_planes):
-        c = _random_in_view(rng, anchor, *plane_dist, hspan, vspan)
-        n = rng.normal(size=3)
-        n /= np.linalg.norm(n)
-        if n[2] > 0:          # face the rig (normal toward -z)
-            n = -n
-        if n[2] > -0.6:       # avoid grazing planes
-            n[2] = -0.6
+        for _try in range(64):
+            c = _random_in_view(rng, anchor, *plane_dist, hspan, vspan)
+            n = rng.normal(size=3)
             n /= np.linalg.norm(n)
-        u = np.cross(n, rng.normal(size=3))
-        u /= np.linalg.norm(u)
-        v = np.cross(n, u)
-        quads.append(Quad(c, u, v, float(rng.uniform(*plane_half)), float(rng.uniform(*plane_half)),
-                          _texture(rng, 1.0)))
+            if n[2] > 0:          # face the rig (normal toward -z)
+                n = -n
+            if n[2] > -0.6:       # avoid grazing planes
+                n[2] = -0.6
+                n /= np.linalg.norm(n)
+            u = np.cross(n, rng.normal(size=3))
+            u /= np.linalg.norm(u)
+            v = np.cross(n, u)
+            hu, hv = float(rng.uniform(*plane_half)), float(rng.uniform(*plane_half))
+            if not near:
+                break
+            d = float(np.linalg.norm(c - anchor))
+            hu, hv = hu * d, hv * d
+            if _rig_clearance(c, arc_radius) >= math.hypot(hu, hv) + 0.45:
+                break
+        quads.append(Quad(c, u, v, hu, hv, _texture(rng, 1.0)))
     spheres = []
     for _ in range(n_spheres):
-        c = _random_in_view(rng, anchor, *sphere_dist, hspan * 0.8, vspan * 0.8)
-        rad = float(rng.uniform(*sphere_radius))
-        if ground_y is not None:
-            c[1] = min(c[1], ground_y - rad - 0.02)
+        for _try in range(64):
+            c = _random_in_view(rng, anchor, *sphere_dist, hspan * 0.8, vspan * 0.8)
+            rad = float(rng.uniform(*sphere_radius))
+            if near:
+                rad = min(rad, 0.35 * float(np.linalg.norm(c - anchor)))
+            if ground_y is not None:
+                c[1] = min(c[1], ground_y - rad - 0.02)
+            if not near or _rig_clearance(c, arc_radius) >= rad + 0.45:
+                break
         vel = amp = np.zeros(3)
         freq = phase = 0.0
         if motion:
@@ -277,6 +305,16 @@ def make_scene(seed: int, n_planes: int, n_spheres: int, plane_dist, sphere_dist
             freq = float(rng.uniform(0.1, 0.4))
             phase = float(rng.uniform(0, 2 * math.pi))
             # |v| + 2 pi f |a| stays below 1 m/s
+            if near:
+                # a stream's 10 s (300 frames at 30 fps) keep clear of the arc
+                probe = Sphere(c, rad, None, vel, amp, freq, phase)
+                for _try in range(8):
+                    if all(_rig_clearance(probe.center_at(t), arc_radius) >= rad + 0.45
+                           for t in np.linspace(0.0, 10.0, 41)):
+                        break
+                    vel = vel * 0.5
+                    amp = amp * 0.5
+                    probe = Sphere(c, rad, None, vel, amp, freq, phase)
         spheres.append(Sphere(c, rad, _texture(rng, 0.5), vel, amp, freq, phase))
     gtex = _texture(rng, 1.5) if ground_y is not None else None
     return Scene(tuple(quads), tuple(spheres), ground_y, gtex)
@@ -429,9 +467,10 @@ def workload_params(name: str, seed: int = 2007) -> dict:
         nv, nf, k = 1, 1, 2
     elif name in ("c1", "c2", "c3"):
         w, h, f, n, radius, gap = 1920, 1080, 1400.0, 9, 3.0, 10.0
-        scene = make_scene(seed, 6, 5, (2.5, 6.0), (2.0, 4.5), (0.15, 0.5), radius,
-                           ground_y=1.2, plane_half=(0.7, 2.2), hspan=28, vspan=14,
-                           motion=(name == "c3"))
+        # BASELINE.json configs[1]: "6 planes + 5 spheres + a ground plane at 0.5-6 m"
+        scene = make_scene(seed, 6, 5, (0.5, 6.0), (0.5, 6.0), (0.15, 0.5), radius,
+                           ground_y=1.2, plane_half=(0.15, 0.4), hspan=28, vspan=14,
+                           motion=(name == "c3"), near=True)
         cap = dict(noise_rel=0.005, invalid_frac=0.03, invalid_mode="edges")
         k = 3
         if name == "c1":
@@ -442,8 +481,9 @@ def workload_params(name: str, seed: int = 2007) -> dict:
             nv, nf, phis = 300, 300, None
     elif name == "c4":
         w, h, f, n, radius, gap = 3840, 2160, 2800.0, 16, 3.0, 8.0
-        scene = make_scene(seed, 10, 40, (2.0, 8.0), (1.2, 6.0), (0.1, 0.45), radius,
-                           ground_y=1.2, hspan=40, vspan=16)
+        # BASELINE.json configs[4]: "40 spheres and 10 planes at 0.5-8 m"
+        scene = make_scene(seed, 10, 40, (0.5, 8.0), (0.5, 8.0), (0.1, 0.45), radius,
+                           ground_y=1.2, plane_half=(0.1, 0.3), hspan=40, vspan=16, near=True)
         cap = dict(noise_rel=0.005, invalid_frac=0.05, invalid_mode="edges")
         nv, nf, k = 32, 1, 4
         phis = None
@@ -455,12 +495,15 @@ def workload_params(name: str, seed: int = 2007) -> dict:
 
 def make_workload(name: str, seed: int = 2007, scale: int = 1, n_frames: Optional[int] = None,
                   n_views: Optional[int] = None, cameras: str = "refs",
-                  render_frames: bool = True) -> Workload:
+                  render_frames: bool = True,
+                  frame_ids: Optional[Sequence[int]] = None) -> Workload:
     """Build config ``name`` (c0..c4). ``scale`` > 1 divides the resolution
     (for CPU-sized parity cases); ``cameras='refs'`` renders only the cameras
     some view references, ``'all'`` the whole rig. ``n_frames`` overrides the
     frame count of c3; ``render_frames=False`` returns rig, views and
-    references without ray-casting any frame (scenes_gpu renders them)."""
+    references without ray-casting any frame (scenes_gpu renders them);
+    ``frame_ids`` renders only those frames of the stream (``frames[i]`` is
+    then frame ``frame_ids[i]``, still at time ``frame_ids[i] / 30`` s)."""
     prm = workload_params(name, seed)
     w, h, f, n = prm["w"], prm["h"], prm["f"], prm["n"]
     radius, gap, scene, cap, k = prm["radius"], prm["gap"], prm["scene"], prm["capture"], prm["k"]
@@ -495,7 +538,7 @@ def make_workload(name: str, seed: int = 2007, scale: int = 1, n_frames: Optiona
     refs = [select_references(v.pose, rig, ids, k) for v in virtuals]
     need = sorted({i for r in refs for i in r}) if cameras == "refs" else ids
     frames = []
-    for fi in range(nf):
+    for fi in (range(nf) if frame_ids is None else frame_ids):
         t = fi / 30.0
         view_ids = set(refs[fi]) if name == "c3" and cameras == "refs" else set(need)
         frames.append({cid: capture(scene, rig[cid], seed * 1_000_003 + cid * 7919 + fi, t,

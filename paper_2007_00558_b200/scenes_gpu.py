@@ -259,10 +259,12 @@ def capture(scene, calib, seed: int, t: float = 0.0, noise_rel: float = 0.0,
 
 def make_workload(name: str, seed: int = 2007, n_frames: Optional[int] = None,
                   n_views: Optional[int] = None, cameras: str = "refs", dev="cuda",
-                  scale: int = 1) -> scenes.Workload:
+                  scale: int = 1, frame_ids=None) -> scenes.Workload:
     """scenes.make_workload with the frames rendered on ``dev`` (DeviceCapture
     values). Rig, virtual cameras, reference lists and the scene are the host
-    generator's own (same seed -> same geometry)."""
+    generator's own (same seed -> same geometry). ``frame_ids`` (c3) renders
+    only those frames of the stream: ``frames[i]`` is frame ``frame_ids[i]``
+    (a rank renders only the frames it owns)."""
     skel = scenes.make_workload(name, seed=seed, scale=scale, n_frames=n_frames,
                                 n_views=n_views, cameras=cameras, render_frames=False)
     params = scenes.workload_params(name, seed)
@@ -271,11 +273,13 @@ def make_workload(name: str, seed: int = 2007, n_frames: Optional[int] = None,
     frames: List[Dict[int, DeviceCapture]] = []
     ids = [c.id for c in skel.rig]
     need = sorted({i for r in skel.refs for i in r}) if cameras == "refs" else ids
-    for fi in range(nf):
+    for fi in (range(nf) if frame_ids is None else frame_ids):
         view_ids = set(skel.refs[fi]) if name == "c3" and cameras == "refs" else set(need)
         frames.append({cid: capture(params["scene"], skel.rig[cid],
                                     seed * 1_000_003 + cid * 7919 + fi, fi / 30.0,
                                     dev=dev, cache=cache, **params["capture"])
                        for cid in sorted(view_ids)})
     desc = skel.description.replace(" 0 frames", f" {nf} frames") + " (frames ray-cast on the GPU)"
+    if frame_ids is not None:
+        desc += f", {len(frames)} of them rendered here"
     return scenes.Workload(skel.name, seed, skel.rig, skel.virtuals, skel.refs, frames, desc)

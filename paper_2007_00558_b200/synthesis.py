@@ -276,17 +276,49 @@ def synthesize_view_debug(virtual, inputs: Mapping[int, CameraStreamInputs],
     return frame, DebugBundle(tuple(contribs[:n]), tuple(contribs[n:]), fg, bg, prov)
 
 
-def write_debug_bundle(root, frame_id: int, bundle: DebugBundle, timestamp_us: int = 0) -> None:
-    """Debug-raster dump in the reference's MVD container (synthesis.py:400-436).
+def _rounded_rgb(color: np.ndarray) -> np.ndarray:
+    """np.clip(np.round(color), 0, 255).astype(uint8) (synthesis.py:419) on the
+    device: the composite kernel's half-even saturating conversion with the
+    layer valid everywhere."""
+    H, W = color.shape[:2]
+    ones = np.ones((H, W), bool)
+    fg = MergedLayer(np.asarray(color, np.float64), np.zeros((H, W)), ones)
+    return composite(fg, fg, SynthesisConfig()).pixels
 
-    The container format (``fvv.mvdio``) is outside this package's scope; when
-    the reference package is importable its writer is used, else this raises.
-    """
-    try:
-        from fvv import synthesis as _ref
-    except ImportError as e:  # pragma: no cover - depends on the host
-        raise NotImplementedError("write_debug_bundle needs the fvv MVD container writer") from e
-    _ref.write_debug_bundle(root, frame_id, bundle, timestamp_us)
+
+def write_debug_bundle(root, frame_id: int, bundle: DebugBundle, timestamp_us: int = 0) -> None:
+    """Debug-raster dump in the MVD container layout (synthesis.py:400-436):
+    each layer's contributions in ``<root>/<layer>/`` keyed by source camera,
+    the merged layer in the reserved virtual camera slot 15, the provenance
+    map as an 8-bit PNG. Written with this package's ``mvdio.MvdWriter``
+    (mm quantisation and validity run-length code on the GPU)."""
+    from pathlib import Path
+
+    from PIL import Image
+
+    from .mvdio import MvdWriter
+    from .types import DepthFrame, MvdFrame
+
+    root = Path(root)
+
+    def to_frame(camera_id, color, depth, valid):
+        valid = np.asarray(valid, bool)
+        h, w = valid.shape
+        validity = np.where(valid, Validity.VALID, Validity.INVALID).astype(np.uint8)
+        d = np.where(valid, depth, 0.0).astype(np.float32)
+        return MvdFrame(camera_id=camera_id, color=ColorFrame(w, h, _rounded_rgb(color),
+                                                              timestamp_us),
+                        depth=DepthFrame(w, h, d, validity, timestamp_us))
+
+    for layer_name, contribs, merged in (("fg", bundle.fg_contributions, bundle.fg),
+                                         ("bg", bundle.bg_contributions, bundle.bg)):
+        h, w = np.asarray(merged.valid).shape
+        with MvdWriter(root / layer_name, 0.0, w, h) as writer:
+            for c in contribs:
+                writer.write_frame(frame_id, to_frame(c.camera_id, c.color, c.depth, c.valid))
+            writer.write_frame(frame_id, to_frame(15, merged.color, merged.depth, merged.valid))
+    Image.fromarray(np.asarray(bundle.provenance, np.uint8), mode="L").save(
+        root / f"{frame_id:06d}.provenance.png")
 
 
 def view_psnr(synth, oracle, exclude: Optional[np.ndarray] = None) -> float:

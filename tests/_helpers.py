@@ -108,3 +108,53 @@ def psnr(a, b, exclude=None) -> float:
 
 def within_1lsb_frac(a, b) -> float:
     return float((np.abs(a.astype(int) - b.astype(int)) <= 1).all(-1).mean())
+
+
+# ---------------------------------------------------------------- full-size goldens
+
+
+def full_inputs(g):
+    """Rebuild the generated inputs of a ``full_<case>.npz`` golden (the same
+    calls as make_golden.full_workload) and check them against its hash.
+    Returns (virtual, refs, frames) with frames as the oracle's es_view dicts
+    (mm + validity sidecar + BG model per reference camera)."""
+    cfg, scale, seed, view = str(g["config"]), int(g["scale"]), int(g["seed"]), int(g["view"])
+    if cfg == "c3":
+        wl = scenes.make_workload("c3", seed=seed, scale=scale, n_frames=300, frame_ids=[view])
+    else:
+        wl = scenes.make_workload(cfg, seed=seed, scale=scale, n_views=view + 1)
+    refs = [int(r) for r in g["refs"]]
+    assert refs == wl.refs[view]
+    fr = wl.frames[0]
+    frames, hashed = [], []
+    for rid in refs:
+        c = fr[rid]
+        hashed += [c.rgb, c.mm, c.validity, c.bg_depth, c.bg_validity]
+        frames.append(dict(calib=c.calib, rgb=c.rgb, mm=c.mm, validity=c.validity,
+                           bg_depth=c.bg_depth, bg_validity=c.bg_validity))
+    assert sha(*hashed) == str(g["input_sha"]), "generator drifted from the golden inputs"
+    return wl.virtuals[view], refs, frames
+
+
+def reference_rgb(g, oracle_rgb):
+    """The reference's RGB of a full-size golden: the oracle's RGB with the
+    stored sparse difference applied, checked against the stored sha256."""
+    assert sha(oracle_rgb) == str(g["oracle_rgb_sha"]), \
+        "oracle output changed since the golden was made: regenerate it"
+    ref = np.ascontiguousarray(oracle_rgb).reshape(-1, 3).copy()
+    ref[g["rgb_diff_idx"]] = g["rgb_diff_val"]
+    ref = ref.reshape(oracle_rgb.shape)
+    assert sha(ref) == str(g["rgb_sha"])
+    return ref
+
+
+def unpack(g, key, shape_key):
+    shape = tuple(int(x) for x in g[shape_key])
+    return np.unpackbits(g[key])[: int(np.prod(shape))].reshape(shape).astype(bool)
+
+
+def rgb_agreement(a, b) -> dict:
+    d = np.abs(a.astype(int) - b.astype(int)).max(-1)
+    return {"pixels": int(d.size), "identical": int((d == 0).sum()),
+            "within_1lsb": int((d <= 1).sum()), "max_diff": int(d.max()),
+            "psnr_db": psnr(a, b)}

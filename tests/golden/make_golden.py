@@ -18,6 +18,11 @@ Three fixture families, all committed as compressed .npz:
   reference outputs and, for the quality cases, the ray-cast ground truth and
   coverage mask used by tests/test_synthesis.py:213-222 and
   tests/test_acceptance.py:188-214.
+* ``full_<case>.npz`` — the reference's whole edge-server path (mm decode,
+  bilateral hole fill, synthesize_view_debug) at BASELINE sizes: c0 640x360,
+  c1 1920x1080, frame 150 of the c3 stream, c4's rig at 1920x1080 (scale 2);
+  RGB as sha256 + sparse difference against the C oracle, masks bit-packed
+  (``python tests/golden/make_golden.py full [case ...]``);
 * ``es_<case>.npz`` / ``codec.npz`` — edge-server preprocessing: reference
   ``depth_from_millimeters`` + ``bilateral_close_holes`` outputs on generated
   mm frames, and ``unpack_yuv420``/``dequantize12`` on generated codes.
@@ -54,6 +59,13 @@ SYN_CASES = [
     ("c4_s16_v0", "c4", 16, 2007, 0),
 ]
 ES_CASES = [("c1_s4", "c1", 4, 2007), ("c0_s1", "c0", 1, 2007)]
+# BASELINE sizes, full edge-server path (case, config, scale, seed, view/frame)
+FULL_CASES = [
+    ("c0", "c0", 1, 2007, 0),
+    ("c1", "c1", 1, 2007, 0),
+    ("c3_f150", "c3", 1, 2007, 150),
+    ("c4_s2_v0", "c4", 2, 2007, 0),
+]
 
 
 def sha(*arrays) -> str:
@@ -154,6 +166,71 @@ def refscene_case(case, preset, virtual, refs, t, quality):
                         rgb=frame.pixels, prov=b.provenance, contrib_valid=cv,
                         merged_valid=np.stack([b.fg.valid, b.bg.valid]), **arrs, **extra)
     print(case, preset, "refs", refs)
+
+
+def full_workload(cfg, scale, seed, view):
+    """The generated inputs of a full-size case (tests/_helpers.full_case
+    rebuilds the same): c3 renders only frame ``view`` of its 300-frame
+    stream, c4 only the cameras view ``view`` references."""
+    if cfg == "c3":
+        return scenes.make_workload("c3", seed=seed, scale=scale, n_frames=300,
+                                    frame_ids=[view]), 0
+    return scenes.make_workload(cfg, seed=seed, scale=scale, n_views=view + 1), 0
+
+
+def full_case(case, cfg, scale, seed, view):
+    """The reference's whole edge-server path at a BASELINE size: per
+    reference camera ``depth_from_millimeters`` -> ``bilateral_close_holes``
+    (pipeline.py:518-519; mvdio.py:132), then ``synthesize_view_debug``
+    (pipeline.py:546). Inputs are stored as their sha256 only. RGB is stored
+    as its sha256 plus the sparse difference against the C oracle's RGB for
+    the same inputs (the tests rebuild the reference RGB from the oracle's and
+    check the hash); masks are bit-packed."""
+    import time
+
+    from oracle import c_oracle as CO
+
+    wl, fidx = full_workload(cfg, scale, seed, view)
+    v, refs = wl.virtuals[view], wl.refs[view]
+    frame = wl.frames[fidx]
+    inputs, hashed, fills = {}, [], {}
+    t0 = time.time()
+    for rid in refs:
+        c = frame[rid]
+        hashed += [c.rgb, c.mm, c.validity, c.bg_depth, c.bg_validity]
+        H, W = c.mm.shape
+        df = rc.depth_from_millimeters(c.mm, c.validity)
+        filled = rproc.bilateral_close_holes(df, rc.ColorFrame(W, H, c.rgb))
+        fills[rid] = (df, filled)
+        inputs[rid] = rs.CameraStreamInputs(ref_calib(c.calib), rc.ColorFrame(W, H, c.rgb),
+                                            filled, rc.DepthFrame(W, H, c.bg_depth,
+                                                                  c.bg_validity))
+    t1 = time.time()
+    img, b = rs.synthesize_view_debug(ref_calib(v), inputs, refs, rs.SynthesisConfig())
+    t2 = time.time()
+    o_rgb, o_prov = CO.es_view(v, [dict(calib=frame[r].calib, rgb=frame[r].rgb, mm=frame[r].mm,
+                                        validity=frame[r].validity, bg_depth=frame[r].bg_depth,
+                                        bg_validity=frame[r].bg_validity) for r in refs])
+    rgb = img.pixels
+    diff = np.flatnonzero((rgb != o_rgb).any(-1)).astype(np.int64)
+    cv = np.stack([c.valid for c in b.fg_contributions + b.bg_contributions])
+    mv = np.stack([b.fg.valid, b.bg.valid])
+    out = dict(config=cfg, scale=scale, seed=seed, view=view, refs=np.asarray(refs),
+               input_sha=sha(*hashed), rgb_sha=sha(rgb), rgb_diff_idx=diff,
+               rgb_diff_val=rgb.reshape(-1, 3)[diff], oracle_rgb_sha=sha(o_rgb),
+               prov=b.provenance, contrib_valid=np.packbits(cv),
+               contrib_shape=np.asarray(cv.shape), merged_valid=np.packbits(mv),
+               merged_shape=np.asarray(mv.shape),
+               ref_seconds=np.asarray([t1 - t0, t2 - t1]))
+    for j, rid in enumerate(refs):
+        df, filled = fills[rid]
+        out[f"fill{j}_validity"] = np.packbits(filled.validity == 0)
+        out[f"fill{j}_depth_sha"] = sha(filled.depth)
+        out[f"fill{j}_holes"] = np.int64((df.validity == 1).sum())
+    np.savez_compressed(OUT / f"full_{case}.npz", **out)
+    print(case, wl.description, "refs", refs, f"reference {t1 - t0:.1f} s fill + "
+          f"{t2 - t1:.1f} s synthesis; RGB pixels differing from the oracle: {diff.size}; "
+          f"prov==oracle {float((o_prov == b.provenance).mean()):.7f}")
 
 
 def es_case(case, cfg, scale, seed):
@@ -340,6 +417,11 @@ def mvd_case():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["full"]:
+        for args in FULL_CASES:
+            if len(sys.argv) == 2 or args[0] in sys.argv[2:]:
+                full_case(*args)
+        sys.exit(0)
     if sys.argv[1:] == ["mvd"]:
         mvd_case()
         sys.exit(0)
@@ -363,3 +445,5 @@ if __name__ == "__main__":
     for args in ES_CASES:
         es_case(*args)
     codec_case()
+    for args in FULL_CASES:
+        full_case(*args)

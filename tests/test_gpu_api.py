@@ -472,3 +472,137 @@ def test_silhouette_holes_mostly_filled_to_ground_truth(P, T):
     assert (rel[filled & gentle] <= 0.02).all()
     assert (filled & gentle).sum() > 100
     assert np.median(rel[filled]) <= 0.02
+
+
+def _noised_frames(wl, refs, n, seed):
+    """``n`` distinct frames of the rig's reference cameras: the capture with
+    fresh depth noise and fresh invalid pixels, as pinned-ready host arrays."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        fr = {}
+        for cid in refs:
+            c = wl.frames[0][cid]
+            mm = c.mm.astype(np.float64)
+            ok = mm > 0
+            mm[ok] = np.clip(np.round(mm[ok] * (1 + 0.01 * rng.normal(size=ok.sum()))), 1, 65535)
+            val = c.validity.copy()
+            kill = (rng.random(mm.shape) < 0.02) & (val == 0)
+            mm[kill] = 0
+            rgb = np.clip(c.rgb.astype(int) + rng.integers(-8, 9, c.rgb.shape), 0, 255)
+            fr[cid] = (rgb.astype(np.uint8), mm.astype(np.uint16), val)
+        out.append(fr)
+    return out
+
+
+def test_edge_stream_downloads_equal_synchronous_renders(cuda):
+    """The e2e path (EdgeStream: pinned H2D -> K0..K3 -> D2H, double-
+    buffered) over 8 distinct frames: every downloaded view equals the view
+    a synchronous ingest + render of the same frame produces — no view is
+    overwritten while it is being copied out (pipeline.py:546-547,762-763)."""
+    import torch
+
+    from paper_2007_00558_b200 import scenes
+    from paper_2007_00558_b200.engine import EdgeRenderer, EdgeStream
+
+    wl = scenes.make_workload("c1", scale=2)
+    v, refs = wl.virtuals[0], wl.refs[0]
+    frames = _noised_frames(wl, refs, 8, 3)
+    bgs = {cid: (wl.frames[0][cid].bg_depth, wl.frames[0][cid].bg_validity) for cid in refs}
+
+    def renderer():
+        r = EdgeRenderer(wl.rig, private=True)
+        for cid, (d, val) in bgs.items():
+            r.set_bg_model(cid, d, val)
+        return r
+
+    want = []
+    sync = renderer()
+    for fr in frames:
+        sync.ingest_mm_many(fr)
+        want.append(sync.render([v], [refs])[0].cpu().numpy())
+    assert not all(np.array_equal(want[0], w) for w in want[1:])
+
+    got = {}
+    es = EdgeStream(renderer(), 1, depth=2,
+                    on_view=lambda host, tag: got.__setitem__(tag, host[0].numpy().copy()))
+    for rep in range(3):   # several laps: buffers rotate while earlier copies are in flight
+        for i, fr in enumerate(frames):
+            pinned = {cid: tuple(torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16
+                                                  else a).pin_memory() for a in t)
+                      for cid, t in fr.items()}
+            es.submit(pinned, [v], [refs], tag=(rep, i))
+    es.flush()
+    assert len(got) == 3 * len(frames)
+    for (rep, i), img in got.items():
+        assert np.array_equal(img, want[i]), f"lap {rep}, frame {i}"
+    assert es.h2d_bytes == 3 * sum(a.nbytes for fr in frames for t in fr.values() for a in t)
+
+
+def test_renderers_sharing_a_context_keep_their_own_slots(cuda):
+    """Two default renderers share the device context but not camera slots:
+    the second never renders the first's frames, and a renderer without BG
+    models or frames raises "missing inputs" (synthesis.py:349-350)."""
+    from paper_2007_00558_b200 import synthesis as S
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    case = refscene_case(golden("refscene_mid34_medium.npz"))
+    inputs = case.inputs()
+    rig = [inputs[r].calib for r in case.refs]
+    a = EdgeRenderer(rig)
+    for r in case.refs:
+        a.set_bg_model(r, inputs[r].bg_depth)
+        a.ingest(r, inputs[r].live_color, inputs[r].live_depth, hole_closing=False)
+    first = a.render([case.virtual], [case.refs])[0].cpu().numpy()
+    b = EdgeRenderer(rig)
+    assert a.ctx is b.ctx and not set(a.slot.values()) & set(b.slot.values())
+    b.ingested = set(case.refs)      # pretend: the library must still refuse
+    with pytest.raises(ValueError, match="missing inputs|background"):
+        b.render([case.virtual], [case.refs])
+    again = a.render([case.virtual], [case.refs])[0].cpu().numpy()
+    np.testing.assert_array_equal(again, first)
+    want = S.synthesize_view(case.virtual, inputs, case.refs, S.SynthesisConfig())
+    np.testing.assert_array_equal(first, want.pixels)
+    b.close()
+    a.close()
+
+
+def test_engine_rejects_rasters_that_do_not_fit_the_calibration(cuda):
+    """Short rasters or outputs fail as ValueError before any kernel runs
+    (the kernels read/write the calibration's W*H elements)."""
+    import torch
+
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    case = refscene_case(golden("refscene_mid34_medium.npz"))
+    inputs = case.inputs()
+    rig = [inputs[r].calib for r in case.refs]
+    r0 = case.refs[0]
+    e = EdgeRenderer(rig, private=True)
+    H, W = inputs[r0].live_depth.depth.shape
+    with pytest.raises(ValueError, match="shape"):
+        e.set_bg_model(r0, np.zeros((H - 1, W), np.float32), np.zeros((H - 1, W), np.uint8))
+    with pytest.raises(ValueError, match="shape"):
+        e.ingest_mm(r0, np.zeros((H, W, 3), np.uint8), np.zeros((H, W - 2), np.uint16), None)
+    with pytest.raises(ValueError, match="shape"):
+        e.ingest_mm_many({r0: (np.zeros((H, W), np.uint8), np.zeros((H, W), np.uint16), None)})
+    with pytest.raises(ValueError, match="shape"):
+        e.ingest_yuv(r0, np.zeros((H, W, 3), np.uint8), np.zeros((H, W), np.uint8),
+                     np.zeros((H // 2, W // 2 - 1), np.uint8), np.zeros((H // 2, W // 2), np.uint8),
+                     None)
+    for r in case.refs:
+        e.set_bg_model(r, inputs[r].bg_depth)
+        e.ingest(r, inputs[r].live_color, inputs[r].live_depth, hole_closing=False)
+    Hv, Wv = int(case.virtual.intrinsics.height), int(case.virtual.intrinsics.width)
+    with pytest.raises(ValueError, match="shape"):
+        e.render([case.virtual], [case.refs],
+                 out=torch.empty((1, Hv, Wv - 1, 3), dtype=torch.uint8, device=cuda))
+    with pytest.raises(ValueError, match="uint8"):
+        e.render([case.virtual], [case.refs],
+                 out=torch.empty((1, Hv, Wv, 3), dtype=torch.int32, device=cuda))
+    with pytest.raises(ValueError, match="contiguous"):
+        e.render([case.virtual], [case.refs],
+                 out=torch.empty((1, Hv, 2 * Wv, 3), dtype=torch.uint8, device=cuda)[:, :, ::2])
+    with pytest.raises(ValueError, match="shape"):
+        e.render([case.virtual], [case.refs],
+                 provenance=torch.empty((1, Hv - 1, Wv), dtype=torch.uint8, device=cuda))

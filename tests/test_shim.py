@@ -27,7 +27,7 @@ for n in pytest_shim._OVERRIDE:
 # names the reference tests touch (tests/test_synthesis.py:8-288)
 for n in ("write_debug_bundle", "CameraStreamInputs", "LAYER_BG", "view_psnr"):
     assert hasattr(mod, n), n
-assert mod.write_debug_bundle.__module__ == "fvv.synthesis"   # reference's own I/O kept
+assert mod.write_debug_bundle is ours.write_debug_bundle   # own MVD container writer
 assert fvv.depthproc.bilateral_close_holes is odp.bilateral_close_holes
 print("OK")
 """
@@ -53,6 +53,7 @@ for n in ("unpack_yuv420", "dequantize12", "quantize12", "pack_yuv420", "encode_
 for n in ("EncodedFrame", "Yuv420Image", "DisparityMap12", "DecodeError",
           "UnsupportedCodecError"):
     assert getattr(ours, n) is getattr(rc, n), n
+assert ours._COMPRESSORS is rc._COMPRESSORS    # codecs registered on either side
 print("OK")
 """
     env = {"PYTHONPATH": f"{REF_SRC}:{ROOT}", "PYTHONDONTWRITEBYTECODE": "1",
