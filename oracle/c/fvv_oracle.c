@@ -135,16 +135,33 @@ static uint64_t zkey(double z, uint64_t idx, int b) {
     return (zc << b) | idx;
 }
 
-static void transfer(const fo_cam *s, const fo_cam *t, double px, double py, double pz,
-                     double *x, double *y, double *z) {
-    const double *R = s->R, *Cs = s->C, *T = t->R, *Ct = t->C;
-    const double wx = ((px * R[0] + py * R[3]) + pz * R[6]) + Cs[0];
-    const double wy = ((px * R[1] + py * R[4]) + pz * R[7]) + Cs[1];
-    const double wz = ((px * R[2] + py * R[5]) + pz * R[8]) + Cs[2];
-    const double dx = wx - Ct[0], dy = wy - Ct[1], dz = wz - Ct[2];
-    *x = (dx * T[0] + dy * T[1]) + dz * T[2];
-    *y = (dx * T[3] + dy * T[4]) + dz * T[5];
-    *z = (dx * T[6] + dy * T[7]) + dz * T[8];
+/* src camera -> dst camera motion, composed once per pair in a fixed order
+ * (oracle relative_pose): M = R_t R_s^T, tt = R_t (C_s - C_t). */
+typedef struct {
+    double M[9], t[3];
+} fo_rel;
+
+static fo_rel relative_pose(const fo_cam *s, const fo_cam *t) {
+    fo_rel r;
+    const double *Rs = s->R, *Rt = t->R;
+    const double dc[3] = {s->C[0] - t->C[0], s->C[1] - t->C[1], s->C[2] - t->C[2]};
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j)
+            r.M[3 * i + j] = (Rt[3 * i] * Rs[3 * j] + Rt[3 * i + 1] * Rs[3 * j + 1]) +
+                             Rt[3 * i + 2] * Rs[3 * j + 2];
+        r.t[i] = (Rt[3 * i] * dc[0] + Rt[3 * i + 1] * dc[1]) + Rt[3 * i + 2] * dc[2];
+    }
+    return r;
+}
+
+/* (x, y, z) in the target camera of the source ray (rx, ry, 1) at depth d:
+ * per coordinate ((M_i0 rx) + ((M_i1 ry) + M_i2)) d + t_i (oracle transfer) */
+static void transfer(const fo_rel *m, double rx, double ry, double d, double *x, double *y,
+                     double *z) {
+    const double *M = m->M;
+    *x = (M[0] * rx + (M[1] * ry + M[2])) * d + m->t[0];
+    *y = (M[3] * rx + (M[4] * ry + M[5])) * d + m->t[1];
+    *z = (M[6] * rx + (M[7] * ry + M[8])) * d + m->t[2];
 }
 
 typedef struct {
@@ -160,6 +177,7 @@ static void forward_warp(const float *depth, const uint8_t *valid_src, const fo_
     const long nc = (long)Wc * (Hd + 2 * r);
     for (long i = 0; i < nc; ++i) w->canvas[i] = KEY_EMPTY;
     w->b = index_bits((long)Ws * Hs);
+    const fo_rel m = relative_pose(src, dst);
     for (int v = 0; v < Hs; ++v) {
         const double ry = ((double)v - src->cy) / src->fy;
         for (int u = 0; u < Ws; ++u) {
@@ -169,7 +187,7 @@ static void forward_warp(const float *depth, const uint8_t *valid_src, const fo_
             const double d = (double)depth[i];
             const double rx = ((double)u - src->cx) / src->fx;
             double x, y, z;
-            transfer(src, dst, rx * d, ry * d, d, &x, &y, &z);
+            transfer(&m, rx, ry, d, &x, &y, &z);
             w->zsrc[i] = z;
             if (!(z > 0.0)) continue;
             const double ui = rint((dst->fx * x) / z + dst->cx);
@@ -254,6 +272,7 @@ static void backward_fetch(const double *zbuf, const fo_cam *src, const fo_cam *
                            const uint8_t *rgb, const uint8_t *cvalid_val, uint8_t cvalid_code,
                            double *col, double *dep, uint8_t *ok_out) {
     const int Wd = dst->width, Hd = dst->height, Ws = src->width, Hs = src->height;
+    const fo_rel m = relative_pose(dst, src);
     for (int y = 0; y < Hd; ++y) {
         const double ry = ((double)y - dst->cy) / dst->fy;
         for (int x = 0; x < Wd; ++x) {
@@ -265,7 +284,7 @@ static void backward_fetch(const double *zbuf, const fo_cam *src, const fo_cam *
             if (!(z < INFINITY)) continue;
             const double rx = ((double)x - dst->cx) / dst->fx;
             double xs, ys, zs;
-            transfer(dst, src, rx * z, ry * z, z, &xs, &ys, &zs);
+            transfer(&m, rx, ry, z, &xs, &ys, &zs);
             if (!(zs > 0.0)) continue;
             const double us = (src->fx * xs) / zs + src->cx;
             const double vs = (src->fy * ys) / zs + src->cy;

@@ -133,21 +133,40 @@ def world_to_cam(wx, wy, wz, cam: Cam):
     return x, y, z
 
 
-def transfer(depth_f64, src: Cam, dst: Cam, us=None, vs=None):
-    """Lift src pixels at ``depth`` and express them in dst's camera frame.
+def relative_pose(src: Cam, dst: Cam):
+    """The src-camera -> dst-camera rigid motion, composed once per camera
+    pair in a fixed order: ``M = R_dst R_src^T``, ``t = R_dst (C_src - C_dst)``
+    (``world_to_camera(camera_to_world(p, src), dst)``, core.py:160-169, is
+    ``M p + t``). Python floats: IEEE f64, no fused multiply-add."""
+    Rs, Rd = src.R, dst.R
+    dc = [float(src.C[k]) - float(dst.C[k]) for k in range(3)]
+    M = [[(float(Rd[i, 0]) * float(Rs[j, 0]) + float(Rd[i, 1]) * float(Rs[j, 1]))
+          + float(Rd[i, 2]) * float(Rs[j, 2]) for j in range(3)] for i in range(3)]
+    t = [(float(Rd[i, 0]) * dc[0] + float(Rd[i, 1]) * dc[1]) + float(Rd[i, 2]) * dc[2]
+         for i in range(3)]
+    return M, t
 
-    ``unproject_map`` (core.py:230-234) followed by ``world_to_camera``.
-    Without ``us``/``vs`` the whole raster is used.
+
+def transfer(depth_f64, src: Cam, dst: Cam, us=None, vs=None):
+    """Lift src pixels at ``depth`` and express them in dst's camera frame:
+    ``unproject_map`` (core.py:230-234) followed by ``world_to_camera``
+    (core.py:160-169), as ``M (rx d, ry d, d) + t`` evaluated per coordinate
+    i as ``((M_i0 rx) + ((M_i1 ry) + M_i2)) d + t_i`` — the ray (rx, ry, 1)
+    is rotated first (its row part once per source row), then scaled by the
+    depth. Without ``us``/``vs`` the whole raster is used.
     """
+    M, t = relative_pose(src, dst)
     rx, ry = rays(src)
     if us is None:
-        px = rx[None, :] * depth_f64
-        py = ry[:, None] * depth_f64
+        RX, RY = rx[None, :], ry[:, None]
     else:
-        px = rx[us] * depth_f64
-        py = ry[vs] * depth_f64
-    pz = depth_f64  # ray z is exactly 1.0
-    return world_to_cam(*cam_to_world(px, py, pz, src), dst)
+        RX, RY = rx[us], ry[vs]
+    out = []
+    for i in range(3):
+        q = M[i][1] * RY + M[i][2]
+        a = M[i][0] * RX + q
+        out.append(a * depth_f64 + t[i])
+    return tuple(out)
 
 
 def project(x, y, z, cam: Cam):

@@ -29,7 +29,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
             and LIB.stat().st_mtime >= max(p.stat().st_mtime for p in deps)):
         return LIB
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2",
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
            "-shared", "-o", str(tmp), *map(str, srcs)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

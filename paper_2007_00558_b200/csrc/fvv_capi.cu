@@ -480,8 +480,10 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
             const int k = L * n + j;
             const float *d = L == 0 ? s.fgd : s.bgd;
             double *zs = ctx->zsrc + ctx->zcap * k;
-            wp.c[k] = WarpContrib{s.dev, d, rx, ry, cbase + per * k, zs, b};
-            rp.c[k] = ResolveContrib{s.dev, s.texel, zs, cbase + per * k, w, b,
+            wp.c[k] = WarpContrib{s.dev, relative_pose(s.dev, dst), d, rx, ry, cbase + per * k,
+                                  zs, b};
+            rp.c[k] = ResolveContrib{s.dev, relative_pose(dst, s.dev), s.texel, zs,
+                                     cbase + per * k, w, b,
                                      L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
         }
     }
@@ -1257,7 +1259,8 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     wp.n = 1;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
     if ((rc = ensure_zsrc(ctx, 1, (size_t)src->width * src->height))) return rc;
-    wp.c[0] = WarpContrib{s.dev, s.fgd, rx, ry, ctx->canvas + 1, ctx->zsrc, b};
+    wp.c[0] = WarpContrib{s.dev, relative_pose(s.dev, dd), s.fgd, rx, ry, ctx->canvas + 1,
+                          ctx->zsrc, b};
     LAUNCH_K(FVV_K_FORWARD_WARP, launch_forward_warp(wp, (long long)src->width * src->height, ctx->stream));
     ResolveParams rp{};
     rp.dst = dd;
@@ -1274,7 +1277,7 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.dbg.contrib_valid = valid_out;
     rp.dbg.contrib_winner = winner_out;
     rp.dbg.contrib_stage = stage_out;
-    rp.c[0] = ResolveContrib{s.dev, s.texel, ctx->zsrc, ctx->canvas + 1,
+    rp.c[0] = ResolveContrib{s.dev, relative_pose(dd, s.dev), s.texel, ctx->zsrc, ctx->canvas + 1,
                              host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
                              layer_fg ? 1 : 0};
     if (r == 1 && resolve_uses_tma() &&

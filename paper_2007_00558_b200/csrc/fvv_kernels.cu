@@ -644,6 +644,8 @@ __global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const 
     const int Wd = p.dst.W, Hd = p.dst.H, P = p.pitch;
     const double lo = -(double)r, uhi = (double)(Wd + r), vhi = (double)(Hd + r);
     const double ry = __ldg(c.ry + sv);
+    // the row part of the rotated ray, once per thread (its 4 pixels share a row)
+    const double q0 = rel_q(c.rel, 0, ry), q1 = rel_q(c.rel, 1, ry), q2 = rel_q(c.rel, 2, ry);
     const bool fgk = p.tf.flag && (int)blockIdx.z < p.tf.n_fg;
     const uint8_t gen8 = (uint8_t)(p.gen_hi >> kGenShift);
     int first_t = -1, last_t = -1;
@@ -655,8 +657,9 @@ __global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const 
         if (!(d[q] > 0.0f)) continue;
         const int su = u0 + q;
         const double dd = (double)d[q];
-        double x, y, z;
-        transfer(c.src, p.dst, dmul(__ldg(c.rx + su), dd), dmul(ry, dd), dd, x, y, z);
+        const double rx = __ldg(c.rx + su);
+        const double x = rel_c(c.rel, 0, rx, q0, dd), y = rel_c(c.rel, 1, rx, q1, dd),
+                     z = rel_c(c.rel, 2, rx, q2, dd);
         if (!(z > 0.0)) continue;
         double ur, vr;
         if (z > 1e-200) {
@@ -911,7 +914,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
             double c0 = 0.0, c1 = 0.0, c2 = 0.0;
             if (z < INFINITY) {
                 double xs, ys, zs;
-                transfer(dst, c.src, dmul(rxd, z), dmul(ryd, z), z, xs, ys, zs);
+                transfer(c.rel, rxd, ryd, z, xs, ys, zs);
                 if (zs > 0.0) {
                     const int Ws = c.src.W, Hs = c.src.H;
                     const double us = proj(c.src.fx, xs, zs, c.src.cx);
@@ -1277,7 +1280,7 @@ double crack_z(const ResolveContrib &c, const DevCam &dst,
 __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst, double rxd,
                                       double ryd, double z, double &c0, double &c1, double &c2) {
     double xs, ys, zs;
-    transfer(dst, c.src, dmul(rxd, z), dmul(ryd, z), z, xs, ys, zs);
+    transfer(c.rel, rxd, ryd, z, xs, ys, zs);
     if (!(zs > 0.0)) return false;
     const int Ws = c.src.W, Hs = c.src.H;
     double us, vs;

@@ -65,6 +65,7 @@ struct PreprocBatch {
 
 struct WarpContrib {
     DevCam src;
+    Rel rel;                 // src camera -> virtual camera (relative_pose)
     const float *depth;      // > 0 marks a source pixel (Valid), else 0
     const double *rx, *ry;   // src ray slope tables (core.py:224-227)
     uint64_t *canvas;        // (Hd+2r) x (Wd+2r) keys
@@ -117,6 +118,7 @@ struct WarpParams {
 
 struct ResolveContrib {
     DevCam src;
+    Rel rel;                 // virtual camera -> src camera (relative_pose)
     const uint32_t *texel;
     const double *zsrc;      // K2's exact z per source pixel (WarpContrib::zsrc)
     const uint64_t *canvas;

@@ -125,6 +125,16 @@ def _wh(calib):
     return int(k.width), int(k.height)
 
 
+def _check_calib(calib, height, width, what="raster"):
+    """A raster must have the size its calibration declares: the kernels
+    read/write the calibration's W*H pixels (the reference fails in numpy
+    broadcasting there)."""
+    W, H = _wh(calib)
+    if (int(height), int(width)) != (H, W):
+        raise ValueError(f"camera {calib.id}: {what} is {width}x{height}, its intrinsics "
+                         f"say {W}x{H}")
+
+
 def _weight(src_calib, dst_calib, cfg) -> float:
     return 1.0 / (camera_distance(src_calib.pose, dst_calib.pose) + cfg.mixing_epsilon)
 
@@ -135,6 +145,9 @@ def warp_layer(color, depth, src, dst, cfg: SynthesisConfig,
     """Warp one camera's layer into ``dst`` (synthesis.py:162-258)."""
     if (color.height, color.width) != (depth.height, depth.width):
         raise ValueError("color and depth dimensions differ")
+    _check_calib(src, color.height, color.width)
+    if color_valid is not None and np.shape(color_valid) != (color.height, color.width):
+        raise ValueError("color_valid does not match the colour raster")
     ctx = _native.context()
     W, H = _wh(dst)
     rgb = _dev.upload(color.pixels, np.uint8)
@@ -163,6 +176,10 @@ def mix_layer(contribs: Sequence[LayerContribution], cfg: SynthesisConfig) -> Me
         raise ValueError("need at least one contribution")
     ctx = _native.context()
     H, W = np.asarray(contribs[0].valid).shape
+    for c in contribs:
+        if np.shape(c.valid) != (H, W) or np.shape(c.depth) != (H, W) or \
+                np.shape(c.color) != (H, W, 3):
+            raise ValueError("contribution dimensions differ")
     cols = [_dev.upload(c.color, np.float64) for c in contribs]
     deps = [_dev.upload(c.depth, np.float64) for c in contribs]
     vals = [_dev.upload(np.asarray(c.valid, bool), np.uint8) for c in contribs]
@@ -183,6 +200,9 @@ def composite(fg: MergedLayer, bg: MergedLayer, cfg: SynthesisConfig,
               return_provenance: bool = False):
     """FG over BG over hole colour; provenance 0 hole / 1 bg / 2 fg (synthesis.py:295-318)."""
     if np.asarray(fg.valid).shape != np.asarray(bg.valid).shape:
+        raise ValueError("layer dimensions differ")
+    shape = np.asarray(fg.valid).shape
+    if np.shape(fg.color) != shape + (3,) or np.shape(bg.color) != shape + (3,):
         raise ValueError("layer dimensions differ")
     ctx = _native.context()
     H, W = np.asarray(fg.valid).shape
@@ -213,6 +233,7 @@ def _ref_frames(virtual, inputs, refs, cfg):
         for d in (s.live_depth, s.bg_depth):
             if (s.live_color.height, s.live_color.width) != (d.height, d.width):
                 raise ValueError("color and depth dimensions differ")
+        _check_calib(s.calib, s.live_color.height, s.live_color.width)
         bufs = (_dev.upload(s.live_color.pixels, np.uint8),
                 _dev.upload(s.live_depth.depth, np.float32),
                 _dev.upload(s.live_depth.validity, np.uint8),
