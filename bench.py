@@ -79,6 +79,10 @@ def parse():
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="launch every step's kernels from the host instead of replaying the "
+                         "step's CUDA graph (EdgeRenderer.capture_step); c3, whose every frame "
+                         "has its own view, always launches from the host")
     ap.add_argument("--launch-check", action="store_true",
                     help="launcher/sharding check without GPU work (CPU, gloo): every rank "
                          "reports the views/frames it owns; rank 0 prints one JSON line")
@@ -344,25 +348,127 @@ def run_reference(args):
 # GPU arm
 
 
-def run_e2e(args, wl, eng, frames, views, dev, stream):
+KERNEL_NAMES = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
+                "resolve": "k_resolve_fast", "fill": "k_gen_fill"}
+FACTS = ROOT / "profiles" / "r02_kernel_facts.json"      # ncu --set full, c1 step
+DEVICE_PEAKS = ROOT / "profiles" / "r02_peaks.json"      # tools/peaks.cu
+
+
+def kernel_rooflines(args, kern, per_kernel, atomics_per_k2, hbm, peak_src):
+    """Every kernel against the roofline that bounds it:
+
+    * ``roofline`` — the dominant kernel (K3) against HBM: algorithmic bytes
+      per launch / its CUDA-event time (this run) vs the measured copy peak;
+    * ``roofline_atomic`` — K2's 64-bit z-buffer atomicMin count per launch
+      (a device counter, this run's profiling pass) / its event time vs the
+      measured RED.E.MIN.64 rate of a warp-coherent scatter into a canvas of
+      the same size (profiles/r02_peaks.json);
+    * ``roofline_fp64`` / ``roofline_issue`` — K2's and K3's FP64 thread
+      operations and warp instructions per launch (ncu, committed capture of
+      the c1 step: profiles/r02_kernel_facts.json) / event time vs the
+      measured DFMA rate and FFMA issue rate;
+    * per kernel in ``kernels``: ncu DRAM bytes per launch / event time vs HBM.
+    """
+    out = {}
+    facts = json.loads(FACTS.read_text()) if FACTS.exists() else {}
+    dpk = json.loads(DEVICE_PEAKS.read_text()) if DEVICE_PEAKS.exists() else {}
+    captured = args.config == "c1" and not args.extensions   # the captured workload
+    for name, k in kern.items():
+        f = facts.get(KERNEL_NAMES.get(name, ""), {}) if captured else {}
+        t = k["avg_ms"] / 1e3
+        if per_kernel.get(name):
+            k["algorithmic_bytes"] = per_kernel[name]
+            k["hbm_frac_algorithmic"] = per_kernel[name] / t / 1e9 / hbm
+        if f.get("dram_bytes"):
+            k["dram_bytes_ncu"] = f["dram_bytes"]
+            k["hbm_frac_ncu_traffic"] = f["dram_bytes"] / t / 1e9 / hbm
+    dom = max(kern, key=lambda n: kern[n]["avg_ms"] * kern[n]["launches"])
+    if per_kernel.get(dom):
+        ach = per_kernel[dom] / (kern[dom]["avg_ms"] / 1e3) / 1e9
+        traffic = facts.get(KERNEL_NAMES.get(dom, ""), {}).get("dram_bytes") if captured else None
+        out["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm,
+                           "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                           "algorithmic_bytes_per_launch": per_kernel[dom],
+                           "peak_source": peak_src}
+    red = dpk.get("red_min_u64", {})
+    canvas = "c4_canvas_66.5MB" if args.config == "c4" else "c1_canvas_16.6MB"
+    peak_red = red.get(f"{canvas}/warp_consecutive")
+    if "forward_warp" in kern and atomics_per_k2 and peak_red:
+        ach = atomics_per_k2 / (kern["forward_warp"]["avg_ms"] / 1e3) / 1e9
+        out["roofline_atomic"] = {
+            "bound": "l2_atomic", "kernel": "forward_warp", "achieved": ach,
+            "peak": peak_red, "unit": "G atomics/s", "frac": ach / peak_red,
+            "atomics_per_launch": atomics_per_k2,
+            "peak_source": f"profiles/r02_peaks.json {canvas}/warp_consecutive (tools/peaks.cu, "
+                           f"measured); random scatter: {red.get(canvas + '/random')}"}
+    fp = dpk.get("fp64", {}).get("dfma_per_s")
+    iss = dpk.get("issue", {}).get("ffma_warp_inst_per_s")
+    if captured and fp and iss:
+        for name in ("forward_warp", "resolve"):
+            f = facts.get(KERNEL_NAMES[name], {})
+            if name not in kern or not f:
+                continue
+            t = kern[name]["avg_ms"] / 1e3
+            out.setdefault("roofline_fp64", {})[name] = {
+                "achieved": f["fp64_thread_ops"] / t, "peak": fp, "unit": "FP64 thread ops/s",
+                "frac": f["fp64_thread_ops"] / t / fp,
+                "fp64_ops_per_launch": f["fp64_thread_ops"],
+                "ncu_fp64_pipe_pct_active": f["fp64_pipe_pct_active"]}
+            out.setdefault("roofline_issue", {})[name] = {
+                "achieved": f["warp_inst"] / t, "peak": iss, "unit": "warp instructions/s",
+                "frac": f["warp_inst"] / t / iss, "inst_per_launch": f["warp_inst"]}
+        for key in ("roofline_fp64", "roofline_issue"):
+            if key in out:
+                out[key]["source"] = ("per-launch counts: ncu capture of this config "
+                                      "(profiles/r02_kernel_facts.json); peaks: "
+                                      "profiles/r02_peaks.json (DFMA lanes/s, FFMA warp "
+                                      "instructions/s, measured)")
+    return out
+
+
+def wire_frame(caps, depth_range):
+    """A frame as the edge server receives it on the wire (pipeline.py:
+    390-394, 466-472): RGB + the live depth quantised to 12-bit inverse-depth
+    codes (FG Valid -> codes, BG Background -> 0, holes Invalid -> 1) packed
+    as YUV420, made by this package's capture-side codec on the GPU."""
+    from paper_2007_00558_b200 import depthcodec
+
+    out = {}
+    for cid, c in caps.items():
+        c = host_capture(c)
+        img = depthcodec.pack_yuv420(depthcodec.quantize12(c.depth_frame(), depth_range))
+        out[cid] = (c.rgb, img.y, img.u, img.v)
+    return out
+
+
+def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
     """``e2e``: the same metric through the public host-memory API,
     ``engine.EdgeStream`` — every step's live inputs start in pinned host
-    memory (16-bit mm + validity sidecar + RGB of the step's reference
-    cameras), its rendered views end in pinned host memory; the H2D of step
-    s+1 and the D2H of step s-1 overlap step s (double-buffered, the device
-    output buffers rotate so a view is never overwritten while downloaded)."""
+    memory (RGB of the step's reference cameras + their depth: the 16-bit mm
+    raster + validity sidecar, or with ``wire`` the 12-bit YUV420 codes the
+    edge server receives), its rendered views end in pinned host memory; the
+    H2D of step s+1 and the D2H of step s-1 overlap step s (double-buffered,
+    the device output buffers rotate so a view is never overwritten while
+    downloaded); repeating ticks replay a captured CUDA graph."""
     import torch
 
     from paper_2007_00558_b200 import distributed as D
     from paper_2007_00558_b200.engine import EdgeStream
+    from paper_2007_00558_b200.types import DepthRange
 
     def pinned(a):
         a = host_array(a)
         return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory()
 
+    # pipeline.py:71-72: the depth codec's range
+    drange = DepthRange(0.5, 6.5) if wire else None
     # at most 8 distinct host frames rotate (c3's 300 would pin 11 GB)
-    host = [{cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm, fr[cid].validity))
-             for cid in fr} for fr in frames[:8]]
+    if wire:
+        host = [{cid: tuple(pinned(a) for a in t) for cid, t in wire_frame(fr, drange).items()}
+                for fr in frames[:8]]
+    else:
+        host = [{cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm, fr[cid].validity))
+                 for cid in fr} for fr in frames[:8]]
 
     def step_views(s):
         # c3: the e2e run cycles over the frames that have host copies
@@ -372,7 +478,8 @@ def run_e2e(args, wl, eng, frames, views, dev, stream):
         need = sorted({c for v in step_views(s) for c in wl.refs[v]})
         return {cid: host[s % len(host)][cid] for cid in need}
 
-    es = EdgeStream(eng, max(len(v) for v in views), depth=2)
+    es = EdgeStream(eng, max(len(v) for v in views), depth=2, depth_range=drange,
+                    graphs=not args.no_graphs)
 
     def run(start, n):
         nv_ = 0
@@ -401,10 +508,13 @@ def run_e2e(args, wl, eng, frames, views, dev, stream):
     return {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
             "h2d_bytes_per_step": (es.h2d_bytes - b0) // args.steps,
             "d2h_bytes_per_step": (es.d2h_bytes - d0) // args.steps,
-            "api": "engine.EdgeStream.submit: pinned H2D (FrameUploader, two copy streams) -> "
-                   "EdgeRenderer.ingest_mm_many + render (C ABI fvv_slots_ingest_mm, "
-                   "fvv_render_views) -> D2H (ResultDownloader, rotating device buffers), "
-                   "double-buffered",
+            "input": ("12-bit YUV420 depth codes (pipeline.py:466-472) + RGB" if wire else
+                      "16-bit mm + validity sidecar (mvdio.py:132) + RGB"),
+            "api": ("engine.EdgeStream.submit: pinned H2D (FrameUploader, two copy streams) -> "
+                    f"EdgeRenderer.{'ingest_yuv_many' if wire else 'ingest_mm_many'} + render "
+                    f"(C ABI {'fvv_slots_ingest_yuv' if wire else 'fvv_slots_ingest_mm'}, "
+                    "fvv_render_views; CUDA graph replays) -> D2H (ResultDownloader, rotating "
+                    "device buffers), double-buffered"),
             "ms_per_step": ms2 / args.steps}
 
 
@@ -509,7 +619,7 @@ def run_ours(args):
             ev.record(comm)
         landed[fi] = ev
 
-    def run_step(s, e, o):
+    def run_step(s, e, o, eager=False):
         fi = s % len(staged)
         vi = views[s % len(views)] if args.config == "c3" else views[0]
         fr = staged[fi]
@@ -519,9 +629,14 @@ def run_ours(args):
                 issue_broadcast(fi)
             cur.wait_event(landed.pop(fi))
             issue_broadcast((s + 1) % len(staged))
-        need = sorted({c for v in vi for c in wl.refs[v]})
-        e.ingest_mm_many({cid: fr[cid] for cid in need}, hole_closing=True)
-        e.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=o)
+        g = graphs.get((id(e), fi)) if graphs is not None and not eager else None
+        if g is not None:
+            g.replay()
+            graph_launches[0] += g.launches
+        else:
+            need = sorted({c for v in vi for c in wl.refs[v]})
+            e.ingest_mm_many({cid: fr[cid] for cid in need}, hole_closing=True)
+            e.render([wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi], out=o)
         if bcast:
             ev = torch.cuda.Event()
             ev.record(cur)
@@ -533,6 +648,22 @@ def run_ours(args):
         with torch.cuda.stream(pstreams[i]):
             return run_step(s, engs[i], outs[i])
 
+    # one CUDA graph per (pipeline, staged frame): the step's K0 -> K1 -> K2 ->
+    # K3 launch sequence replayed with one call (EdgeRenderer.capture_step);
+    # every graph is captured before the warm-up, outside the timed region
+    graphs = None if (args.no_graphs or args.config == "c3") else {}
+    graph_launches = [0]
+    if graphs is not None:
+        vi = views[0]
+        need = sorted({c for v in vi for c in wl.refs[v]})
+        for i, e in enumerate(engs):
+            with torch.cuda.stream(pstreams[i]):
+                for fi, fr in enumerate(staged):
+                    graphs[(id(e), fi)] = e.capture_step(
+                        {cid: fr[cid] for cid in need}, [wl.virtuals[v] for v in vi],
+                        [wl.refs[v] for v in vi], out=outs[i][:len(vi)])
+        torch.cuda.synchronize()
+
     for s in range(args.warmup):
         step(s)
     torch.cuda.synchronize()
@@ -543,6 +674,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     D.barrier()
     l0 = sum(e.ctx.launches() for e in engs)
+    g0 = graph_launches[0]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for st in pstreams:
@@ -554,7 +686,7 @@ def run_ours(args):
         stream.wait_stream(st)
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = sum(e.ctx.launches() for e in engs) - l0
+    launches = sum(e.ctx.launches() for e in engs) - l0 + graph_launches[0] - g0
     ms = e0.elapsed_time(e1)
     D.barrier()
     clk = clocks.stop() if clocks else None
@@ -567,14 +699,24 @@ def run_ours(args):
     # one pipeline, so no kernel shares the GPU with another frame's)
     eng.ctx.profile(True)
     for s in range(args.steps):
-        run_step(s, eng, out)
+        run_step(s, eng, out, eager=True)
     prof = eng.ctx.profile_read()
     eng.ctx.profile(False)
+    # untimed counting pass over the rotation: K2's z-buffer atomics per launch
+    eng.ctx.count_atomics(True)
+    n_count = max(len(staged), 1)
+    for s in range(n_count):
+        run_step(s, eng, out, eager=True)
+    atomics_per_k2 = eng.ctx.profile_atomics() / (n_count * max(len(views[0]), 1))
+    eng.ctx.count_atomics(False)
 
     # e2e: public API with host buffers (run_e2e)
-    e2e = None
+    e2e = e2e_mm = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, eng, frames, views, dev, stream)
+        # headline: the edge server's wire format (12-bit YUV420 depth);
+        # beside it the mm + validity sidecar form (MVD container, mvdio.py)
+        e2e = run_e2e(args, wl, eng, frames, views, dev, stream, wire=True)
+        e2e_mm = run_e2e(args, wl, eng, frames, views, dev, stream, wire=False)
     if rank != 0:
         return 0
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
@@ -594,42 +736,8 @@ def run_ours(args):
         kern[name]["share"] = prof[name][0] / tot_ms if tot_ms else None
     dom = max(kern, key=lambda n: prof[n][0])
     dom_bytes = per_kernel.get(dom)
-    # ncu DRAM bytes per launch of the same kernel, from the committed capture
-    # (tools/round_bench.sh: the default c1 step, reference mixing), so only
-    # for that configuration
-    captured = args.config == "c1" and not args.extensions
-    traffic = None
-    tfile = ROOT / "profiles" / "r01_traffic.json"
-    if tfile.exists() and captured:
-        kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
-              "resolve": "k_resolve_fast"}.get(dom)
-        traffic = json.loads(tfile.read_text()).get(kn)
-    roof = None
-    if dom_bytes:
-        ach = dom_bytes / (kern[dom]["avg_ms"] / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
-                "peak_source": peak_src}
-    # issue roofline of the same kernel: warp instructions per launch (ncu,
-    # committed capture) / event-timed launch duration, against the SM issue
-    # peak of 4 warp instructions per clock per SM (one per sub-partition)
-    issue = None
-    ifile = ROOT / "profiles" / "r01_inst.json"
-    if ifile.exists() and dom_bytes and captured:
-        kn = {"preprocess": "k_preprocess", "forward_warp": "k_forward_warp",
-              "resolve": "k_resolve_fast"}.get(dom)
-        inst = json.loads(ifile.read_text()).get(kn)
-        sm_clk = (clk or {}).get("sm_mhz") or 1965.0
-        if inst:
-            import torch as _t
-
-            nsm = _t.cuda.get_device_properties(dev).multi_processor_count
-            ach_i = inst / (kern[dom]["avg_ms"] / 1e3)
-            peak_i = 4.0 * nsm * sm_clk * 1e6
-            issue = {"kernel": dom, "achieved": ach_i, "peak": peak_i,
-                     "unit": "warp instructions/s", "frac": ach_i / peak_i,
-                     "inst_per_launch": inst, "note": "instruction count from the committed ncu "
-                     "capture (profiles/r01_inst.json); peak = 4 issue slots/clock/SM"}
+    rl = kernel_rooflines(args, kern, per_kernel, atomics_per_k2, hbm, peak_src)
+    roof = rl.pop("roofline", None)
     pipe = value / ws * b_view / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": ws, "steps": args.steps,
@@ -643,6 +751,8 @@ def run_ours(args):
                                          f"views sharded x{ws} + NCCL frame broadcast"),
                    "views_per_step": views_per_step, "frames_rotating": len(staged),
                    "pipelines": P,
+                   "launch": "CUDA graph replay per step (EdgeRenderer.capture_step)"
+                             if graphs is not None else "host launches",
                    "mode": "extensions (angular weights + inpainting)" if args.extensions
                            else "parity (reference semantics)",
                    "l2": f"inputs rotate over {len(staged)} pre-staged frames; per-step "
@@ -651,7 +761,7 @@ def run_ours(args):
                    "path": "mm decode + bilateral hole fill + forward warp + resolve/blend "
                            "(full edge-server path)"},
         "roofline": roof,
-        "roofline_issue": issue,
+        **rl,
         "roofline_pipeline": {"bytes_per_view": b_view, "achieved": pipe, "peak": hbm,
                               "unit": "GB/s", "frac": pipe / hbm,
                               "note": "SURVEY.md §8(d) B_view x views/s per GPU"},
@@ -659,6 +769,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
         "e2e": e2e,
+        "e2e_mm": e2e_mm,
         "cpu_baseline": cpu,
         "published_reference": {"value": 1000.0 / 30.0, "unit": "views/s",
                                 "source": "PAPER.md:505 (30 ms max on a GTX 1080)"},

@@ -107,6 +107,14 @@ int fvv_sync(fvv_ctx *ctx);
 const char *fvv_last_error(const fvv_ctx *ctx);
 const char *fvv_version(void);
 int64_t fvv_launch_count(const fvv_ctx *ctx); /* kernels launched by this context */
+/* 1: the canvases' generation tag lives in device memory and every view
+ * advances it with a kernel (k_gen_fill, which also does the periodic canvas
+ * fill), so the launch sequence of a view is identical from call to call and
+ * can be captured once in a CUDA graph and replayed (cudaStreamBeginCapture on
+ * the context's stream around fvv_slots_ingest_mm + fvv_render_views; the
+ * first call for a new view size must run outside capture, it allocates).
+ * 0 (default): the host keeps the tag and passes it as a kernel argument. */
+int fvv_ctx_device_generation(fvv_ctx *ctx, int32_t enable);
 
 /* Per-kernel device timing: when enabled, every launch is bracketed by CUDA
  * events on the context's stream (the stream the kernel runs on).
@@ -119,6 +127,11 @@ int64_t fvv_launch_count(const fvv_ctx *ctx); /* kernels launched by this contex
 #define FVV_K_OTHER 4
 int fvv_profile_enable(fvv_ctx *ctx, int32_t enable); /* also resets */
 int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches);
+/* Counting pass (not for timing: the counters add work): with 1, K2 counts
+ * the 64-bit z-buffer atomicMin operations it issues (counters reset);
+ * fvv_profile_atomics returns the count so far (synchronises). */
+int fvv_count_atomics(fvv_ctx *ctx, int32_t enable);
+int fvv_profile_atomics(fvv_ctx *ctx, int64_t *atomics);
 
 /* Numerics self-test of the shared-reciprocal division and K2's filtered
  * rint(f*x/z + c) against the correctly rounded __ddiv_rn path, on n seeded
@@ -303,6 +316,13 @@ int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
 int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
                         const uint8_t *u, const uint8_t *v, double z_near, double z_far,
                         int32_t hole_closing, float *depth_out, uint8_t *validity_out);
+/* fvv_slot_ingest_yuv for n cameras of a render tick in one K0 launch (one
+ * grid layer per camera), then one K1 over all of their fill candidates:
+ * the edge server's wire-format decode (pipeline.py:466-472,518-519). */
+int fvv_slots_ingest_yuv(fvv_ctx *ctx, int32_t n, const int32_t *slots,
+                         const uint8_t *const *rgb, const uint8_t *const *y,
+                         const uint8_t *const *u, const uint8_t *const *v, double z_near,
+                         double z_far, int32_t hole_closing);
 /* n_views views; view i blends slots ref_slots[i*n_refs .. +n_refs) in that
  * order with weights[i*n_refs ..] (NULL or <= 0 -> computed on device).
  * rgb_out: n_views*H*W*3; provenance_out: n_views*H*W or NULL. */

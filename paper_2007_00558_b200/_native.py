@@ -39,7 +39,8 @@ EXPORTS = (
     "fvv_quantize12", "fvv_pack_yuv420", "fvv_capture_encode", "fvv_slots_ingest_mm",
     "fvv_set_range_weights", "fvv_rice_stream_bound", "fvv_rice_encode_plane",
     "fvv_rice_decode_plane", "fvv_rice_decode_planes", "fvv_encode_mm", "fvv_rle_decode",
-    "fvv_rle_encode", "fvv_slot_reset",
+    "fvv_rle_encode", "fvv_slot_reset", "fvv_ctx_device_generation", "fvv_slots_ingest_yuv",
+    "fvv_profile_atomics", "fvv_count_atomics",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -98,6 +99,12 @@ _SIGS = {
     "fvv_slot_set_camera": ([_VP, _I32, C.POINTER(FvvCamera)], C.c_int),
     "fvv_slot_set_bg": ([_VP, _I32, _VP, _VP], C.c_int),
     "fvv_slot_reset": ([_VP, _I32], C.c_int),
+    "fvv_ctx_device_generation": ([_VP, _I32], C.c_int),
+    "fvv_profile_atomics": ([_VP, C.POINTER(C.c_int64)], C.c_int),
+    "fvv_count_atomics": ([_VP, _I32], C.c_int),
+    "fvv_slots_ingest_yuv": ([_VP, _I32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                              C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                              C.POINTER(C.c_void_p), _D, _D, _I32], C.c_int),
     "fvv_slot_ingest": ([_VP, _I32, _VP, _VP, _VP, _I32], C.c_int),
     "fvv_slot_ingest_mm": ([_VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP], C.c_int),
     "fvv_slot_ingest_yuv": ([_VP, _I32, _VP, _VP, _VP, _VP, _D, _D, _I32, _VP, _VP], C.c_int),
@@ -144,7 +151,8 @@ RANGE_TABLE_LEN = 3 * 255 * 255 + 1
 _DEFAULT_SIGMA_RANGE = 10.0  # depthproc.py:176
 # entry points that run K1 with the reference defaults when hole_closing != 0
 _DEFAULT_HOLE_CLOSING = frozenset((
-    "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slots_ingest_mm", "fvv_slot_ingest_yuv"))
+    "fvv_slot_ingest", "fvv_slot_ingest_mm", "fvv_slots_ingest_mm", "fvv_slot_ingest_yuv",
+    "fvv_slots_ingest_yuv"))
 
 
 def range_weight_table(sigma_range: float) -> np.ndarray:
@@ -270,6 +278,16 @@ class Context:
             self.check(self.lib.fvv_profile_read(self.h, kid, C.byref(ms), C.byref(n)))
             out[name] = (ms.value, n.value)
         return out
+
+    def count_atomics(self, enable: bool) -> None:
+        """Counting pass on/off (resets): K2 counts its z-buffer atomics."""
+        self.check(self.lib.fvv_count_atomics(self.h, int(bool(enable))), "count_atomics")
+
+    def profile_atomics(self) -> int:
+        """K2's z-buffer atomics counted since count_atomics(True)."""
+        n = C.c_int64()
+        self.check(self.lib.fvv_profile_atomics(self.h, C.byref(n)), "profile_atomics")
+        return int(n.value)
 
     def close(self) -> None:
         if getattr(self, "h", None):

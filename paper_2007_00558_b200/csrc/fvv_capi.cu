@@ -53,6 +53,11 @@ struct fvv_ctx {
     size_t canvas_cap = 0;  // keys allocated
     int cW = -1, cH = -1, cr = -1, cn = 0;
     int gen = -1;  // generation of the last view; -1 = canvases need a fill
+    // device-resident generation (fvv_ctx_device_generation): every view
+    // runs k_gen_fill, which advances dgen[0] on the device, so a captured
+    // CUDA graph of views stays correct when replayed
+    bool dev_gen = false;
+    int *dgen = nullptr;  // [generation, CTA counter]
     // per contribution: K2's exact z of every source pixel (zcap doubles each)
     double *zsrc = nullptr;
     size_t zcap = 0, zn = 0;
@@ -87,6 +92,11 @@ struct fvv_ctx {
     std::vector<cudaEvent_t> pool;
     double prof_ms[5] = {0, 0, 0, 0, 0};
     int64_t prof_n[5] = {0, 0, 0, 0, 0};
+    unsigned long long *prof_atomics = nullptr;  // [256] K2 z-buffer atomics while counting
+    bool count_atomics = false;
+    // dequantize12 of every 12-bit code for the depth range (dq_span, dq_zf)
+    float *dq = nullptr;
+    double dq_span = 0.0, dq_zf = 0.0;
 };
 
 namespace {
@@ -254,6 +264,21 @@ int bilateral_defaults(fvv_ctx *ctx, BilateralParams &p) {
     return bilateral_params(ctx, p, 2, 2.0, 10.0, 6);
 }
 
+// K0/K1 read a 12-bit code's depth from the context's table for the code's
+// depth range (built by k_dq_table with the exact formula, once per range)
+int dq_table(fvv_ctx *ctx, PreprocCore &c) {
+    if (!ctx->dq) CK(cudaMalloc(&ctx->dq, 4096 * sizeof(float)));
+    if (ctx->dq_span != c.inv_span || ctx->dq_zf != c.inv_zf) {
+        LAUNCH(launch_dq_table(ctx->dq, c.inv_span, c.inv_zf, ctx->stream));
+        // once per range: later calls may come on another stream
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dq_span = c.inv_span;
+        ctx->dq_zf = c.inv_zf;
+    }
+    c.dq = ctx->dq;
+    return FVV_OK;
+}
+
 // room for `px` K1 candidates (a batch's pixel count bounds it)
 int fill_list(fvv_ctx *ctx, size_t px, uint32_t *&cand, int *&ncand) {
     if (!ctx->ncand) CK(cudaMalloc(&ctx->ncand, sizeof(int)));
@@ -290,6 +315,15 @@ int ensure_canvas(fvv_ctx *ctx, int n, int W, int H, int r) {
     if (ctx->cW != W || ctx->cH != H || ctx->cr != r || ctx->cn < n) {
         ctx->cW = W; ctx->cH = H; ctx->cr = r; ctx->cn = n;
         ctx->gen = -1;
+    }
+    if (ctx->dev_gen) {
+        if (ctx->gen < 0) {   // new canvases: the device generation restarts
+            CK(cudaMemsetAsync(ctx->dgen, 0xFF, sizeof(int), ctx->stream));
+            ctx->gen = 0;
+        }
+        LAUNCH_K(FVV_K_FILL, launch_gen_fill(ctx->canvas, per * (size_t)ctx->cn + 2, ctx->dgen,
+                                             ctx->stream));
+        return FVV_OK;
     }
     // generation tags: keys of this view carry gen; anything else is empty.
     // One fill per 127 views instead of a clear per view.
@@ -447,8 +481,11 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
     wp.pitch = canvas_pitch(virt.width, r);
     wp.n = 2 * n;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
+    wp.gen_ptr = ctx->dev_gen ? ctx->dgen : nullptr;
+    wp.n_atomics = ctx->count_atomics ? ctx->prof_atomics : nullptr;
     ResolveParams rp{};
     rp.dst = dst;
+    rp.gen_ptr = wp.gen_ptr;
     rp.r = r;
     rp.window = cfg.crack_fill_window;
     rp.need = cfg.crack_fill_window * cfg.crack_fill_window / 2 + 1;
@@ -575,6 +612,9 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
     for (auto &s : ctx->tmp) s.release();
     cudaFree(ctx->canvas);
     cudaFree(ctx->zsrc);
+    cudaFree(ctx->dgen);
+    cudaFree(ctx->prof_atomics);
+    cudaFree(ctx->dq);
     cudaFree(ctx->rle.block);
     cudaFree(ctx->rle.n_runs);
     for (void *q : {(void *)ctx->rice.zz, (void *)ctx->rice.res, (void *)ctx->rice.skew,
@@ -646,6 +686,30 @@ int fvv_profile_enable(fvv_ctx *ctx, int32_t enable) {
     return FVV_OK;
 }
 
+int fvv_count_atomics(fvv_ctx *ctx, int32_t enable) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (enable) {
+        if (!ctx->prof_atomics) CK(cudaMalloc(&ctx->prof_atomics, 256 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(ctx->prof_atomics, 0, 256 * sizeof(unsigned long long), ctx->stream));
+    }
+    ctx->count_atomics = enable != 0;
+    return FVV_OK;
+}
+
+int fvv_profile_atomics(fvv_ctx *ctx, int64_t *atomics) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!atomics) return fail(ctx, FVV_EINVAL, "profile_atomics: NULL");
+    *atomics = 0;
+    if (!ctx->prof_atomics) return FVV_OK;
+    unsigned long long v[256];
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(v, ctx->prof_atomics, sizeof(v), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 256; ++i) *atomics += (int64_t)v[i];
+    return FVV_OK;
+}
+
 int fvv_profile_read(fvv_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches) {
     int rc = enter(ctx);
     if (rc) return rc;
@@ -695,6 +759,7 @@ int fvv_decode_yuv420_12(fvv_ctx *ctx, const uint8_t *y, const uint8_t *u, const
     p.y = y; p.u = u; p.v = v;
     p.inv_span = 1.0 / z_near - 1.0 / z_far;  // depthcodec.py:121
     p.inv_zf = 1.0 / z_far;
+    if ((rc = dq_table(ctx, p))) return rc;
     p.depth_out = depth_out;
     p.validity_out = validity_out;
     p.codes_out = codes_out;
@@ -717,6 +782,7 @@ int fvv_dequantize12(fvv_ctx *ctx, const uint16_t *codes, int32_t width, int32_t
     p.codes = codes;
     p.inv_span = 1.0 / z_near - 1.0 / z_far;
     p.inv_zf = 1.0 / z_far;
+    if ((rc = dq_table(ctx, p))) return rc;
     p.depth_out = depth_out;
     p.validity_out = validity_out;
     LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess(p, ctx->stream));
@@ -1019,6 +1085,19 @@ int fvv_slot_set_camera(fvv_ctx *ctx, int32_t slot, const fvv_camera *cam) {
     return slot_camera(ctx, ctx->slots[slot], *cam);
 }
 
+int fvv_ctx_device_generation(fvv_ctx *ctx, int32_t enable) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (enable && !ctx->dgen) CK(cudaMalloc(&ctx->dgen, 2 * sizeof(int)));
+    if (enable && !ctx->dev_gen) {
+        CK(cudaMemsetAsync(ctx->dgen, 0, 2 * sizeof(int), ctx->stream));
+        CK(cudaMemsetAsync(ctx->dgen, 0xFF, sizeof(int), ctx->stream));   // fill first
+    }
+    if (!enable && ctx->dev_gen) ctx->gen = -1;   // host rule restarts with a fill
+    ctx->dev_gen = enable != 0;
+    return FVV_OK;
+}
+
 int fvv_slot_reset(fvv_ctx *ctx, int32_t slot) {
     int rc = enter(ctx);
     if (rc) return rc;
@@ -1127,6 +1206,50 @@ int fvv_slots_ingest_mm(fvv_ctx *ctx, int32_t n, const int32_t *slots,
     return FVV_OK;
 }
 
+int fvv_slots_ingest_yuv(fvv_ctx *ctx, int32_t n, const int32_t *slots,
+                         const uint8_t *const *rgb, const uint8_t *const *y,
+                         const uint8_t *const *u, const uint8_t *const *v, double z_near,
+                         double z_far, int32_t hole_closing) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 0 || n > FVV_MAX_REFS || (n && (!slots || !rgb || !y || !u || !v)))
+        return fail(ctx, FVV_EINVAL, "slots_ingest_yuv: bad arguments");
+    if (!(0 < z_near && z_near < z_far)) return fail(ctx, FVV_EINVAL, "need 0 < z_near < z_far");
+    PreprocBatch b{};
+    if (hole_closing && (rc = bilateral_defaults(ctx, b.bil))) return rc;
+    b.n = n;
+    for (int i = 0; i < n; ++i) {
+        const int sl = slots[i];
+        if (sl < 0 || sl >= FVV_MAX_SLOTS || !ctx->slots[sl].has_cam)
+            return fail(ctx, FVV_EINVAL, "slot %d has no camera", sl);
+        if (!rgb[i] || !y[i] || !u[i] || !v[i])
+            return fail(ctx, FVV_EINVAL, "slots_ingest_yuv: NULL buffer");
+        Slot &s = ctx->slots[sl];
+        PreprocCore &c = b.cam[i];
+        c.W = s.cam.width;
+        c.H = s.cam.height;
+        c.src = kSrcYUV;
+        c.y = y[i];
+        c.u = u[i];
+        c.v = v[i];
+        // host-evaluated like numpy's 1/zn - 1/zf, 1/zf (depthcodec.py:113-125)
+        c.inv_span = 1.0 / z_near - 1.0 / z_far;
+        c.inv_zf = 1.0 / z_far;
+        if ((rc = dq_table(ctx, c))) return rc;
+        c.rgb = rgb[i];
+        c.texel = s.texel;
+        c.warp_depth = s.fgd;
+    }
+    if (hole_closing) {
+        size_t px = 0;
+        for (int i = 0; i < n; ++i) px += (size_t)b.cam[i].W * b.cam[i].H;
+        if ((rc = fill_list(ctx, px, b.cand, b.ncand))) return rc;
+    }
+    LAUNCH_K(FVV_K_PREPROCESS, launch_preprocess_batch(b, ctx->stream));
+    for (int i = 0; i < n; ++i) ctx->slots[slots[i]].has_frame = true;
+    return FVV_OK;
+}
+
 int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const uint8_t *y,
                         const uint8_t *u, const uint8_t *v, double z_near, double z_far,
                         int32_t hole_closing, float *depth_out, uint8_t *validity_out) {
@@ -1142,6 +1265,7 @@ int fvv_slot_ingest_yuv(fvv_ctx *ctx, int32_t slot, const uint8_t *rgb, const ui
     p.y = y; p.u = u; p.v = v;
     p.inv_span = 1.0 / z_near - 1.0 / z_far;
     p.inv_zf = 1.0 / z_far;
+    if ((rc = dq_table(ctx, p))) return rc;
     p.rgb = rgb;
     if (hole_closing && (rc = bilateral_defaults(ctx, p))) return rc;
     if ((rc = with_fill(ctx, p))) return rc;
@@ -1258,6 +1382,7 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     wp.pitch = canvas_pitch(dst->width, r);
     wp.n = 1;
     wp.gen_hi = (uint64_t)ctx->gen << kGenShift;
+    wp.gen_ptr = ctx->dev_gen ? ctx->dgen : nullptr;
     if ((rc = ensure_zsrc(ctx, 1, (size_t)src->width * src->height))) return rc;
     wp.c[0] = WarpContrib{s.dev, relative_pose(s.dev, dd), s.fgd, rx, ry, ctx->canvas + 1,
                           ctx->zsrc, b};
@@ -1269,6 +1394,7 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.need = cfg->crack_fill_window * cfg->crack_fill_window / 2 + 1;
     rp.pitch = wp.pitch;
     rp.gen = (uint64_t)ctx->gen;
+    rp.gen_ptr = wp.gen_ptr;
     rp.n_fg = layer_fg ? 1 : 0;
     rp.n_bg = layer_fg ? 0 : 1;
     rp.band_rel = cfg->depth_band_rel;

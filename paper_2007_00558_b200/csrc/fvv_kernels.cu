@@ -44,6 +44,46 @@ cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Device-resident canvas generation (graph-replayable views): g[0] is the
+// generation K2/K3 of the coming view read, g[1] a CTA counter. The host
+// rule of ensure_canvas, on the device: a previous generation <= 0 fills
+// every canvas with empty keys and restarts at 126, else it counts down. All
+// CTAs read g[0] before the last one to finish (counter) writes it.
+__global__ void k_gen_fill(uint64_t *p, size_t n, int *g) {
+    __shared__ int prev;
+    if (threadIdx.x == 0) prev = *(volatile int *)g;
+    __syncthreads();
+    const int old = prev;
+    if (old <= 0) {
+        // 16-byte stores from the first 16-byte aligned key on
+        const size_t head = (reinterpret_cast<uintptr_t>(p) & 15) ? 1 : 0;
+        const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const size_t stride = (size_t)gridDim.x * blockDim.x;
+        if (t == 0 && head) p[0] = kEmpty;
+        ulonglong2 *q = reinterpret_cast<ulonglong2 *>(p + head);
+        const size_t n2 = (n - head) / 2;
+        for (size_t i = t; i < n2; i += stride) q[i] = make_ulonglong2(kEmpty, kEmpty);
+        if (t == 0 && ((n - head) & 1)) p[n - 1] = kEmpty;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(reinterpret_cast<unsigned *>(g + 1), 1u);
+        if (t == gridDim.x - 1) {
+            *(volatile int *)g = old <= 0 ? 126 : old - 1;
+            *(volatile int *)(g + 1) = 0;
+            __threadfence();
+        }
+    }
+}
+
+cudaError_t launch_gen_fill(uint64_t *p, size_t n, int *g, cudaStream_t s) {
+    // one CTA per SM: cheap when only the generation advances (126 of 127
+    // views), enough 16-byte stores in flight for the periodic fill
+    k_gen_fill<<<148, 512, 0, s>>>(p, n, g);
+    return cudaGetLastError();
+}
+
 // ray slopes (u - cx)/fx and (v - cy)/fy, core.py:224-227
 __global__ void k_rays(DevCam c, double *rx, double *ry) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -102,6 +142,25 @@ __device__ __forceinline__ void decode_mm(uint32_t mm, uint8_t &val, float &z) {
     z = (val == FVV_VALID) ? mm_to_m(mm) : 0.0f;
 }
 
+// depthcodec.dequantize_codes (depthcodec.py:113-125) of one code >= 2:
+// f64 frac = (c - 2) / 4093, z = 1 / (frac * inv_span + inv_zf), cast to f32
+__device__ __forceinline__ float dequant_code(uint32_t c, double inv_span, double inv_zf) {
+    const double frac = ddiv((double)c - 2.0, 4093.0);
+    return __double2float_rn(ddiv(1.0, dadd(dmul(frac, inv_span), inv_zf)));
+}
+
+// the 4096-entry table of dequant_code for one depth range (entries 0, 1:
+// the reserved codes, unused)
+__global__ void k_dq_table(float *t, double inv_span, double inv_zf) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < 4096) t[c] = c < 2 ? 0.0f : dequant_code((uint32_t)c, inv_span, inv_zf);
+}
+
+cudaError_t launch_dq_table(float *t, double inv_span, double inv_zf, cudaStream_t s) {
+    k_dq_table<<<16, 256, 0, s>>>(t, inv_span, inv_zf);
+    return cudaGetLastError();
+}
+
 // depthcodec.dequantize12 / dequantize_codes (depthcodec.py:113-138)
 __device__ __forceinline__ void decode_code(const PreprocCore &p, uint32_t c, uint8_t &val,
                                             float &z) {
@@ -110,8 +169,24 @@ __device__ __forceinline__ void decode_code(const PreprocCore &p, uint32_t c, ui
         z = 0.0f;
     } else {
         val = FVV_VALID;
-        const double frac = ddiv((double)c - 2.0, 4093.0);
-        z = __double2float_rn(ddiv(1.0, dadd(dmul(frac, p.inv_span), p.inv_zf)));
+        z = p.dq ? __ldg(p.dq + c) : dequant_code(c, p.inv_span, p.inv_zf);
+    }
+}
+
+// codes of 4 consecutive pixels xb..xb+3 (xb % 4 == 0) of row iy from the
+// Y word (4 LSB bytes) and the 2 chroma bytes of the U (even rows) or V (odd
+// rows) plane that cover them (yuv_code, depthcodec.py:154-177, 213-222)
+__device__ __forceinline__ void yuv_codes4(uint32_t yw, uint32_t cw, uint32_t code[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t c = (cw >> (8 * (q >> 1))) & 0xFFu;
+        const uint32_t sh = (q & 1) ? 0u : 1u;   // even column: odd bit positions
+        uint32_t msb = 0;
+#pragma unroll
+        for (int bit = 0; bit < 4; ++bit) msb |= ((c >> (2 * bit + sh)) & 1u) << bit;
+        uint32_t lsb = (yw >> (8 * q)) & 0xFFu;
+        if (msb & 1u) lsb = 255u - lsb;
+        code[q] = (msb << 8) | lsb;
     }
 }
 
@@ -169,13 +244,22 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
 #pragma unroll
     for (int r = 0; r < PROWS; ++r) {
         const int iy = y0 + ty + 8 * r;
-        vec[r] = iy < p.H && xb + 3 < p.W && (p.W & 3) == 0 && p.src == kSrcMM && p.rgb &&
-                 p.validity;
+        vec[r] = iy < p.H && xb + 3 < p.W && (p.W & 3) == 0 && p.rgb &&
+                 ((p.src == kSrcMM && p.validity) || p.src == kSrcYUV);
         if (vec[r]) {
             // 16-B aligned vector path (W % 4 == 0; torch/cudaMalloc bases are 256-B aligned)
             const size_t i0 = (size_t)iy * p.W + xb;
-            rm[r] = __ldcs(reinterpret_cast<const uint2 *>(p.mm + i0));
-            rv[r] = __ldcs(reinterpret_cast<const uint32_t *>(p.validity + i0));
+            if (p.src == kSrcMM) {
+                rm[r] = __ldcs(reinterpret_cast<const uint2 *>(p.mm + i0));
+                rv[r] = __ldcs(reinterpret_cast<const uint32_t *>(p.validity + i0));
+            } else {
+                // wire format: 4 Y bytes + the 2 chroma bytes under them
+                const uint8_t *plane = (iy & 1) ? p.v : p.u;
+                rm[r].x = __ldcs(reinterpret_cast<const uint32_t *>(p.y + i0));
+                rm[r].y = __ldcs(reinterpret_cast<const uint16_t *>(
+                    plane + (size_t)(iy >> 1) * (p.W >> 1) + (xb >> 1)));
+                rv[r] = 0;
+            }
             const uint32_t *c3 = reinterpret_cast<const uint32_t *>(p.rgb + i0 * 3);
             rc[r][0] = __ldcs(c3);
             rc[r][1] = __ldcs(c3 + 1);
@@ -195,7 +279,11 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
         uint8_t val[4];
         uchar4 g[4];
         uint32_t code[4] = {0, 0, 0, 0};
-        if (vec[r]) {
+        if (vec[r] && p.src == kSrcYUV) {
+            yuv_codes4(rm[r].x, rm[r].y, code);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) decode_code(p, code[q], val[q], z[q]);
+        } else if (vec[r]) {
             const uint32_t mm4[4] = {rm[r].x & 0xFFFFu, rm[r].x >> 16, rm[r].y & 0xFFFFu,
                                      rm[r].y >> 16};
 #pragma unroll
@@ -203,6 +291,8 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                 val[q] = (uint8_t)(rv[r] >> (8 * q));
                 decode_mm(mm4[q], val[q], z[q]);
             }
+        }
+        if (vec[r]) {
             const uint32_t ca = rc[r][0], cb = rc[r][1], cc = rc[r][2];
             g[0] = make_uchar4(ca & 255, (ca >> 8) & 255, (ca >> 16) & 255, 0);
             g[1] = make_uchar4(ca >> 24, cb & 255, (cb >> 8) & 255, 0);
@@ -330,6 +420,17 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
             sv[ry * SC + rx] = vv;
         }
         __syncthreads();
+        // no Valid pixel in the tile and its ring (sky, ray misses): no
+        // candidate can reach min_valid > 0, skip the per-pixel counts
+        {
+            const int nw = (SR * SC + 3) / 4;
+            int anyv = 0;
+            for (int i = tid; i < nw; i += 256) {
+                const uint32_t w = reinterpret_cast<const uint32_t *>(sv)[i];
+                anyv |= __vcmpeq4(w, 0u) != 0u;   // a Valid (0) byte
+            }
+            if (!__syncthreads_or(anyv) && bl.min_valid > 0) return;
+        }
         unsigned cm[PROWS][4];
         int wc = 0;
 #pragma unroll
@@ -647,7 +748,8 @@ __global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const 
     // the row part of the rotated ray, once per thread (its 4 pixels share a row)
     const double q0 = rel_q(c.rel, 0, ry), q1 = rel_q(c.rel, 1, ry), q2 = rel_q(c.rel, 2, ry);
     const bool fgk = p.tf.flag && (int)blockIdx.z < p.tf.n_fg;
-    const uint8_t gen8 = (uint8_t)(p.gen_hi >> kGenShift);
+    const uint64_t gen_hi = p.gen_ptr ? (uint64_t)__ldg(p.gen_ptr) << kGenShift : p.gen_hi;
+    const uint8_t gen8 = (uint8_t)(gen_hi >> kGenShift);
     int first_t = -1, last_t = -1;
     double zq[K2_PX];
     unsigned stored = 0;
@@ -673,7 +775,7 @@ __global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const 
         if (!(ur >= lo && ur < uhi && vr >= lo && vr < vhi)) continue;
         const size_t cell = (size_t)((int)vr + r) * P + (size_t)((int)ur + r);
         atomicMin((unsigned long long *)(c.canvas + cell),
-                  (unsigned long long)(p.gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
+                  (unsigned long long)(gen_hi | zkey(z, (uint32_t)(row + su), c.b)));
         if (fgk) {
             // the K3 tile of the target (padding columns/rows clamp to the edge
             // tiles, whose neighbourhood check covers them); a plain store
@@ -691,6 +793,16 @@ __global__ void __launch_bounds__(K2_THREADS, FVV_K2_MINB) k_forward_warp(const 
         }
         zq[q] = z;
         stored |= 1u << q;
+    }
+    if (p.n_atomics) {
+        // counting pass (untimed): the warp's z-buffer atomics, added to one
+        // of 256 counters (the host sums them) so the adds do not serialise
+        unsigned n = __popc(stored);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        const unsigned slot = (blockIdx.x * 131u + blockIdx.y * 31u + blockIdx.z * 7u +
+                               (threadIdx.x >> 5)) & 255u;
+        if ((threadIdx.x & 31) == 0 && n) atomicAdd(p.n_atomics + slot, (unsigned long long)n);
     }
     if (fgk) {
         // lanes hold consecutive source pixels: one store per run of a tile
@@ -802,6 +914,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
     const int Wd = dst.W, Hd = dst.H;
     const int ix = x0 + tx, iy = y0 + ty;
     const bool inimg = ix < Wd && iy < Hd;
+    const uint64_t gen = p.gen_ptr ? (uint64_t)__ldg(p.gen_ptr) : p.gen;
     const size_t pix = (size_t)iy * Wd + ix;
     const int r = p.r, rc = p.window >> 1;
     const int Hh = (r > 1 ? r : 1) + rc;
@@ -833,7 +946,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
                 uint64_t key = kEmpty;
                 if (cy >= 0 && cy < Hc && cx >= 0 && cx < Wc) {
                     const uint64_t v = c.canvas[(size_t)cy * p.pitch + cx];
-                    if ((v >> kGenShift) == p.gen) { key = v; any = 1; }
+                    if ((v >> kGenShift) == gen) { key = v; any = 1; }
                 }
                 sk[i] = key;
             }
@@ -1372,7 +1485,7 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     const size_t pix = (size_t)iy * Wd + ix;
     const int P = p.pitch, Hc = Hd + 2;
     const size_t plane = (size_t)Wd * Hd;
-    const uint64_t gen = p.gen;
+    const uint64_t gen = p.gen_ptr ? (uint64_t)__ldg(p.gen_ptr) : p.gen;
     const int ntot = p.n_fg + p.n_bg;
     // the contributions this tile resolves, in reference order: every BG
     // contribution, and the FG ones K2 flagged near this tile (all of them

@@ -24,6 +24,8 @@ struct PreprocCore {
     const uint8_t *y, *u, *v;// kSrcYUV
     const uint16_t *codes;   // kSrcCodes
     double inv_span, inv_zf; // kSrcYUV/Codes: 1/zn - 1/zf, 1/zf (host-evaluated like numpy)
+    const float *dq;         // kSrcYUV/Codes: dequantize12 of every code 0..4095 for
+                             // (inv_span, inv_zf) (k_dq_table; same formula), or null
     const uint8_t *rgb;      // guide / colour (H*W*3)
     const uint8_t *color_valid; // optional explicit colour-valid mask -> flag bit 0
     // outputs (any may be null)
@@ -112,6 +114,8 @@ struct WarpParams {
     int pitch;
     int n;
     uint64_t gen_hi;         // generation code << 57
+    const int *gen_ptr;      // non-null: the generation is read from here (k_gen_fill)
+    unsigned long long *n_atomics;  // non-null (profiling): += atomics issued
     TileFlags tf;
     WarpContrib c[2 * FVV_MAX_REFS];
 };
@@ -139,6 +143,7 @@ struct ResolveParams {
     int r, window, need;
     int pitch;
     uint64_t gen;            // generation code (0..127)
+    const int *gen_ptr;      // non-null: the generation is read from here (k_gen_fill)
     TileFlags tf;            // FG tile occupancy written by K2 (fast path, non-debug)
     int n_fg, n_bg;
     double band_rel;
@@ -194,6 +199,8 @@ cudaError_t launch_selftest_div(long long n, uint64_t seed, int mode, unsigned l
 cudaError_t launch_inpaint(const InpaintParams &p, cudaStream_t s);
 int take_extra_launches();  // kernels beyond one issued by the last launcher call
 cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t s);
+cudaError_t launch_dq_table(float *t, double inv_span, double inv_zf, cudaStream_t s);
+cudaError_t launch_gen_fill(uint64_t *p, size_t n, int *g, cudaStream_t s);
 size_t resolve_smem_bytes(int maxr);
 int resolve_tile_rows();  // K3 fast-path tile height (the tile width is 32)
 

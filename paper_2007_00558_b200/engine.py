@@ -194,6 +194,36 @@ class EdgeRenderer:
                       int(bool(hole_closing)), None, None)
         self.ingested.add(cid)
 
+    def ingest_yuv_many(self, frames: Mapping, depth_range, hole_closing: bool = True) -> None:
+        """``{cam_id: (rgb, y, u, v)}``, 12-bit YUV420 depth (pipeline.py:469-472),
+        in one K0 launch (one grid layer per camera) + one K1 — a render
+        tick's reference cameras in the edge server's wire format."""
+        self._bind()
+        items = list(frames.items())
+        n = len(items)
+        if n > _native.MAX_REFS:
+            for i in range(0, n, _native.MAX_REFS):
+                self.ingest_yuv_many(dict(items[i:i + _native.MAX_REFS]), depth_range,
+                                     hole_closing)
+            return
+        keep = []
+        for cid, (rgb, y, u, v) in items:
+            self._slot(cid)
+            H, W = self._hw(cid)
+            self._check(rgb, cid, "colour", 3)
+            self._check(y, cid, "Y plane")
+            for a, what in ((u, "U plane"), (v, "V plane")):
+                if tuple(a.shape) != (H // 2, W // 2):
+                    raise ValueError(f"camera {cid}: {what} has shape {tuple(a.shape)}, its "
+                                     f"calibration needs {(H // 2, W // 2)}")
+            keep.append(tuple(_dev.upload(a, np.uint8) for a in (rgb, y, u, v)))
+        arr = C.c_void_p * n
+        slots = (C.c_int32 * n)(*[self._slot(cid) for cid, _ in items])
+        self.ctx.call("fvv_slots_ingest_yuv", n, slots,
+                      *[arr(*[k[q].data_ptr() for k in keep]) for q in range(4)],
+                      float(depth_range.z_near), float(depth_range.z_far), int(bool(hole_closing)))
+        self.ingested.update(cid for cid, _ in items)
+
     def ingest_encoded_many(self, frames: Mapping, depth_range,
                             hole_closing: bool = True) -> None:
         """Live frames in the edge server's wire format, ``{cam_id: (rgb,
@@ -253,6 +283,47 @@ class EdgeRenderer:
                       C.byref(_native.synth_cfg(self.cfg)), out.data_ptr(), _dev.ptr(provenance))
         return out
 
+    def capture_step(self, frame: Mapping, virtuals: Sequence, refs=None,
+                     out: Optional[torch.Tensor] = None,
+                     provenance: Optional[torch.Tensor] = None,
+                     hole_closing: bool = True, depth_range=None) -> "StepGraph":
+        """One render tick — ``ingest_mm_many(frame)`` (K0 + K1; with
+        ``depth_range``, ``ingest_yuv_many(frame, depth_range)``) and
+        ``render(virtuals, refs)`` (K2 + K3) — captured once as a CUDA graph:
+        ``replay()`` re-runs the tick with one launch call, on whatever the
+        device buffers of ``frame`` (and the context's slots) hold by then.
+        The renderer's context switches to device-resident canvas generations
+        (``fvv_ctx_device_generation``), so replays stay correct. The tick is
+        run once eagerly first (allocations), which renders ``out``."""
+        self._bind()
+        self.ctx.call("fvv_ctx_device_generation", 1)
+        virtuals = list(virtuals)
+        k = virtuals[0].intrinsics
+        n, H, W = len(virtuals), int(k.height), int(k.width)
+        if out is None:
+            out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=self.ctx.device)
+        cur = torch.cuda.current_stream(self.ctx.device)
+
+        def tick():
+            if depth_range is None:
+                self.ingest_mm_many(frame, hole_closing=hole_closing)
+            else:
+                self.ingest_yuv_many(frame, depth_range, hole_closing=hole_closing)
+            self.render(virtuals, refs, out=out, provenance=provenance)
+
+        tick()
+        side = torch.cuda.Stream(self.ctx.device)
+        side.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        l0 = self.ctx.launches()
+        with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+            tick()
+        cur.wait_stream(side)
+        self._bind()
+        sg = StepGraph(self, g, out, frame)
+        sg.launches = self.ctx.launches() - l0    # kernels per replay
+        return sg
+
     def synthesize(self, virtual, mvd_frame: Optional[Mapping] = None, refs=None,
                    hole_closing: bool = True) -> ColorFrame:
         """One view on the host: optional new frame (``{id: MvdFrame}``), then render."""
@@ -261,6 +332,21 @@ class EdgeRenderer:
         img = self.render([virtual], None if refs is None else [refs])
         W, H = int(virtual.intrinsics.width), int(virtual.intrinsics.height)
         return ColorFrame(W, H, img[0].cpu().numpy())
+
+
+class StepGraph:
+    """A captured render tick (``EdgeRenderer.capture_step``): ``replay()``
+    launches the whole K0 -> K1 -> K2 -> K3 sequence as one CUDA graph on
+    the current stream; ``out`` receives the views."""
+
+    def __init__(self, renderer, graph, out, frame):
+        self.renderer, self.graph, self.out = renderer, graph, out
+        self._keep = frame           # the device buffers the graph reads
+        self.launches = None
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out
 
 
 _SESSION: list = []   # [(key, pinned objects, renderer)] of the last synthesize() call
@@ -449,16 +535,21 @@ class EdgeStream:
     out, with the H2D copies of frame t+1 and the D2H copy of view t-1
     overlapping frame t's decode/fill/warp/resolve on the renderer's stream.
 
-    ``submit(frame, virtuals, refs)`` takes ``{cam_id: (rgb, mm, validity)}``
-    (the 16-bit mm raster + validity sidecar, mvdio.py:132) and runs one
-    render tick (pipeline.py:514-547): upload, ``ingest_mm_many`` (K0 + K1),
-    ``render`` (K2 + K3), download. ``on_view(host_views, tag)`` receives each
-    tick's views once they are in host memory (pipeline.py:762-763
-    ``on_display``); ``flush()`` drains the last ones.
+    ``submit(frame, virtuals, refs)`` runs one render tick (pipeline.py:
+    514-547): upload, ingest (K0 + K1), render (K2 + K3), download. A frame is
+    ``{cam_id: (rgb, mm, validity)}`` — the 16-bit mm raster + validity
+    sidecar (mvdio.py:132) — or, with ``depth_range``, ``{cam_id: (rgb, y, u,
+    v)}`` — the 12-bit YUV420 depth the edge server receives on the wire
+    (pipeline.py:466-472). ``on_view(host_views, tag)`` receives each tick's
+    views once they are in host memory (pipeline.py:762-763 ``on_display``);
+    ``flush()`` drains the last ones. With ``graphs`` (default), a tick whose
+    buffers and views repeat is replayed from a CUDA graph captured on its
+    first occurrence (EdgeRenderer.capture_step).
     """
 
     def __init__(self, renderer: "EdgeRenderer", max_views: int, depth: int = 2,
-                 on_view=None, hole_closing: bool = True):
+                 on_view=None, hole_closing: bool = True, depth_range=None,
+                 graphs: bool = True):
         self.r = renderer
         dev = torch.device("cuda", renderer.ctx.device)
         self.dev = dev
@@ -468,6 +559,9 @@ class EdgeStream:
         self.depth = depth
         self.ups = {}
         self.hole_closing = hole_closing
+        self.depth_range = depth_range
+        self.graphs = {} if graphs else None
+        self.graph_launches = 0
 
     def _uploader(self, frame):
         key = tuple((cid, tuple(tuple(t.shape) for t in ts)) for cid, ts in sorted(frame.items()))
@@ -488,10 +582,27 @@ class EdgeStream:
         up = self._uploader(frame)
         ticket = up.put(dict(sorted(frame.items())))
         fr = up.get(ticket)
-        self.r.ingest_mm_many(fr, hole_closing=self.hole_closing)
         n = len(virtuals)
         out = self.dl.next_buffer()[:n]
-        self.r.render(virtuals, refs, out=out)
+        key = None
+        if self.graphs is not None and refs is not None:
+            key = (id(up), ticket % up.depth, self.dl.n % self.dl.depth,
+                   tuple(bytes(_native.camera(v)) for v in virtuals),
+                   tuple(tuple(r) for r in refs))
+        g = self.graphs.get(key) if key is not None else None
+        if g is not None:
+            g.replay()
+            self.graph_launches += g.launches
+        elif key is not None:
+            self.graphs[key] = self.r.capture_step(fr, virtuals, refs, out=out,
+                                                   hole_closing=self.hole_closing,
+                                                   depth_range=self.depth_range)
+        else:
+            if self.depth_range is None:
+                self.r.ingest_mm_many(fr, hole_closing=self.hole_closing)
+            else:
+                self.r.ingest_yuv_many(fr, self.depth_range, hole_closing=self.hole_closing)
+            self.r.render(virtuals, refs, out=out)
         up.release(ticket)
         return self.dl.put(out, tag)
 

@@ -133,6 +133,34 @@ def main():
             traffic.setdefault(name, []).append(b)
         print(json.dumps({k: sum(v) / len(v) for k, v in traffic.items()}, indent=1))
         return
+    if sys.argv[1] == "--facts":
+        # per kernel, averaged over its launches in the capture: what bench.py
+        # needs to put each kernel against its own roofline (DRAM bytes, warp
+        # instructions, FP64 thread operations, L2 RED requests per launch)
+        facts = {}
+        for d in raw_rows(sys.argv[2]):
+            name = d.get("Kernel Name", ("", ""))[0].split("(")[0].split("<")[0].replace(
+                "void ", "").replace("fvv::", "")
+            cyc = val(d, "sm__cycles_elapsed.avg") or 0
+            fp64 = sum((val(d, f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum."
+                                "per_cycle_elapsed") or 0) for op in ("dadd", "dmul", "dfma"))
+            f = {"duration_s": val(d, "gpu__time_duration.sum"),
+                 "dram_bytes": (val(d, "dram__bytes_read.sum") or 0) +
+                               (val(d, "dram__bytes_write.sum") or 0),
+                 "warp_inst": val(d, "smsp__inst_executed.sum"),
+                 "fp64_thread_ops": fp64 * cyc,
+                 "fp64_pipe_pct_active": val(d, "sm__pipe_fp64_cycles_active.avg."
+                                                "pct_of_peak_sustained_active"),
+                 "l2_red_requests": val(d, "lts__t_requests_srcunit_tex_op_red.sum"),
+                 "ipc_active": val(d, "sm__inst_executed.avg.per_cycle_active")}
+            facts.setdefault(name, []).append(f)
+        out = {}
+        for k, v in facts.items():
+            out[k] = {n: (sum(x[n] for x in v if x[n] is not None) / len(v)
+                          if any(x[n] is not None for x in v) else None) for n in v[0]}
+            out[k]["launches_captured"] = len(v)
+        print(json.dumps(out, indent=1))
+        return
     if sys.argv[1] == "--inst":
         inst = {}
         for d in raw_rows(sys.argv[2]):

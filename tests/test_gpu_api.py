@@ -606,3 +606,99 @@ def test_engine_rejects_rasters_that_do_not_fit_the_calibration(cuda):
     with pytest.raises(ValueError, match="shape"):
         e.render([case.virtual], [case.refs],
                  provenance=torch.empty((1, Hv - 1, Wv), dtype=torch.uint8, device=cuda))
+
+
+def test_captured_step_graph_replays_equal_eager_renders(cuda):
+    """EdgeRenderer.capture_step: a render tick (K0 + K1 + K2 + K3) captured
+    as a CUDA graph and replayed 300 times over two staged frames — across
+    the canvas-generation wrap-around (a fill every 127 views, now decided on
+    the device) — gives exactly the eager renders of the same frames."""
+    import torch
+
+    from paper_2007_00558_b200 import scenes
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    wl = scenes.make_workload("c0", scale=2)
+    v, refs = wl.virtuals[0], wl.refs[0]
+    host = _noised_frames(wl, refs, 2, 11)
+
+    def dev(fr):
+        return {cid: tuple(torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+                           .to(cuda) for a in t) for cid, t in fr.items()}
+
+    def renderer():
+        r = EdgeRenderer(wl.rig, private=True)
+        for cid in refs:
+            c = wl.frames[0][cid]
+            r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+        return r
+
+    eager = renderer()
+    want = []
+    for fr in host:
+        eager.ingest_mm_many(fr)
+        want.append(eager.render([v], [refs])[0].cpu().numpy())
+    assert not np.array_equal(want[0], want[1])
+
+    r = renderer()
+    staged = [dev(fr) for fr in host]
+    graphs = [r.capture_step(staged[i], [v], [refs]) for i in range(2)]
+    assert graphs[0].launches >= 4
+    for rep in range(300):
+        out = graphs[rep % 2].replay()
+        if rep % 37 == 0 or rep >= 296:
+            np.testing.assert_array_equal(out[0].cpu().numpy(), want[rep % 2],
+                                          err_msg=f"replay {rep}")
+    # eager calls on the same (now device-generation) context still agree
+    r.ingest_mm_many(staged[1])
+    np.testing.assert_array_equal(r.render([v], [refs])[0].cpu().numpy(), want[1])
+
+
+def test_edge_stream_wire_format_equals_per_camera_yuv_ingest(cuda):
+    """EdgeStream fed the edge server's wire format (12-bit YUV420 depth,
+    pipeline.py:466-472; batched fvv_slots_ingest_yuv, graph replays) gives
+    the views of per-camera ingest_yuv + render of the same frames."""
+    import torch
+
+    from paper_2007_00558_b200 import depthcodec, scenes
+    from paper_2007_00558_b200.engine import EdgeRenderer, EdgeStream
+    from paper_2007_00558_b200.types import DepthRange
+
+    wl = scenes.make_workload("c1", scale=4)
+    v, refs = wl.virtuals[0], wl.refs[0]
+    rng = DepthRange(0.5, 6.5)
+    frames = []
+    for fr in _noised_frames(wl, refs, 3, 5):
+        w = {}
+        for cid, (rgb, mm, val) in fr.items():
+            c = scenes.CameraCapture(wl.frames[0][cid].calib, rgb, mm, val,
+                                     wl.frames[0][cid].bg_depth, wl.frames[0][cid].bg_validity)
+            img = depthcodec.pack_yuv420(depthcodec.quantize12(c.depth_frame(), rng))
+            w[cid] = (rgb, img.y, img.u, img.v)
+        frames.append(w)
+
+    def renderer():
+        r = EdgeRenderer(wl.rig, private=True)
+        for cid in refs:
+            c = wl.frames[0][cid]
+            r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+        return r
+
+    sync = renderer()
+    want = []
+    for fr in frames:
+        for cid, (rgb, y, u, vv) in fr.items():
+            sync.ingest_yuv(cid, rgb, y, u, vv, rng)
+        want.append(sync.render([v], [refs])[0].cpu().numpy())
+    got = {}
+    es = EdgeStream(renderer(), 1, depth=2, depth_range=rng,
+                    on_view=lambda host, tag: got.__setitem__(tag, host[0].numpy().copy()))
+    for rep in range(2):
+        for i, fr in enumerate(frames):
+            pinned = {cid: tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in t)
+                      for cid, t in fr.items()}
+            es.submit(pinned, [v], [refs], tag=(rep, i))
+    es.flush()
+    assert es.graph_launches > 0
+    for (rep, i), img in got.items():
+        np.testing.assert_array_equal(img, want[i], err_msg=f"lap {rep}, frame {i}")
