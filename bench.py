@@ -79,10 +79,13 @@ def parse():
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
-    ap.add_argument("--no-graphs", action="store_true",
-                    help="launch every step's kernels from the host instead of replaying the "
-                         "step's CUDA graph (EdgeRenderer.capture_step); c3, whose every frame "
-                         "has its own view, always launches from the host")
+    ap.add_argument("--graphs", default="auto", choices=("auto", "on", "off"),
+                    help="replay each step as a captured CUDA graph (EdgeRenderer."
+                         "capture_step) instead of host launches; auto = on for c0, whose "
+                         "0.05 ms steps are bound by the host's launch calls, off for the "
+                         "GPU-bound configs (a graph's device-side canvas generation step "
+                         "costs c1 ~1%); c3, whose every frame has its own view, always "
+                         "launches from the host")
     ap.add_argument("--launch-check", action="store_true",
                     help="launcher/sharding check without GPU work (CPU, gloo): every rank "
                          "reports the views/frames it owns; rank 0 prints one JSON line")
@@ -94,6 +97,11 @@ def parse():
         args.gen = "gpu" if args.config in ("c3", "c4") else "host"
     if args.frames is None:
         args.frames = 300 if args.config == "c3" else 4
+    # the e2e leg (PCIe-bound) replays graphs unless they are switched off
+    args.e2e_graphs = args.graphs != "off"
+    if args.graphs == "auto":
+        args.graphs = "on" if args.config == "c0" else "off"
+    args.no_graphs = args.graphs == "off"
     if args.pipelines is None:
         args.pipelines = {"c0": 1, "c1": 3, "c3": 3}.get(args.config, 2)
     return args
@@ -479,7 +487,7 @@ def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
         return {cid: host[s % len(host)][cid] for cid in need}
 
     es = EdgeStream(eng, max(len(v) for v in views), depth=2, depth_range=drange,
-                    graphs=not args.no_graphs)
+                    graphs=args.e2e_graphs)
 
     def run(start, n):
         nv_ = 0

@@ -513,18 +513,25 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
     }
 }
 
-// Radius 2, the default: 4 candidates per warp, 8 lanes per candidate, lane
-// t evaluating taps t, t+8, t+16 (loads + table read + weight products);
-// the products go through shared memory and the group's first lane adds the
-// 24 taps in the reference's order. All 4 groups accumulate in the same
-// instructions, so a candidate costs ~1/4 of a warp pass.
+// Radius 2, the default: 32/LPC candidates per warp, LPC lanes per
+// candidate, lane t evaluating taps t, t+LPC, ... (loads + table read +
+// weight products); the products go through shared memory and the group's
+// first lane adds the 24 taps in the reference's order. All groups
+// accumulate in the same instructions. K1 is latency-bound (a chain of
+// dependent loads per candidate): 4 lanes per candidate (8 candidates per
+// warp pass, 6 independent taps per lane) halve the passes of 8 lanes.
+#ifndef FVV_K1_LPC
+#define FVV_K1_LPC 4
+#endif
+template <int LPC>
 __global__ void __launch_bounds__(256) k_fill_g8(const __grid_constant__ PreprocBatch batch) {
-    __shared__ double2 s_w[8][4][24];   // [warp][group][tap] = (w, w * z)
+    constexpr int G = 32 / LPC, TPL = 24 / LPC;   // candidates per warp, taps per lane
+    __shared__ double2 s_w[8][G][24];   // [warp][group][tap] = (w, w * z)
     const BilateralParams &bl = batch.bil;
     const int n = *batch.ncand;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 3, t = lane & 7;
-    const unsigned gmask = 0xFFu << (8 * g);
-    for (int base = (blockIdx.x * 8 + warp) * 4; base < n; base += gridDim.x * 8 * 4) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / LPC, t = lane % LPC;
+    const unsigned gmask = ((1u << LPC) - 1u) << (LPC * g);
+    for (int base = (blockIdx.x * 8 + warp) * G; base < n; base += gridDim.x * 8 * G) {
         const int e = base + g;
         const bool live = e < n;
         const uint32_t ent = live ? batch.cand[e] : 0u;
@@ -533,20 +540,27 @@ __global__ void __launch_bounds__(256) k_fill_g8(const __grid_constant__ Preproc
         const int y = i / p.W, x = i - y * p.W;
         const uchar4 gc = live ? load_rgb(p, (size_t)i) : make_uchar4(0, 0, 0, 0);
         int cnt = 0;
+        float zn[TPL];
+        bool ok[TPL];
+        uchar4 n4[TPL];
 #pragma unroll
-        for (int m = 0; m < 3; ++m) {
-            const int k = t + 8 * m, kk = k < 12 ? k : k + 1;  // skip the centre
-            float zn = 0.0f;
-            bool ok = false;
-            uchar4 n4 = make_uchar4(0, 0, 0, 0);
-            if (live) fill_tap(p, x, y, kk / 5 - 2, kk % 5 - 2, zn, ok, n4);
+        for (int m = 0; m < TPL; ++m) {   // every tap's loads first
+            const int k = t + LPC * m, kk = k < 12 ? k : k + 1;  // skip the centre
+            zn[m] = 0.0f;
+            ok[m] = false;
+            n4[m] = make_uchar4(0, 0, 0, 0);
+            if (live) fill_tap(p, x, y, kk / 5 - 2, kk % 5 - 2, zn[m], ok[m], n4[m]);
+        }
+#pragma unroll
+        for (int m = 0; m < TPL; ++m) {
+            const int k = t + LPC * m, kk = k < 12 ? k : k + 1;
             double w = 0.0;
-            if (ok) {
-                const int e0 = gc.x - n4.x, e1 = gc.y - n4.y, e2 = gc.z - n4.z;
+            if (ok[m]) {
+                const int e0 = gc.x - n4[m].x, e1 = gc.y - n4[m].y, e2 = gc.z - n4[m].z;
                 w = dmul(bl.sw[kk / 5][kk % 5], __ldg(bl.range_w + (e0 * e0 + e1 * e1 + e2 * e2)));
             }
-            s_w[warp][g][k] = make_double2(w, dmul(w, (double)zn));
-            cnt += __popc(__ballot_sync(0xffffffffu, ok) & gmask);
+            s_w[warp][g][k] = make_double2(w, dmul(w, (double)zn[m]));
+            cnt += __popc(__ballot_sync(0xffffffffu, ok[m]) & gmask);
         }
         __syncwarp();
         if (t == 0 && live) {
@@ -643,7 +657,7 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
     dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
     k_preprocess<<<grid, 256, 0, s>>>(b);
     if (fill) {
-        if (b.bil.radius == 2) k_fill_g8<<<148 * 4, 256, 0, s>>>(b);
+        if (b.bil.radius == 2) k_fill_g8<FVV_K1_LPC><<<148 * 4, 256, 0, s>>>(b);
         else k_fill<<<148 * 8, 256, 0, s>>>(b);
         ++t_extra_launches;
     }
@@ -1288,8 +1302,21 @@ __device__ __forceinline__ double key_z(const ResolveContrib &c, const DevCam &d
     return w_none(w) ? INFINITY : winner_z(c, dst, w_idx(w, c.b));
 }
 
+// compare-exchange of two non-NaN depths (finite or +inf): one compare and
+// selects (fmin + fmax would compare twice for their NaN rules)
+#ifndef FVV_K3_CSWAP1
+#define FVV_K3_CSWAP1 1
+#endif
+#ifndef FVV_K3_RAYRCP
+#define FVV_K3_RAYRCP 0
+#endif
 __device__ __forceinline__ void cswap(double &a, double &b) {
+#if FVV_K3_CSWAP1
+    const bool sw = b < a;
+    const double lo = sw ? b : a, hi = sw ? a : b;
+#else
     const double lo = fmin(a, b), hi = fmax(a, b);
+#endif
     a = lo;
     b = hi;
 }
@@ -1388,6 +1415,20 @@ double crack_z(const ResolveContrib &c, const DevCam &dst,
     return (cnt & 1) ? lo : dmul(dadd(lo, cnt == 6 ? v3 : v4), 0.5);
 }
 
+// np.clip(v, 0, hi) of a finite v: two compares and selects (fmin/fmax
+// would add their NaN handling)
+#ifndef FVV_K3_CLIP
+#define FVV_K3_CLIP 1
+#endif
+__device__ __forceinline__ double clip_finite(double v, double hi) {
+#if FVV_K3_CLIP
+    v = v < 0.0 ? 0.0 : v;
+    return v > hi ? hi : v;
+#else
+    return fmin(fmax(v, 0.0), hi);
+#endif
+}
+
 // backward projection + masked bilinear fetch of one covered pixel
 // (synthesis.py:224-247, _bilinear_fetch :128-159)
 __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst, double rxd,
@@ -1407,8 +1448,7 @@ __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst
     }
     if (!(us >= -0.5 && us <= (double)Ws - 0.5 && vs >= -0.5 && vs <= (double)Hs - 0.5))
         return false;
-    const double uc = fmin(fmax(us, 0.0), (double)(Ws - 1));
-    const double vc = fmin(fmax(vs, 0.0), (double)(Hs - 1));
+    const double uc = clip_finite(us, (double)(Ws - 1)), vc = clip_finite(vs, (double)(Hs - 1));
     const double u0 = floor(uc), v0 = floor(vc);
     const int iu = (int)u0, iv = (int)v0;
     const double fu = dsub(uc, u0), fv = dsub(vc, v0);
@@ -1551,9 +1591,15 @@ __global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_
     } else if (tid < 32 + TX + FTY) {
         // virtual-camera rays of the tile's columns and rows (pixel_rays,
         // core.py:224-227), once per CTA, while warp 0 picks the contributions
+        // (the correctly rounded quotient from a Newton reciprocal, div_rcp)
         const int t = tid - 32;
+#if FVV_K3_RAYRCP
+        if (t < TX) sray[t] = div_rcp(dsub((double)(x0 + t), dst.cx), dst.fx, rcp_nr(dst.fx));
+        else sray[t] = div_rcp(dsub((double)(y0 + t - TX), dst.cy), dst.fy, rcp_nr(dst.fy));
+#else
         if (t < TX) sray[t] = ddiv(dsub((double)(x0 + t), dst.cx), dst.fx);
         else sray[t] = ddiv(dsub((double)(y0 + t - TX), dst.cy), dst.fy);
+#endif
     }
     __syncthreads();
     const int nitems = s_nitems;

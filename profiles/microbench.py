@@ -68,6 +68,8 @@ def main():
     # without the hole fill, and of one view: the calls are captured into a
     # CUDA graph and replayed, so host submission gaps are excluded
     many = {c2: staged[c2] for c2 in wl.refs[0]}
+    # graph replays need the device-resident canvas generation
+    eng.ctx.call("fvv_ctx_device_generation", 1)
 
     def graphed(fn, n=20):
         fn()

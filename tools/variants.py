@@ -16,7 +16,7 @@ out.mkdir(parents=True, exist_ok=True)
 procs = []
 for spec in sys.argv[1:]:
     name, _, flags = spec.partition("=")
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-shared",
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
            *[f for f in flags.split(",") if f], "-o", str(out / f"{name}.so"),
            *[str(CSRC / s) for s in SOURCES]]
     procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
