@@ -464,33 +464,6 @@ int tile_flags(fvv_ctx *ctx, int n, int W, int H, WarpParams &wp, ResolveParams 
     return FVV_OK;
 }
 
-#ifndef FVV_ZSRC_BG
-#define FVV_ZSRC_BG 1
-#endif
-ResolveContrib resolve_contrib(const Slot &s, const Rel &back, const Rel &fwd, const double *zs,
-                               const float *depth, const uint64_t *canvas, double w, int b,
-                               uint32_t flag, int layer_fg) {
-    ResolveContrib c{};
-    c.src = s.dev;
-    c.rel = back;
-    c.texel = s.texel;
-    c.zsrc = zs;
-    c.depth = depth;
-    c.rx = s.rays;
-    c.ry = s.rays + s.cam.width;
-    c.fz[0] = fwd.M[6];
-    c.fz[1] = fwd.M[7];
-    c.fz[2] = fwd.M[8];
-    c.fz[3] = fwd.t[2];
-    c.inv_w = 1.0f / (float)s.cam.width;
-    c.canvas = canvas;
-    c.weight = w;
-    c.b = b;
-    c.flag = flag;
-    c.layer_fg = layer_fg;
-    return c;
-}
-
 // One view from n reference slots: K2 over 2n contributions, then K3.
 int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const double *weights,
                 int n, const fvv_synth_cfg &cfg, uint8_t *rgb_out, uint8_t *prov_out,
@@ -543,13 +516,12 @@ int render_view(fvv_ctx *ctx, const fvv_camera &virt, Slot *const *refs, const d
         for (int L = 0; L < 2; ++L) {
             const int k = L * n + j;
             const float *d = L == 0 ? s.fgd : s.bgd;
-            // FVV_ZSRC_BG 0: BG contributions (dense, ~every source scatters)
-            // skip K2's z store; K3 recomputes their winners' z
-            double *zs = (L == 1 && !FVV_ZSRC_BG) ? nullptr : ctx->zsrc + ctx->zcap * k;
-            const Rel fwd = relative_pose(s.dev, dst);
-            wp.c[k] = WarpContrib{s.dev, fwd, d, rx, ry, cbase + per * k, zs, b};
-            rp.c[k] = resolve_contrib(s, relative_pose(dst, s.dev), fwd, zs, d, cbase + per * k,
-                                      w, b, L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0);
+            double *zs = ctx->zsrc + ctx->zcap * k;
+            wp.c[k] = WarpContrib{s.dev, relative_pose(s.dev, dst), d, rx, ry, cbase + per * k,
+                                  zs, b};
+            rp.c[k] = ResolveContrib{s.dev, relative_pose(dst, s.dev), s.texel, zs,
+                                     cbase + per * k, w, b,
+                                     L == 0 ? kFlagLiveValid : kFlagLiveBackground, L == 0};
         }
     }
     rp.ang = cfg.angular_weight ? 1 : 0;
@@ -1431,9 +1403,9 @@ int fvv_warp_layer(fvv_ctx *ctx, const fvv_camera *src, const fvv_camera *dst, c
     rp.dbg.contrib_valid = valid_out;
     rp.dbg.contrib_winner = winner_out;
     rp.dbg.contrib_stage = stage_out;
-    rp.c[0] = resolve_contrib(s, relative_pose(dd, s.dev), relative_pose(s.dev, dd), ctx->zsrc,
-                              s.fgd, ctx->canvas + 1, host_weight(*src, *dst, cfg->mixing_epsilon),
-                              b, kFlagLiveValid, layer_fg ? 1 : 0);
+    rp.c[0] = ResolveContrib{s.dev, relative_pose(dd, s.dev), s.texel, ctx->zsrc, ctx->canvas + 1,
+                             host_weight(*src, *dst, cfg->mixing_epsilon), b, kFlagLiveValid,
+                             layer_fg ? 1 : 0};
     if (r == 1 && resolve_uses_tma() &&
         (rc = canvas_tensor_map(ctx, ctx->cn, dst->width, dst->height, r, rp)))
         return rc;

@@ -914,8 +914,6 @@ __device__ __forceinline__ double angular_factor(const DevCam &dst, const DevCam
     return 1.0 / ((double)acosf((float)cs) + eps);
 }
 
-__device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &, uint32_t idx);
-
 template <int MAXR>
 __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ ResolveParams p) {
     __shared__ uint64_t sk[KMAX];
@@ -1010,7 +1008,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
                         if (w != kEmpty) {
                             // exact f64 z of the winner, as K2 computed it
                             const uint32_t idx = (uint32_t)(w & ((1ull << c.b) - 1));
-                            zq = winner_z(c, dst, idx);
+                            zq = __ldg(c.zsrc + idx);
                             wq = (int)idx;
                         }
                     }
@@ -1280,17 +1278,7 @@ __device__ __forceinline__ uint32_t rgb_u8(double v) {
 // exact f64 z of a winner index: the value K2 computed and stored for it
 __device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam &,
                                            uint32_t idx) {
-    if (c.zsrc) return __ldg(c.zsrc + idx);
-    // K2's z of source pixel idx, the same operations (bit-identical):
-    // ((M20 rx) + ((M21 ry) + M22)) d + t2
-    const int Ws = c.src.W;
-    int sv = __float2int_rz((float)idx * c.inv_w);
-    sv -= sv * Ws > (int)idx;
-    sv += (sv + 1) * Ws <= (int)idx;
-    const int su = (int)idx - sv * Ws;
-    const double d = (double)__ldg(c.depth + idx);
-    const double q = dadd(dmul(c.fz[1], __ldg(c.ry + sv)), c.fz[2]);
-    return dadd(dmul(dadd(dmul(c.fz[0], __ldg(c.rx + su)), q), d), c.fz[3]);
+    return __ldg(c.zsrc + idx);
 }
 
 // A cell's winner as K3 keeps it in shared memory: the whole 64-bit key, or

@@ -124,13 +124,7 @@ struct ResolveContrib {
     DevCam src;
     Rel rel;                 // virtual camera -> src camera (relative_pose)
     const uint32_t *texel;
-    const double *zsrc;      // K2's exact z per source pixel (WarpContrib::zsrc), or
-                             // null: the winner's z is recomputed from the source
-                             // depth as K2 computed it (fz, depth, rx, ry below)
-    const float *depth;      // the contribution's source depth raster
-    const double *rx, *ry;   // src ray slope tables
-    double fz[4];            // src -> virtual z row: M20, M21, M22, t2 (WarpContrib::rel)
-    float inv_w;             // 1 / src width (winner index -> row)
+    const double *zsrc;      // K2's exact z per source pixel (WarpContrib::zsrc)
     const uint64_t *canvas;
     double weight;
     int b;
