@@ -319,6 +319,17 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def workload_config(args, wl) -> dict:
+    """The bench line's ``config``: what is measured, identical for both arms
+    (the reference arm runs the same workload through the CPU port); how it
+    is run goes to ``setup``."""
+    return {"workload": wl.description.split(" (")[0],
+            "mode": "extensions (angular weights + inpainting)" if args.extensions
+                    else "parity (reference semantics)",
+            "path": "mm decode + bilateral hole fill + forward warp + resolve/blend "
+                    "(full edge-server path)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
@@ -343,7 +354,9 @@ def run_reference(args):
             "warmup": args.warmup,
             "ms_per_step": 1e3 * total / len(walls), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.description, "views_per_step": threads},
+            "config": workload_config(args, wl),
+            "setup": {"views_per_step": threads, "threads": threads,
+                      "generator": wl.description},
             "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads,
                              "kind": "port", "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
@@ -754,20 +767,18 @@ def run_ours(args):
             ms_max / max(nviews, 1), "higher_is_better": True, "scaling": "weak",
         # 30 ms max synthesis time, 1080p, 3 refs
         "vs_baseline": (value / ws) / (1000.0 / 30.0) if args.config == "c1" else None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.description, "parallelism": f"replicas x{ws}" if args.config
-                   in ("c0", "c1") else (f"frames sharded x{ws}" if args.config == "c3" else
-                                         f"views sharded x{ws} + NCCL frame broadcast"),
-                   "views_per_step": views_per_step, "frames_rotating": len(staged),
-                   "pipelines": P,
-                   "launch": "CUDA graph replay per step (EdgeRenderer.capture_step)"
-                             if graphs is not None else "host launches",
-                   "mode": "extensions (angular weights + inpainting)" if args.extensions
-                           else "parity (reference semantics)",
-                   "l2": f"inputs rotate over {len(staged)} pre-staged frames; per-step "
-                         f"footprint (live inputs + BG models + 2R z canvases) exceeds the "
-                         f"126 MB L2 across the rotation",
-                   "path": "mm decode + bilateral hole fill + forward warp + resolve/blend "
-                           "(full edge-server path)"},
+        "config": workload_config(args, wl),
+        "setup": {"generator": wl.description,
+                  "parallelism": f"replicas x{ws}" if args.config in ("c0", "c1") else
+                                 (f"frames sharded x{ws}" if args.config == "c3" else
+                                  f"views sharded x{ws} + NCCL frame broadcast"),
+                  "views_per_step": views_per_step, "frames_rotating": len(staged),
+                  "pipelines": P,
+                  "launch": "CUDA graph replay per step (EdgeRenderer.capture_step)"
+                            if graphs is not None else "host launches",
+                  "l2": f"inputs rotate over {len(staged)} pre-staged frames; per-step "
+                        f"footprint (live inputs + BG models + 2R z canvases) exceeds the "
+                        f"126 MB L2 across the rotation"},
         "roofline": roof,
         **rl,
         "roofline_pipeline": {"bytes_per_view": b_view, "achieved": pipe, "peak": hbm,

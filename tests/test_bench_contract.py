@@ -45,6 +45,10 @@ def test_reference_arm_contract():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["sample"]
     assert cb["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    # the same workload description as the product arm's (bench.workload_config)
+    assert set(d["config"]) == {"workload", "mode", "path"}
+    assert d["config"]["workload"].startswith("c1: 1920x1080, 9 cams, 3 refs/view")
+    assert d["config"]["mode"] == "parity (reference semantics)"
 
 
 @pytest.mark.gpu
@@ -61,3 +65,7 @@ def test_product_arm_contract(cuda):
     assert "sm_mhz" in c and "reasons" in c
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert set(d["config"]) == {"workload", "mode", "path"}
+    for k in ("roofline_atomic", "kernels", "rank_ms", "e2e_mm", "setup"):
+        assert k in d, k
+    assert d["roofline_atomic"]["atomics_per_launch"] > 0
