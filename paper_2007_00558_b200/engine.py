@@ -38,7 +38,9 @@ class EdgeRenderer:
         different frames concurrently on different CUDA streams. The default
         shares the device's context (and its z canvases) but reserves its own
         camera slots in it, so renderers never see each other's frames; when
-        the shared context has too few free slots, a private one is made."""
+        the shared context has too few free slots, a private one is made.
+        Renderers sharing the context also share its z canvases: use them
+        from one stream at a time (or make them private)."""
         self.cfg = cfg or SynthesisConfig()
         self.rig = list(rig)
         self.by_id = {c.id: c for c in self.rig}
