@@ -520,6 +520,9 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
 // accumulate in the same instructions. K1 is latency-bound (a chain of
 // dependent loads per candidate): 4 lanes per candidate (8 candidates per
 // warp pass, 6 independent taps per lane) halve the passes of 8 lanes.
+#ifndef FVV_K1_CTAS
+#define FVV_K1_CTAS 4   // CTAs per SM of the K1 grid
+#endif
 #ifndef FVV_K1_LPC
 #define FVV_K1_LPC 4
 #endif
@@ -657,7 +660,7 @@ cudaError_t launch_preprocess_batch(const PreprocBatch &b, cudaStream_t s) {
     dim3 grid((W + PX - 1) / PX, (H + PY - 1) / PY, b.n);
     k_preprocess<<<grid, 256, 0, s>>>(b);
     if (fill) {
-        if (b.bil.radius == 2) k_fill_g8<FVV_K1_LPC><<<148 * 4, 256, 0, s>>>(b);
+        if (b.bil.radius == 2) k_fill_g8<FVV_K1_LPC><<<148 * FVV_K1_CTAS, 256, 0, s>>>(b);
         else k_fill<<<148 * 8, 256, 0, s>>>(b);
         ++t_extra_launches;
     }
