@@ -20,7 +20,8 @@ Three fixture families, all committed as compressed .npz:
   tests/test_acceptance.py:188-214.
 * ``full_<case>.npz`` — the reference's whole edge-server path (mm decode,
   bilateral hole fill, synthesize_view_debug) at BASELINE sizes: c0 640x360,
-  c1 1920x1080, frame 150 of the c3 stream, c4's rig at 1920x1080 (scale 2);
+  c1 1920x1080, view 4 of c2's jittered batch, frame 150 of the c3 stream,
+  c4's rig at 1920x1080 (scale 2);
   RGB as sha256 + sparse difference against the C oracle, masks bit-packed
   (``python tests/golden/make_golden.py full [case ...]``);
 * ``es_<case>.npz`` / ``codec.npz`` — edge-server preprocessing: reference
@@ -63,6 +64,7 @@ ES_CASES = [("c1_s4", "c1", 4, 2007), ("c0_s1", "c0", 1, 2007)]
 FULL_CASES = [
     ("c0", "c0", 1, 2007, 0),
     ("c1", "c1", 1, 2007, 0),
+    ("c2_v4", "c2", 1, 2007, 4),      # virtual camera 0.2 m off the arc, near its end
     ("c3_f150", "c3", 1, 2007, 150),
     ("c4_s2_v0", "c4", 2, 2007, 0),
 ]

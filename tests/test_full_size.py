@@ -14,7 +14,7 @@ from _helpers import full_inputs, golden, reference_rgb, rgb_agreement, sha, unp
 from oracle import c_oracle as CO
 from oracle import fvv_oracle as O
 
-CASES = ["c0", "c1", "c3_f150", "c4_s2_v0"]
+CASES = ["c0", "c1", "c2_v4", "c3_f150", "c4_s2_v0"]
 
 
 @pytest.mark.parametrize("case", CASES)

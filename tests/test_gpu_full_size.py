@@ -3,8 +3,9 @@
 Goldens ``full_<case>.npz`` (tests/golden/make_golden.py) hold the
 reference's whole edge-server path — ``depth_from_millimeters`` ->
 ``bilateral_close_holes`` -> ``synthesize_view_debug`` (pipeline.py:518-547)
-— at c0 640x360, c1 1920x1080, frame 150 of the c3 stream (moving spheres)
-and c4's 16-camera 4-reference rig at 1920x1080. Integer outputs (fill mask,
+— at c0 640x360, c1 1920x1080, view 4 of c2's batch (0.2 m off the arc),
+frame 150 of the c3 stream (moving spheres) and c4's 16-camera 4-reference
+rig at 1920x1080. Integer outputs (fill mask,
 per-contribution and merged validity, provenance) must be bit-exact, the
 filled f32 depths too; RGB within the north star's float tolerance (<= 1 LSB
 on >= 99.9 % of pixels, PSNR >= 50 dB), with the exact counts printed."""
@@ -19,7 +20,7 @@ from _helpers import full_inputs, golden, reference_rgb, rgb_agreement, sha, unp
 
 from oracle import c_oracle as CO
 
-CASES = ["c0", "c1", "c3_f150", "c4_s2_v0"]
+CASES = ["c0", "c1", "c2_v4", "c3_f150", "c4_s2_v0"]
 RESULTS = {}
 
 
