@@ -511,7 +511,9 @@ def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
         es.dl.wait_into(stream)
         return nv_
 
-    run(0, args.warmup)
+    # warm-up: at least two laps of the host-frame rotation, so every
+    # repeating tick has been captured as a graph before the timed steps
+    run(0, max(args.warmup, 2 * len(host) + 2))
     es.flush()
     torch.cuda.synchronize()
     D.barrier()

@@ -17,6 +17,7 @@ the north star names.
 from __future__ import annotations
 
 import ctypes as C
+from collections import OrderedDict
 from typing import Mapping, Optional, Sequence
 
 import numpy as np
@@ -545,13 +546,14 @@ class EdgeStream:
     (pipeline.py:466-472). ``on_view(host_views, tag)`` receives each tick's
     views once they are in host memory (pipeline.py:762-763 ``on_display``);
     ``flush()`` drains the last ones. With ``graphs`` (default), a tick whose
-    buffers and views repeat is replayed from a CUDA graph captured on its
-    first occurrence (EdgeRenderer.capture_step).
+    buffers, views and references repeat is replayed from a CUDA graph
+    captured on its second occurrence (EdgeRenderer.capture_step; at most
+    ``max_graphs`` kept, least recently used dropped).
     """
 
     def __init__(self, renderer: "EdgeRenderer", max_views: int, depth: int = 2,
                  on_view=None, hole_closing: bool = True, depth_range=None,
-                 graphs: bool = True):
+                 graphs: bool = True, max_graphs: int = 64):
         self.r = renderer
         dev = torch.device("cuda", renderer.ctx.device)
         self.dev = dev
@@ -562,7 +564,12 @@ class EdgeStream:
         self.ups = {}
         self.hole_closing = hole_closing
         self.depth_range = depth_range
-        self.graphs = {} if graphs else None
+        # ticks whose key (buffer slots, cameras, references) repeats are
+        # captured on their second occurrence; a moving viewer, whose every
+        # tick is new, stays on host launches (no capture per tick)
+        self.graphs = OrderedDict() if graphs else None
+        self.seen = OrderedDict()
+        self.max_graphs = max_graphs
         self.graph_launches = 0
 
     def _uploader(self, frame):
@@ -593,13 +600,22 @@ class EdgeStream:
                    tuple(tuple(r) for r in refs))
         g = self.graphs.get(key) if key is not None else None
         if g is not None:
+            self.graphs.move_to_end(key)
             g.replay()
             self.graph_launches += g.launches
-        elif key is not None:
+        elif key is not None and key in self.seen:
+            # a tick seen before (same buffers, views and references): capture
+            # it now (its eager run renders this tick) and replay it from then on
             self.graphs[key] = self.r.capture_step(fr, virtuals, refs, out=out,
                                                    hole_closing=self.hole_closing,
                                                    depth_range=self.depth_range)
+            if len(self.graphs) > self.max_graphs:
+                self.graphs.popitem(last=False)
         else:
+            if key is not None:
+                self.seen[key] = None
+                if len(self.seen) > 4 * self.max_graphs:
+                    self.seen.popitem(last=False)
             if self.depth_range is None:
                 self.r.ingest_mm_many(fr, hole_closing=self.hole_closing)
             else:
