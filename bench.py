@@ -477,27 +477,52 @@ def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
     from paper_2007_00558_b200.engine import EdgeStream
     from paper_2007_00558_b200.types import DepthRange
 
-    def pinned(a):
-        a = host_array(a)
-        return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory()
+    def as_tensor(a):
+        a = np.ascontiguousarray(host_array(a))
+        return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+
+    def pinned_tick(fr):
+        """A tick's rasters in ONE pinned host allocation, the way a receive
+        buffer holds them (FrameUploader then moves one span per copy lane)."""
+        ts = [(cid, [as_tensor(a) for a in arrays]) for cid, arrays in fr.items()]
+        sizes = [t.numel() * t.element_size() for _, v in ts for t in v]
+        flat = torch.empty(sum((n + 15) // 16 * 16 for n in sizes), dtype=torch.uint8).pin_memory()
+        out, off = {}, 0
+        for cid, v in ts:
+            tup = []
+            for t in v:
+                n = t.numel() * t.element_size()
+                dst = flat[off:off + n].view(t.dtype).view(tuple(t.shape))
+                dst.copy_(t)
+                tup.append(dst)
+                off += (n + 15) // 16 * 16
+            out[cid] = tuple(tup)
+        return out
 
     # pipeline.py:71-72: the depth codec's range
     drange = DepthRange(0.5, 6.5) if wire else None
-    # at most 8 distinct host frames rotate (c3's 300 would pin 11 GB)
-    if wire:
-        host = [{cid: tuple(pinned(a) for a in t) for cid, t in wire_frame(fr, drange).items()}
-                for fr in frames[:8]]
-    else:
-        host = [{cid: tuple(pinned(a) for a in (fr[cid].rgb, fr[cid].mm, fr[cid].validity))
-                 for cid in fr} for fr in frames[:8]]
+
+    def step_cams(s):
+        return sorted({c for v in step_views(s) for c in wl.refs[v]})
 
     def step_views(s):
         # c3: the e2e run cycles over the frames that have host copies
-        return views[s % len(host)] if args.config == "c3" else views[0]
+        return views[s % n_host] if args.config == "c3" else views[0]
+
+    # at most 8 distinct host ticks rotate (c3's 300 frames would pin 11 GB);
+    # each holds the step's reference cameras only
+    n_host = min(len(frames), 8)
+    host = []
+    for i, fr in enumerate(frames[:n_host]):
+        cams = step_cams(i)
+        sel = {cid: fr[cid] for cid in cams}
+        if wire:
+            host.append(pinned_tick(wire_frame(sel, drange)))
+        else:
+            host.append(pinned_tick({cid: (c.rgb, c.mm, c.validity) for cid, c in sel.items()}))
 
     def step_frame(s):
-        need = sorted({c for v in step_views(s) for c in wl.refs[v]})
-        return {cid: host[s % len(host)][cid] for cid in need}
+        return host[s % n_host]
 
     es = EdgeStream(eng, max(len(v) for v in views), depth=2, depth_range=drange,
                     graphs=args.e2e_graphs)

@@ -407,13 +407,46 @@ class FrameUploader:
         lanes = int(os.environ.get("FVV_UPLOAD_LANES", lanes or (2 if nbytes >= 8 << 20 else 1)))
         self.extra = [torch.cuda.Stream(self.dev) for _ in range(max(lanes, 1) - 1)]
         self.depth = depth
-        self.bufs = [{cid: tuple(torch.empty(tuple(t.shape), dtype=t.dtype, device=self.dev)
-                                 for t in ts) for cid, ts in example_frame.items()}
-                     for _ in range(depth)]
+        # a frame whose rasters all live in one host allocation (the way a
+        # receive buffer holds a tick's data) moves as one span per lane
+        # instead of one copy per raster
+        self.layout = self._layout(example_frame)
+        if self.layout is not None:
+            span = self.layout[1]
+            self.flat = [torch.empty(span, dtype=torch.uint8, device=self.dev)
+                         for _ in range(depth)]
+            self.bufs = [{cid: tuple(self._view(self.flat[d], o, t) for o, t in zip(offs, ts))
+                          for (cid, ts), offs in zip(example_frame.items(), self.layout[2])}
+                         for d in range(depth)]
+        else:
+            self.bufs = [{cid: tuple(torch.empty(tuple(t.shape), dtype=t.dtype, device=self.dev)
+                                     for t in ts) for cid, ts in example_frame.items()}
+                         for _ in range(depth)]
         self.done = [None] * depth        # copy-finished events
         self.free = [None] * depth        # consumer-finished events
         self.n = 0
         self.bytes = 0
+
+    @staticmethod
+    def _layout(frame: Mapping):
+        """(start, span bytes, [[byte offset per raster] per camera]) when
+        every raster is a contiguous view of one allocation (offsets relative
+        to the lowest raster), else None."""
+        ts = [t for v in frame.values() for t in v]
+        if not ts or not all(isinstance(t, torch.Tensor) and t.is_contiguous() for t in ts):
+            return None
+        base = ts[0].untyped_storage().data_ptr()
+        if any(t.untyped_storage().data_ptr() != base for t in ts):
+            return None
+        lo = min(t.data_ptr() for t in ts) - base
+        hi = max(t.data_ptr() + t.numel() * t.element_size() for t in ts) - base
+        offs = [[t.data_ptr() - base - lo for t in v] for v in frame.values()]
+        return lo, hi - lo, offs
+
+    @staticmethod
+    def _view(flat, off, t):
+        n = t.numel() * t.element_size()
+        return flat[off:off + n].view(t.dtype).view(tuple(t.shape))
 
     def put(self, frame: Mapping) -> int:
         slot = self.n % self.depth
@@ -421,13 +454,26 @@ class FrameUploader:
         for st in streams:
             if self.free[slot] is not None:
                 st.wait_event(self.free[slot])
-        pairs = [(dst, src) for cid, ts in frame.items()
-                 for dst, src in zip(self.bufs[slot][cid], ts)]
-        for li, st in enumerate(streams):
-            with torch.cuda.stream(st):
-                for dst, src in pairs[li::len(streams)]:
-                    dst.copy_(src, non_blocking=True)
-        self.bytes += sum(src.numel() * src.element_size() for _, src in pairs)
+        lay = self._layout(frame) if self.layout is not None else None
+        if lay is not None and lay[1:] == self.layout[1:]:
+            # one span, split evenly over the copy lanes
+            src = torch.empty(0, dtype=torch.uint8).set_(
+                next(iter(frame.values()))[0].untyped_storage(), lay[0], (lay[1],), (1,))
+            step = -(-lay[1] // len(streams) // 256) * 256
+            for li, st in enumerate(streams):
+                a, b = li * step, min((li + 1) * step, lay[1])
+                if a < b:
+                    with torch.cuda.stream(st):
+                        self.flat[slot][a:b].copy_(src[a:b], non_blocking=True)
+            self.bytes += sum(t.numel() * t.element_size() for v in frame.values() for t in v)
+        else:
+            pairs = [(dst, src) for cid, ts in frame.items()
+                     for dst, src in zip(self.bufs[slot][cid], ts)]
+            for li, st in enumerate(streams):
+                with torch.cuda.stream(st):
+                    for dst, src in pairs[li::len(streams)]:
+                        dst.copy_(src, non_blocking=True)
+            self.bytes += sum(src.numel() * src.element_size() for _, src in pairs)
         for st in self.extra:   # the ticket's event covers every lane
             ev_l = torch.cuda.Event()
             ev_l.record(st)

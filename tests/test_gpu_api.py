@@ -524,19 +524,43 @@ def test_edge_stream_downloads_equal_synchronous_renders(cuda):
     assert not all(np.array_equal(want[0], w) for w in want[1:])
 
     got = {}
-    es = EdgeStream(renderer(), 1, depth=2,
-                    on_view=lambda host, tag: got.__setitem__(tag, host[0].numpy().copy()))
-    for rep in range(3):   # several laps: buffers rotate while earlier copies are in flight
-        for i, fr in enumerate(frames):
-            pinned = {cid: tuple(torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16
-                                                  else a).pin_memory() for a in t)
-                      for cid, t in fr.items()}
-            es.submit(pinned, [v], [refs], tag=(rep, i))
-    es.flush()
-    assert len(got) == 3 * len(frames)
-    for (rep, i), img in got.items():
-        assert np.array_equal(img, want[i]), f"lap {rep}, frame {i}"
-    assert es.h2d_bytes == 3 * sum(a.nbytes for fr in frames for t in fr.values() for a in t)
+
+    def packed(fr):
+        """the tick's rasters in one pinned allocation (FrameUploader's span copy)"""
+        ts = {cid: [torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+                    for a in t] for cid, t in fr.items()}
+        n = sum((x.numel() * x.element_size() + 15) // 16 * 16 for v in ts.values() for x in v)
+        flat = torch.empty(n + 64, dtype=torch.uint8).pin_memory()
+        out, off = {}, 32
+        for cid, v in ts.items():
+            tup = []
+            for x in v:
+                m = x.numel() * x.element_size()
+                d = flat[off:off + m].view(x.dtype).view(tuple(x.shape))
+                d.copy_(x)
+                tup.append(d)
+                off += (m + 15) // 16 * 16
+            out[cid] = tuple(tup)
+        return out
+
+    for mode in ("per-raster", "one span"):
+        es = EdgeStream(renderer(), 1, depth=2,
+                        on_view=lambda host, tag: got.__setitem__(tag, host[0].numpy().copy()))
+        for rep in range(2):   # laps: buffers rotate while earlier copies are in flight
+            for i, fr in enumerate(frames):
+                if mode == "per-raster":
+                    pinned = {cid: tuple(torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16
+                                                          else a).pin_memory() for a in t)
+                              for cid, t in fr.items()}
+                else:
+                    pinned = packed(fr)
+                es.submit(pinned, [v], [refs], tag=(mode, rep, i))
+        es.flush()
+        assert (next(iter(es.ups.values())).layout is not None) == (mode == "one span")
+    assert len(got) == 4 * len(frames)
+    for (mode, rep, i), img in got.items():
+        assert np.array_equal(img, want[i]), f"{mode}, lap {rep}, frame {i}"
+    assert es.h2d_bytes == 2 * sum(a.nbytes for fr in frames for t in fr.values() for a in t)
 
 
 def test_renderers_sharing_a_context_keep_their_own_slots(cuda):
