@@ -404,13 +404,15 @@ class FrameUploader:
         # (FVV_UPLOAD_LANES overrides)
         import os
         nbytes = sum(t.numel() * t.element_size() for ts in example_frame.values() for t in ts)
+        # a frame whose rasters all live in one host allocation (the way a
+        # receive buffer holds a tick's data) moves as one span instead of
+        # one copy per raster (one lane: splitting the span measured no faster)
+        self.layout = self._layout(example_frame)
+        if self.layout is not None:
+            lanes = lanes or 1
         lanes = int(os.environ.get("FVV_UPLOAD_LANES", lanes or (2 if nbytes >= 8 << 20 else 1)))
         self.extra = [torch.cuda.Stream(self.dev) for _ in range(max(lanes, 1) - 1)]
         self.depth = depth
-        # a frame whose rasters all live in one host allocation (the way a
-        # receive buffer holds a tick's data) moves as one span per lane
-        # instead of one copy per raster
-        self.layout = self._layout(example_frame)
         if self.layout is not None:
             span = self.layout[1]
             self.flat = [torch.empty(span, dtype=torch.uint8, device=self.dev)
