@@ -407,3 +407,21 @@ def test_bench_gpus_2_launches_two_ranks():
 def test_bench_refuses_a_world_size_that_is_not_gpus():
     out = _bench("--gpus", "1", "--launch-check", env={"WORLD_SIZE": "2"})
     assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr
+
+
+def test_frame_uploader_recognises_a_single_span_tick():
+    """A tick whose rasters are views of one pinned allocation is uploaded as
+    one span (FrameUploader._layout: start, span, offsets from the start);
+    rasters in separate allocations keep one copy each."""
+    import torch
+
+    from paper_2007_00558_b200.engine import FrameUploader
+
+    flat = torch.empty(256, dtype=torch.uint8)
+    rgb = flat[32:44].view(2, 2, 3)
+    mm = flat[48:56].view(torch.int16).view(2, 2)
+    val = flat[64:68].view(2, 2)
+    assert FrameUploader._layout({7: (rgb, mm, val)}) == (32, 36, [[0, 16, 32]])
+    other = torch.empty(16, dtype=torch.uint8)[:4].view(2, 2)
+    assert FrameUploader._layout({7: (rgb, mm, other)}) is None
+    assert FrameUploader._layout({7: (rgb[:, :1],)}) is None   # not contiguous
