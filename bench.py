@@ -558,7 +558,8 @@ def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
             "d2h_bytes_per_step": (es.d2h_bytes - d0) // args.steps,
             "input": ("12-bit YUV420 depth codes (pipeline.py:466-472) + RGB" if wire else
                       "16-bit mm + validity sidecar (mvdio.py:132) + RGB"),
-            "api": ("engine.EdgeStream.submit: pinned H2D (FrameUploader, two copy streams) -> "
+            "api": ("engine.EdgeStream.submit: pinned H2D of the tick's single-span receive "
+                    "buffer (FrameUploader, copy stream) -> "
                     f"EdgeRenderer.{'ingest_yuv_many' if wire else 'ingest_mm_many'} + render "
                     f"(C ABI {'fvv_slots_ingest_yuv' if wire else 'fvv_slots_ingest_mm'}, "
                     "fvv_render_views; CUDA graph replays) -> D2H (ResultDownloader, rotating "
