@@ -352,13 +352,23 @@ int ensure_zsrc(fvv_ctx *ctx, int n, size_t px) {
     return FVV_OK;
 }
 
-// codec scratch for n pixels (ns in the skewed rebuild layout) and c chunks
-int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0) {
+// codec scratch for n pixels (ns in the skewed rebuild layout, ne strip-edge
+// slots) and c chunks
+int rice_scratch(fvv_ctx *ctx, size_t n, size_t c, size_t ns = 0, size_t ne = 0) {
     RiceScratch &r = ctx->rice;
     if (!r.costs) {
         CK(cudaMalloc(&r.costs, 2 * kRiceMaxPlanes * sizeof(unsigned long long)));
         CK(cudaMalloc(&r.total, kRiceMaxPlanes * sizeof(unsigned long long)));
         CK(cudaMalloc(&r.changed, sizeof(int)));
+        CK(cudaMalloc(&r.wave, 2 * sizeof(int)));
+    }
+    if (ne > r.e_cap) {
+        CK(cudaFree(r.edge));
+        r.edge = nullptr;
+        CK(cudaMalloc(&r.edge, ne * sizeof(unsigned long long)));
+        // no slot carries a tag (the rebuild runs on the same stream)
+        CK(cudaMemsetAsync(r.edge, 0, ne * sizeof(unsigned long long), ctx->stream));
+        r.e_cap = ne;
     }
     const size_t blocks = (n + 1023) / 1024 + 1;
     const size_t bneed = blocks > c + 1 ? blocks : c + 1;
@@ -621,7 +631,7 @@ int fvv_ctx_destroy(fvv_ctx *ctx) {
                     (void *)ctx->rice.block,
                     (void *)ctx->rice.costs, (void *)ctx->rice.total, (void *)ctx->rice.entry,
                     (void *)ctx->rice.exit, (void *)ctx->rice.exit_prev, (void *)ctx->rice.count,
-                    (void *)ctx->rice.changed})
+                    (void *)ctx->rice.changed, (void *)ctx->rice.edge, (void *)ctx->rice.wave})
         cudaFree(q);
     cudaFree(ctx->cand);
     cudaFree(ctx->tflag);
@@ -1033,7 +1043,7 @@ int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *stream
     NEED(streams && nbytes && ks && widths && heights && planes_out && adlers_out && status_out,
          "rice_decode_planes: NULL argument array");
     RicePlane pl[kRiceMaxPlanes];
-    size_t px = 0, skew = 0, chunks = 0;
+    size_t px = 0, skew = 0, edge = 0, chunks = 0;
     for (int i = 0; i < n; ++i) {
         NEED(widths[i] > 0 && heights[i] > 0 && planes_out[i] && nbytes[i] >= 0 &&
                  (streams[i] || !nbytes[i]),
@@ -1049,9 +1059,10 @@ int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *stream
         pl[i].out = planes_out[i];
         px += (size_t)widths[i] * heights[i];
         skew += rice_skew_size(widths[i], heights[i]);
+        edge += rice_edge_size(widths[i], heights[i]);
         chunks += (size_t)((nbytes[i] * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
     }
-    if ((rc = rice_scratch(ctx, px, chunks + n, skew))) return rc;
+    if ((rc = rice_scratch(ctx, px, chunks + n, skew, edge))) return rc;
     LAUNCH(rice_decode_batch(pl, n, ctx->rice, ctx->stream));
     ctx->launches += 6;  // spec, >= 2 sync rounds, scan, emit, rebuild, deskew, adler (counted once)
     for (int i = 0; i < n; ++i) {

@@ -20,9 +20,11 @@
 //                         settle an exact symbol segmentation
 //           k_scan_blocks symbol base of every chunk
 //           k_rice_emit   each chunk writes its residuals
-//           k_med_rebuild_diag  the MED recurrence as an anti-diagonal
-//                         wavefront, one CTA per plane, one barrier per
-//                         diagonal; all planes of a batch run concurrently
+//           k_med_rebuild_wave  the MED recurrence, one warp per 32-row
+//                         strip (lane = row, skewed by one column per lane,
+//                         neighbours by shuffle), strip edges handed down
+//                         through epoch-tagged global slots; every strip of
+//                         every plane of a batch runs concurrently
 //           k_adler       adler32 of the rebuilt plane (zlib.adler32 check)
 
 #include <cstdint>
@@ -48,10 +50,13 @@ namespace fvv {
 // encode
 
 // LOCO-I median predictor (depthcodec.py:281-298): a left, b up, c up-left,
-// 0 outside the plane
+// 0 outside the plane. The reference's three cases (c >= max(a, b): min;
+// c <= min(a, b): max; else a + b - c) are all max(a, b, c) + min(a, b, c) - c:
+// two 3-input min/max and one add, no compare-and-select chain, and exact in
+// wrapping int32 arithmetic (the true value lies between min and max).
 __device__ __forceinline__ int med(int a, int b, int c) {
-    const int mx = a > b ? a : b, mn = a < b ? a : b;
-    return c >= mx ? mn : (c <= mn ? mx : a + b - c);
+    const int mx = max(max(a, b), c), mn = min(min(a, b), c);
+    return (int)((unsigned)mx + (unsigned)mn - (unsigned)c);
 }
 
 __global__ void k_med_zz(const uint8_t *x, int W, int H, uint16_t *zz,
@@ -252,12 +257,18 @@ __device__ __forceinline__ long long rice_one(const uint8_t *s, long long nbytes
     return t + 1 + k - p;
 }
 
-// Position of residual (row, col) in the rebuild's anti-diagonal-major
-// layout: diagonal t = row + col holds rows 0..H-1 at t*H + row, so each
-// wavefront step reads and writes contiguous words.
+// Position of residual (row, col) in the rebuild's strip layout
+// (rice_skew_size): row = kWaveStrip s + kWaveRows l + h runs in lane l of
+// strip s's warp as its row h, computing column col at step
+// u = col + kWaveRows l + h; each strip stores [u / 4][h][l][u % 4], so a
+// warp reads a row's 4 steps as one 16-byte word per lane and writes its 4
+// output bytes as one word.
 __device__ __forceinline__ long long skew_index(long long idx, int W, int H) {
     const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
-    return (long long)(row + col) * H + row;
+    const int st = row / kWaveStrip, rr = row - st * kWaveStrip;
+    const int l = rr / kWaveRows, h = rr - l * kWaveRows, u = col + rr;
+    return (long long)st * kWaveStrip * rice_wave_steps(W) +
+           ((long long)(u >> 2) * kWaveRows + h) * 128 + l * 4 + (u & 3);
 }
 
 // A batch of planes decoded together (all depth planes of a render tick):
@@ -267,6 +278,7 @@ struct RiceBatch {
     int np;
     RicePlane pl[kRiceMaxPlanes];
     long long nchunks;             // over all planes
+    int ngroups;                   // rebuild CTAs over all planes
     long long *entry;              // symbol start the chunk decodes from (plane bits)
     long long *exit;               // first symbol start at or past the chunk end
     unsigned long long *count;     // symbols starting inside the chunk
@@ -348,65 +360,221 @@ __global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned 
     }
 }
 
-// The MED recurrence as an anti-diagonal wavefront in one CTA: step t
-// computes every (row, t - row) at once, since x(i, j) needs only diagonal
-// t-1 (left (i, j-1), up (i-1, j)) and t-2 (up-left). The last two diagonals
-// live in shared memory indexed by row; residuals and outputs use the
-// anti-diagonal-major layout, so each step reads and writes contiguous
-// words. One barrier per step; each thread owns rows tid, tid + blockDim, ...
-constexpr int kDiagPf = 8;  // residual prefetch depth (steps)
+// The MED recurrence (depthcodec.py:301-317) as a wavefront of strips of
+// kWaveStrip rows, one warp each, lane l holding rows R l .. R l + R - 1
+// (R = kWaveRows). Row h of a lane runs h steps behind row h - 1 and lane l
+// runs R steps behind lane l - 1, so at step u every row needs only values
+// of steps u - 1 and u - 2: its own (left), the row above (up, up-left), from
+// a register for h > 0 and by shuffle from lane l - 1 for h = 0. The R rows
+// of a step are independent (instruction-level parallelism) and a value
+// crosses lanes once per R steps.
+//
+// Lane 0 of strip s reads strip s - 1's last row from global memory: 64-bit
+// slots tagged with the batch's epoch, stored by the producer (lane 31) per
+// column. Residuals and those slots are staged kWavePf blocks (of 4 steps)
+// ahead into shared memory by cp.async, so no load latency and no register
+// ring sits on the step chain; a slot whose tag is still stale when its
+// block comes is re-read (warp-uniformly) until it is current, and at its
+// start a consumer waits until the producer is kWaveLead columns ahead, past
+// the staging window. The producer belongs to the same CTA or to a CTA with
+// a smaller ticket (taken at CTA start), which has started and waits only on
+// smaller tickets: every wait ends (a lost producer would set wave[1] after
+// kWaveSpinLimit re-reads instead of hanging).
+constexpr int kWavePf = 5;                        // blocks staged ahead
+constexpr int kWaveLead = 4 * kWavePf + 40;       // producer lead at a consumer's start
+constexpr long long kWaveSpinLimit = 1ll << 26;
 
-template <int ROWS>
-__global__ void __launch_bounds__(1024, 1) k_med_rebuild_diag(const __grid_constant__ RiceBatch b,
-                                                              const int32_t *res_all,
-                                                              uint8_t *diag_all) {
-    // one CTA per plane
-    const RicePlane &pl = b.pl[blockIdx.x];
-    const int W = pl.W, H = pl.H;
-    const int32_t *res = res_all + pl.rbase;
-    uint8_t *out_diag = diag_all + pl.rbase;
-    extern __shared__ int32_t s_diag[];   // [3][H]: diagonals t, t-1, t-2 (rotating)
-    const int nt = blockDim.x;
-    const int steps = W + H - 1;
-    // residuals of this thread's rows, kDiagPf steps ahead: ring slot u
-    // holds step t0 + u and is refilled with step t0 + u + kDiagPf
-    int32_t ring[kDiagPf][ROWS];
-    auto fetch = [&](int t, int q) -> int32_t {
-        const int i = threadIdx.x + q * nt;
-        return (i < H && i <= t && t - i < W) ? __ldg(res + (long long)t * H + i) : 0;
+__device__ __forceinline__ unsigned long long ld_edge(const unsigned long long *ptr) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr));
+    return v;
+}
+__device__ __forceinline__ void st_edge(unsigned long long *ptr, int p, unsigned long long v) {
+    // no "memory" clobber: nothing else in the kernel reads these slots
+    // through ordinary accesses, and keeping the compiler free to move the
+    // next block's shared-memory loads across this store matters
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+        " @q st.relaxed.gpu.global.u64 [%0], %1;\n}" ::"l"(ptr),
+        "l"(v), "r"(p));
+}
+__device__ __forceinline__ void wave_cp16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// A slot's value once its tag is the batch's: the whole warp re-reads the
+// same slot while any lane sees a stale tag (v: the value each lane last
+// read). Warp-uniform on purpose: a wait taken by lane 0 alone would leave
+// the warp diverged, and every later shuffle would go through the divergent
+// (collective) path.
+__device__ __forceinline__ unsigned long long edge_wait(const unsigned long long *slot,
+                                                        unsigned long long v, unsigned epoch,
+                                                        int *stall) {
+    long long n = 0;
+#pragma unroll 1
+    while (__any_sync(0xffffffffu, (uint32_t)(v >> 32) != epoch)) {
+        if (++n == kWaveSpinLimit) {  // a lost producer: report, never hang
+            if ((threadIdx.x & 31) == 0) atomicExch(stall, 1);
+            break;
+        }
+        v = ld_edge(slot);
+    }
+    return v;
+}
+
+template <bool C>
+struct WaveCheck {
+    static constexpr bool value = C;
+};
+
+__global__ void __launch_bounds__(32 * kWaveWarps) k_med_rebuild_wave(
+    const __grid_constant__ RiceBatch b, const int32_t *res_all, uint8_t *skew_all,
+    unsigned long long *edge_all, int *wave, unsigned epoch) {
+    constexpr int R = kWaveRows, PF = kWavePf;
+    // per warp: PF staged blocks of residuals [R][32 lanes] and edge slots [4]
+    __shared__ __align__(16) int4 s_res[kWaveWarps][PF][R][32];
+    __shared__ __align__(16) unsigned long long s_top[kWaveWarps][PF][4];
+    __shared__ int s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(wave, 1);
+    __syncthreads();
+    const int g = s_ticket;
+    int p = 0;
+    while (p + 1 < b.np && g >= b.pl[p + 1].g0) ++p;
+    const RicePlane &pl = b.pl[p];
+    const int W = pl.W, H = pl.H, ns = (H + kWaveStrip - 1) / kWaveStrip;
+    const int wid = threadIdx.x >> 5;
+    const int st = (g - pl.g0) * kWaveWarps + wid;
+    if (st >= ns) return;
+    const int lane = threadIdx.x & 31;
+    const int U = rice_wave_steps(W), nblk = U >> 2, Wp = (W + 3) & ~3;
+    const long long sbase = pl.rbase + (long long)st * kWaveStrip * U;
+    // block k, row h of this lane: res[32 (R k + h)]
+    const int4 *res = reinterpret_cast<const int4 *>(res_all + sbase) + lane;
+    uint32_t *out = reinterpret_cast<uint32_t *>(skew_all + sbase) + lane;
+    const bool up = st > 0 && lane == 0, down = st + 1 < ns && lane == 31;
+    const unsigned long long *top = edge_all + pl.ebase + (long long)(st > 0 ? st - 1 : 0) * Wp;
+    unsigned long long *mine = edge_all + pl.ebase + (long long)st * Wp;
+    const unsigned long long tag = (unsigned long long)epoch << 32;
+    const int l0 = R * lane;  // this lane's first row within the strip
+    int4(*sres)[R][32] = s_res[wid];
+    unsigned long long(*stop)[4] = s_top[wid];
+    if (st > 0) {  // start once the producer is kWaveLead columns ahead
+        const int c = min(kWaveLead, W - 1);
+        edge_wait(top + c, ld_edge(top + c), epoch, wave + 1);
+    }
+    // stage block k (clamped to the strip; past-the-end stages are unused):
+    // this lane's R residual words, and for lane 0 the 4 edge slots above
+    auto stage = [&](int k) {
+        const int kc = min(k, nblk - 1), slot = k % PF;
+#pragma unroll
+        for (int h = 0; h < R; ++h) wave_cp16(&sres[slot][h][lane], res + 32 * (R * kc + h));
+        if (up) {
+            const unsigned long long *src = top + min(4 * kc, Wp - 4);
+            wave_cp16(&stop[slot][0], src);
+            wave_cp16(&stop[slot][2], src + 2);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
 #pragma unroll
-    for (int u = 0; u < kDiagPf; ++u)
+    for (int k = 0; k < PF - 1; ++k) stage(k);
+    int x1[R], x2[R];
 #pragma unroll
-        for (int q = 0; q < ROWS; ++q) ring[u][q] = fetch(u, q);
-    for (int t0 = 0; t0 < steps; t0 += kDiagPf) {
+    for (int h = 0; h < R; ++h) x1[h] = x2[h] = 0;
+    int tprev = 0;
+    // One block of 4 steps. CHECK: some row of some step may lie outside
+    // columns 0..W-1 (the strip's first 32R - 1 and last steps); elsewhere
+    // every row's column is inside and the range tests go.
+    // the staged inputs of block k: this lane's residuals and the 4 edge slots
+    // (every lane reads the slots, a broadcast; only lane 0 of a strip > 0
+    // uses them)
+    struct Staged {
+        int4 r[R];
+        ulonglong2 v01, v23;
+    };
+    auto load = [&](int k) {
+        Staged d;
+        const int slot = k % PF;
 #pragma unroll
-        for (int u = 0; u < kDiagPf; ++u) {
-            const int t = t0 + u;
-            if (t >= steps) break;
-            int32_t *d0 = s_diag + (t % 3) * H;
-            const int32_t *d1 = s_diag + ((t + 2) % 3) * H;   // t - 1
-            const int32_t *d2 = s_diag + ((t + 1) % 3) * H;   // t - 2
+        for (int h = 0; h < R; ++h) d.r[h] = sres[slot][h][lane];
+        d.v01 = *reinterpret_cast<const ulonglong2 *>(&stop[slot][0]);
+        d.v23 = *reinterpret_cast<const ulonglong2 *>(&stop[slot][2]);
+        return d;
+    };
+    // One block of 4 steps. CHECK: some row of some step may lie outside
+    // columns 0..W-1 (the strip's first 32R - 1 and last steps); elsewhere
+    // every row's column is inside and the range tests go.
+    auto block = [&](auto check, int k, const Staged &d) {
+        constexpr bool CHECK = decltype(check)::value;
+        const int4 *r = d.r;
+        // lane 0: columns 4k..4k+3 of the row above (stale tags are rare)
+        int t[4];
+        bool stale = false;
+        {
+            const unsigned long long v[4] = {d.v01.x, d.v01.y, d.v23.x, d.v23.y};
 #pragma unroll
-            for (int q = 0; q < ROWS; ++q) {
-                const int i = threadIdx.x + q * nt;
-                const int j = t - i;
-                if (i < H && j >= 0 && j < W) {
-                    const int a = j > 0 ? d1[i] : 0;
-                    const int b = i > 0 ? d1[i - 1] : 0;
-                    const int c = (i > 0 && j > 0) ? d2[i - 1] : 0;
-                    const int x = ring[u][q] + med(a, b, c);
-                    d0[i] = x;
-                    out_diag[(long long)t * H + i] = (uint8_t)x;   // astype(uint8): modulo 256
-                }
-                ring[u][q] = fetch(t + kDiagPf, q);
+            for (int e = 0; e < 4; ++e) {
+                t[e] = up ? (int)(uint32_t)v[e] : 0;
+                stale |= up && 4 * k + e < W && (uint32_t)(v[e] >> 32) != epoch;
             }
-            __syncthreads();
         }
+        if (__any_sync(0xffffffffu, stale)) {  // warp-uniform slow path
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (4 * k + e < W)
+                    t[e] = (int)(uint32_t)edge_wait(top + 4 * k + e, ld_edge(top + 4 * k + e),
+                                                    epoch, wave + 1);
+            if (!up) t[0] = t[1] = t[2] = t[3] = 0;
+        }
+        int xs[4][R];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            int bu = __shfl_up_sync(0xffffffffu, x1[R - 1], 1);
+            int cu = __shfl_up_sync(0xffffffffu, x2[R - 1], 1);
+            if (lane == 0) {  // strip 0: t and tprev stay 0 (row -1 is 0)
+                bu = t[e];
+                cu = e ? t[e - 1] : tprev;
+            }
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const int bb = h ? x1[h - 1] : bu, cc = h ? x2[h - 1] : cu;
+                const int rv = e == 0 ? r[h].x : e == 1 ? r[h].y : e == 2 ? r[h].z : r[h].w;
+                const int x = (int)((unsigned)rv + (unsigned)med(x1[h], bb, cc));
+                // x1 is 0 left of column 0, so a = 0 there (as in the reference)
+                xs[e][h] = !CHECK || (unsigned)(4 * k + e - l0 - h) < (unsigned)W ? x : 0;
+            }
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                x2[h] = x1[h];
+                x1[h] = xs[e][h];
+            }
+        }
+        tprev = t[3];
+#pragma unroll
+        for (int h = 0; h < R; ++h)  // astype(uint8): the low bytes of 4 steps
+            out[32 * (R * k + h)] = __byte_perm(__byte_perm(xs[0][h], xs[1][h], 0x0040),
+                                                __byte_perm(xs[2][h], xs[3][h], 0x0040), 0x5410);
+        // lane 31: this block's columns of the strip's last row
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * k + e - (kWaveStrip - 1);
+            st_edge(mine + j, down && (!CHECK || (unsigned)j < (unsigned)W),
+                    tag | (uint32_t)xs[e][R - 1]);
+        }
+    };
+    // blocks whose steps u all have u >= 32R - 1 and u <= W - 1
+    const int km0 = (kWaveStrip - 1 + 3) / 4, km1 = W / 4;
+#pragma unroll 1
+    for (int k = 0; k < nblk; ++k) {
+        stage(k + PF - 1);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(PF - 1) : "memory");
+        if (k >= km0 && k < km1)
+            block(WaveCheck<false>{}, k, load(k));
+        else
+            block(WaveCheck<true>{}, k, load(k));
     }
 }
 
-// anti-diagonal rebuild output -> raster plane (blockIdx.y = plane)
+// strip-layout rebuild output -> raster plane (blockIdx.y = plane)
 __global__ void k_deskew(const __grid_constant__ RiceBatch b, const uint8_t *diag_all) {
     const RicePlane &pl = b.pl[blockIdx.y];
     const uint8_t *skew = diag_all + pl.rbase;
@@ -471,8 +639,8 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
     cudaError_t e;
     RiceBatch b{};
     b.np = np;
-    long long c0 = 0, rbase = 0;
-    int maxH = 0;
+    long long c0 = 0, rbase = 0, ebase = 0;
+    int g0 = 0;
     for (int p = 0; p < np; ++p) {
         RicePlane &pl = planes[p];
         pl.nbits = pl.nbytes * 8;
@@ -482,16 +650,25 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
         pl.rbase = rbase;
         pl.status = 0;
         c0 += pl.nchunks;
+        pl.ebase = ebase;
+        pl.g0 = g0;
         rbase += (long long)rice_skew_size(pl.W, pl.H);
-        maxH = pl.H > maxH ? pl.H : maxH;
+        ebase += (long long)rice_edge_size(pl.W, pl.H);
+        g0 += (rice_wave_strips(pl.H) + kWaveWarps - 1) / kWaveWarps;
         b.pl[p] = pl;
     }
     b.nchunks = c0;
+    b.ngroups = g0;
     b.entry = sc.entry;
     b.exit = sc.exit;
     b.count = sc.count;
     const unsigned g = (unsigned)((b.nchunks + 127) / 128);
     unsigned long long tot[kRiceMaxPlanes] = {0};
+#ifdef FVV_CODEC_TRACE
+    cudaEvent_t t0_;
+    cudaEventCreate(&t0_);
+    cudaEventRecord(t0_, s);
+#endif
     if (b.nchunks) {
         k_rice_spec<<<g, 128, 0, s>>>(b);
         for (long long round = 0;; round += 2) {
@@ -511,6 +688,7 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
             if (!changed) break;
             if (round > b.nchunks) return cudaErrorUnknown;  // cannot happen: >= 1 chunk settles per round
         }
+        TRACE_EV("segment");
         if ((e = cudaMemcpyAsync(sc.block, sc.count, sizeof(unsigned long long) * b.nchunks,
                                  cudaMemcpyDeviceToDevice, s)))
             return e;
@@ -519,6 +697,7 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
                                  cudaMemcpyDeviceToHost, s)))
             return e;
         if ((e = cudaStreamSynchronize(s))) return e;
+        TRACE_EV("scan");
     }
     // a plane whose stream runs out before its n symbols (a truncated symbol
     // ends its chain) is reported and left undecoded
@@ -530,21 +709,31 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
     }
     if (!any) return cudaSuccess;
     if (b.nchunks) k_rice_emit<<<g, 128, 0, s>>>(b, sc.block, sc.res);
-    const size_t sm = (size_t)3 * maxH * sizeof(int32_t);
-    if (maxH <= 1024)
-        k_med_rebuild_diag<1><<<np, (maxH + 31) / 32 * 32, sm, s>>>(b, sc.res, sc.skew);
-    else if (maxH <= 2048)
-        k_med_rebuild_diag<2><<<np, 1024, sm, s>>>(b, sc.res, sc.skew);
-    else
-        k_med_rebuild_diag<4><<<np, 1024, sm, s>>>(b, sc.res, sc.skew);
+    TRACE_EV("emit");
+    // edge tags: a fresh epoch per batch (the slots start zeroed, epoch 0 is
+    // never used, so no stale slot matches)
+    if (++sc.epoch == 0) {
+        if ((e = cudaMemsetAsync(sc.edge, 0, sc.e_cap * sizeof(unsigned long long), s))) return e;
+        sc.epoch = 1;
+    }
+    if ((e = cudaMemsetAsync(sc.wave, 0, 2 * sizeof(int), s))) return e;
+    k_med_rebuild_wave<<<b.ngroups, 32 * kWaveWarps, 0, s>>>(b, sc.res, sc.skew, sc.edge, sc.wave,
+                                                            sc.epoch);
+    TRACE_EV("rebuild");
     k_deskew<<<dim3(148 * 2, np), 256, 0, s>>>(b, sc.skew);
+    TRACE_EV("deskew");
     if ((e = cudaMemsetAsync(sc.costs, 0, 2 * np * sizeof(unsigned long long), s))) return e;
     k_adler<<<dim3(148, np), 256, 0, s>>>(b, sc.costs);
     unsigned long long ab[2 * kRiceMaxPlanes];
+    int stall = 0;
     if ((e = cudaMemcpyAsync(ab, sc.costs, 2 * np * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s)))
         return e;
+    if ((e = cudaMemcpyAsync(&stall, sc.wave + 1, sizeof(int), cudaMemcpyDeviceToHost, s)))
+        return e;
     if ((e = cudaStreamSynchronize(s))) return e;
+    TRACE_EV("adler");
+    if (stall) return cudaErrorLaunchTimeout;  // a strip never received the row above
     for (int p = 0; p < np; ++p) {
         const unsigned long long n = (unsigned long long)planes[p].n;
         const uint32_t A = (uint32_t)((1 + ab[2 * p]) % 65521ull);

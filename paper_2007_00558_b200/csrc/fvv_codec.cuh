@@ -8,7 +8,7 @@ namespace fvv {
 
 constexpr int kRiceKMax = 14;          // depthcodec.py:380: k in range(15)
 constexpr int kRiceChunkBits = 256;    // decode chunk (speculative segmentation unit)
-constexpr int kMedMaxWidth = 12288;    // MED rebuild: 2 x W x 8 B of row slots in shared memory
+constexpr int kMedMaxWidth = 12288;    // MED rebuild: widest plane (strip rows of W + 31 steps)
 
 constexpr int kRiceMaxPlanes = 48;     // planes per decode batch (16 cameras x Y, U, V)
 
@@ -21,6 +21,8 @@ struct RicePlane {
     uint8_t *out;           // device plane (W x H)
     // filled by rice_decode_batch
     long long nbits, n, c0, nchunks, rbase;
+    long long ebase;        // first strip-edge slot of the plane (rice_edge_size)
+    int g0;                 // first rebuild CTA of the plane (kWaveWarps strips each)
     int status;             // 1: the stream runs out before W*H symbols
     uint32_t adler;         // adler32 of the rebuilt plane
 };
@@ -36,6 +38,10 @@ struct RiceScratch {
     long long *entry = nullptr, *exit = nullptr, *exit_prev = nullptr;  // [c] over all planes
     unsigned long long *count = nullptr;    // [c]
     int *changed = nullptr;                 // [1]
+    unsigned long long *edge = nullptr;     // [sum rice_edge_size] strip edges, epoch-tagged
+    int *wave = nullptr;                    // [2] rebuild CTA ticket, stall flag
+    unsigned epoch = 0;                     // tag of the current batch's strip edges
+    size_t e_cap = 0;
     size_t n_cap = 0, c_cap = 0;
 };
 
@@ -46,16 +52,38 @@ cudaError_t rice_encode(const uint8_t *plane, int W, int H, RiceScratch &sc, uin
                         int *k_out, long long *nbits_out, cudaStream_t s);
 
 // Decode np planes together: W*H symbols of parameter k from each stream,
-// rebuild each plane (one CTA per plane, concurrently) and its adler32.
-// Scratch must hold sum(rice_skew_size) residuals and sum(chunks) + np chunk
-// entries. Synchronous.
+// rebuild every plane (one warp per 32-row strip, all planes concurrently)
+// and its adler32. Scratch must hold sum(rice_skew_size) residuals,
+// sum(rice_edge_size) edge slots and sum(chunks) + np chunk entries.
+// Synchronous.
 cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaStream_t s);
 
-// elements of the rebuild's skewed layout for a W x H plane
+// The MED rebuild (fvv_codec.cu, k_med_rebuild_wave) runs one warp per strip
+// of 32 x kWaveRows rows, lane l on rows kWaveRows l .. kWaveRows l + R - 1,
+// skewed so that step u computes column u - (row within the strip): a strip
+// takes W + 32 kWaveRows - 1 steps, padded to a multiple of 4.
+#ifndef FVV_WAVE_R
+#define FVV_WAVE_R 4
+#endif
+constexpr int kWaveRows = FVV_WAVE_R;     // rows per lane
+constexpr int kWaveStrip = 32 * kWaveRows;  // rows per strip (warp)
+#ifndef FVV_WAVE_WARPS
+#define FVV_WAVE_WARPS 4
+#endif
+constexpr int kWaveWarps = FVV_WAVE_WARPS;  // strips per rebuild CTA
+__host__ __device__ inline int rice_wave_steps(int W) { return (W + kWaveStrip - 1 + 3) & ~3; }
+inline int rice_wave_strips(int H) { return (H + kWaveStrip - 1) / kWaveStrip; }
+
+// elements of the rebuild's skewed layout for a W x H plane (residuals in,
+// bytes out): per strip, [steps / 4][kWaveRows][32 lanes][4 steps]
 inline size_t rice_skew_size(int W, int H) {
-    const size_t strips = (size_t)((H + 31) / 32) * (size_t)(W + 31) * 32;
-    const size_t diags = (size_t)(W + H - 1) * (size_t)H;
-    return strips > diags ? strips : diags;
+    return (size_t)rice_wave_strips(H) * kWaveStrip * (size_t)rice_wave_steps(W);
+}
+
+// 64-bit strip-edge slots for a W x H plane: the last row of every strip, as
+// the next strip reads it (row stride W rounded up to 4)
+inline size_t rice_edge_size(int W, int H) {
+    return (size_t)rice_wave_strips(H) * (size_t)((W + 3) & ~3);
 }
 
 // bytes `stream` must hold for a W x H plane: the cheapest k costs at most

@@ -82,11 +82,14 @@ def test_gpu_codec_reproduces_reference_payloads(DC, name):
 @pytest.mark.gpu
 @pytest.mark.parametrize("h,w,kind", [(1080, 1920, "smooth"), (2160, 3840, "smooth"),
                                       (1100, 64, "noise"), (34, 2050, "noise"),
-                                      (2, 2, "noise"), (64, 96, "const")])
+                                      (2, 2, "noise"), (64, 96, "const"),
+                                      (4096, 4, "noise"), (2, 4000, "noise"), (38, 2, "noise"),
+                                      (162, 34, "smooth")])
 def test_gpu_codec_round_trip_and_oracle_payload(DC, h, w, kind):
-    """Round trips at full 1080p / 4K plane sizes (strips > 32 exercise the
-    wavefront's strip hand-off), tall/narrow and wide/short planes, and the
-    payload equal to the oracle's encoder."""
+    """Round trips at full 1080p / 4K plane sizes (34 / 68 strips of 32 rows:
+    edge hand-offs inside and across rebuild CTAs), tall/narrow (4 columns),
+    two-row, two-column and ragged planes, and the payload
+    equal to the oracle's encoder."""
     rng = np.random.default_rng(h * 7 + w)
     if kind == "smooth":
         yy, xx = np.mgrid[0:h, 0:w]
@@ -170,6 +173,30 @@ def test_edge_server_ingests_the_wire_format(DC):
             r.ingest_yuv(cid, c.rgb, *planes, rng_)
         outs.append(r.render([wl.virtuals[0]], [wl.refs[0]])[0].cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.gpu
+def test_full_batch_of_48_planes_twice(DC):
+    """The largest batch (16 frames = 48 planes, 1080p: 1,088 strips in 272
+    rebuild CTAs) decodes exactly, and a second batch with other content in
+    the same scratch does too (strip edges left by the first batch carry an
+    older epoch and are never taken for the second's)."""
+    h, w = 1080, 1920
+    yy, xx = np.mgrid[0:h, 0:w]
+    for rnd in range(2):
+        frames, expect = [], []
+        for f in range(16):
+            rng = np.random.default_rng(100 * rnd + f)
+            y = ((np.sin(xx / (20.0 + f + 7 * rnd)) + np.cos(yy / (15.0 + f))) * 60 + 128
+                 + rng.integers(-3, 4, (h, w))).clip(0, 255).astype(np.uint8)
+            u = np.ascontiguousarray(y[::2, ::2][:, ::-1])
+            v = np.ascontiguousarray(y[1::2, 1::2])
+            frames.append(DC.encode_lossless(DC.Yuv420Image(y, u, v)))
+            expect.append((y, u, v))
+        got = DC.decode_lossless_many(frames)
+        for planes, exp in zip(got, expect):
+            for p, e in zip(planes, exp):
+                np.testing.assert_array_equal(p.cpu().numpy(), e)
 
 
 @pytest.mark.gpu
