@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps) k_med_rebuild_wave(
         else
             block(WaveCheck<true>{}, k, load(k));
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copy outlives the CTA
 }
 
 // strip-layout rebuild output -> raster plane (blockIdx.y = plane)
