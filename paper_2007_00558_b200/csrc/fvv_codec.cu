@@ -381,7 +381,7 @@ __global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned 
 // smaller tickets: every wait ends (a lost producer would set wave[1] after
 // kWaveSpinLimit re-reads instead of hanging).
 constexpr int kWavePf = 5;                        // blocks staged ahead
-constexpr int kWaveLead = 4 * kWavePf + 40;       // producer lead at a consumer's start
+constexpr int kWaveLead = 4 * kWavePf + 4;  // producer lead at a consumer's start (past the staging window)
 constexpr long long kWaveSpinLimit = 1ll << 26;
 
 __device__ __forceinline__ unsigned long long ld_edge(const unsigned long long *ptr) {
