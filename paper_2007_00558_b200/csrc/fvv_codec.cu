@@ -112,39 +112,43 @@ __global__ void k_rice_lens(const uint16_t *zz, long long n, int k,
     }
 }
 
-// exclusive scan of v[0..n) in place by one CTA of 1024 threads; total in *total
+// exclusive scan of v[0..n) in place by one CTA of 1024 threads; total in
+// *total. Warp w owns a contiguous range, read 32 consecutive elements at a
+// time (coalesced): pass 1 sums it, one CTA barrier scans the 32 warp sums,
+// pass 2 scans the range slice by slice with shuffles and a running carry.
 __device__ void scan_segment(unsigned long long *v, long long n, unsigned long long *total) {
     __shared__ unsigned long long ws[32];
-    __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (long long base = 0; base < n; base += 1024) {
-        const long long i = base + threadIdx.x;
-        const unsigned long long x = i < n ? v[i] : 0;
-        unsigned long long inc = x;
+    const long long per = ((n + 31) / 32 + 31) / 32 * 32;  // whole slices per warp
+    const long long i0 = (long long)w * per;
+    const long long i1 = i0 + per < n ? i0 + per : n;
+    unsigned long long x = 0;
+    for (long long i = i0 + lane; i < i1; i += 32) x += v[i];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long t = ws[lane];
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
         }
-        if (lane == 31) ws[w] = inc;
-        __syncthreads();
-        if (w == 0) {
-            unsigned long long s = ws[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            ws[lane] = s;  // inclusive over warps
-        }
-        __syncthreads();
-        const unsigned long long before = carry + (w ? ws[w - 1] : 0) + inc - x;
-        if (i < n) v[i] = before;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = before + x;
-        __syncthreads();
+        ws[lane] = t;  // inclusive over warps
     }
-    if (threadIdx.x == 0) *total = carry;
+    __syncthreads();
+    unsigned long long carry = w ? ws[w - 1] : 0;
+    for (long long base = i0; base < i1; base += 32) {
+        const long long i = base + lane;
+        const unsigned long long y = i < i1 ? v[i] : 0;
+        unsigned long long inc = y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (i < i1) v[i] = carry + inc - y;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (threadIdx.x == 0) *total = ws[31];
 }
 
 __global__ void __launch_bounds__(1024) k_scan_blocks(unsigned long long *v, long long n,
@@ -257,14 +261,90 @@ __device__ __forceinline__ long long rice_one(const uint8_t *s, long long nbytes
     return t + 1 + k - p;
 }
 
+// MSB-first bit reader for the chunk decoders: a 64-bit buffer refilled from
+// big-endian 32-bit words with the next word loaded one refill ahead, so a
+// symbol costs shifts and a clz instead of the two dependent 64-bit peeks of
+// rice_one (same results; bytes past the stream read as zero). Streams of
+// any alignment: bits are counted from the 4-byte boundary below s.
+struct BitReader {
+    const uint32_t *w;       // aligned base (<= s)
+    long long nbytes;        // stream bytes (from s)
+    int skew;                // s - w, bytes
+    unsigned long long buf;  // bits [pos, pos + nb), MSB-aligned, zero below
+    int nb;
+    long long pos;           // stream bit of buf's MSB
+    long long wi;            // aligned index of the prefetched word
+    uint32_t next;
+
+    __device__ __forceinline__ uint32_t word(long long i) const {
+        const long long b0 = 4 * i - skew;  // stream byte of the word's first byte
+        if (b0 >= 0 && b0 + 3 < nbytes) return bswap32(__ldg(w + i));
+        uint32_t v = 0;
+        const uint8_t *s = reinterpret_cast<const uint8_t *>(w) + skew;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long b = b0 + q;
+            v = (v << 8) | (b >= 0 && b < nbytes ? (uint32_t)__ldg(s + b) : 0u);
+        }
+        return v;
+    }
+    __device__ __forceinline__ void refill() {
+        while (nb <= 32) {
+            buf |= (unsigned long long)next << (32 - nb);
+            nb += 32;
+            next = word(++wi);
+        }
+    }
+    __device__ __forceinline__ void start(const uint8_t *s, long long nbytes_, long long p) {
+        skew = (int)((uintptr_t)s & 3);
+        w = reinterpret_cast<const uint32_t *>(s - skew);
+        nbytes = nbytes_;
+        const long long a = p + 8 * skew;  // aligned bit position
+        wi = a >> 5;
+        const int off = (int)(a & 31);
+        buf = (unsigned long long)word(wi) << (32 + off);
+        nb = 32 - off;
+        next = word(++wi);
+        pos = p;
+        refill();
+    }
+    __device__ __forceinline__ void skip(int n) {  // n <= nb
+        buf = n < 64 ? buf << n : 0ull;
+        nb -= n;
+        pos += n;
+        refill();
+    }
+    // one symbol (depthcodec.py:337-355); false (truncated) if its unary run
+    // or remainder runs past nbits; requires k <= 32
+    __device__ __forceinline__ bool symbol(long long nbits, int k, unsigned long long &zz) {
+        unsigned long long q = 0;
+        while (true) {
+            if (pos >= nbits) return false;
+            const int lz = __clzll(buf);  // 64 when buf == 0
+            if (lz < nb) {
+                q += lz;
+                if (pos + lz >= nbits) return false;  // the one lies in the padding
+                if (pos + lz + 1 + k > nbits) return false;
+                skip(lz + 1);
+                break;
+            }
+            q += nb;
+            skip(nb);
+        }
+        const unsigned long long rem = k ? buf >> (64 - k) : 0ull;
+        if (k) skip(k);
+        zz = (q << k) | rem;
+        return true;
+    }
+};
+
 // Position of residual (row, col) in the rebuild's strip layout
 // (rice_skew_size): row = kWaveStrip s + kWaveRows l + h runs in lane l of
 // strip s's warp as its row h, computing column col at step
 // u = col + kWaveRows l + h; each strip stores [u / 4][h][l][u % 4], so a
 // warp reads a row's 4 steps as one 16-byte word per lane and writes its 4
 // output bytes as one word.
-__device__ __forceinline__ long long skew_index(long long idx, int W, int H) {
-    const int row = (int)(idx / W), col = (int)(idx - (long long)row * W);
+__device__ __forceinline__ long long skew_rc(int row, int col, int W) {
     const int st = row / kWaveStrip, rr = row - st * kWaveStrip;
     const int l = rr / kWaveRows, h = rr - l * kWaveRows, u = col + rr;
     return (long long)st * kWaveStrip * rice_wave_steps(W) +
@@ -296,12 +376,23 @@ __device__ void chunk_decode(const RiceBatch &b, const RicePlane &pl, long long 
         (lj + 1) * kRiceChunkBits < pl.nbits ? (lj + 1) * kRiceChunkBits : pl.nbits;
     long long p = e;
     unsigned long long n = 0;
-    while (p < end) {
-        unsigned long long zz;
-        const long long len = rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
-        if (!len) { p = pl.nbits; break; }   // truncated: no further symbols
-        p += len;
-        ++n;
+    if (pl.k <= 32) {
+        BitReader br;
+        if (p < end) br.start(pl.s, pl.nbytes, p);
+        while (p < end) {
+            unsigned long long zz;
+            if (!br.symbol(pl.nbits, pl.k, zz)) { p = pl.nbits; break; }  // truncated
+            p = br.pos;
+            ++n;
+        }
+    } else {
+        while (p < end) {
+            unsigned long long zz;
+            const long long len = rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
+            if (!len) { p = pl.nbits; break; }   // truncated: no further symbols
+            p += len;
+            ++n;
+        }
     }
     b.entry[j] = e;
     b.exit[j] = p;
@@ -352,11 +443,23 @@ __global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned 
     unsigned long long idx = base[j];
     const unsigned long long cnt = b.count[j];
     int32_t *r = res + pl.rbase;
+    // raster position of the first symbol; later ones step along the row
+    int row = (int)(idx / (unsigned long long)pl.W), col = (int)(idx - (unsigned long long)row * pl.W);
+    BitReader br;
+    const bool fast = pl.k <= 32;
+    if (fast && cnt) br.start(pl.s, pl.nbytes, p);
     for (unsigned long long s = 0; s < cnt && (long long)idx < pl.n; ++s, ++idx) {
         unsigned long long zz = 0;
-        p += rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
+        if (fast)
+            br.symbol(pl.nbits, pl.k, zz);  // counted symbols decode (chunk_decode)
+        else
+            p += rice_one(pl.s, pl.nbytes, pl.nbits, pl.k, p, zz);
         const long long z = (long long)zz;
-        r[skew_index((long long)idx, pl.W, pl.H)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
+        r[skew_rc(row, col, pl.W)] = (int32_t)((z & 1) == 0 ? z / 2 : -(z + 1) / 2);
+        if (++col == pl.W) {
+            col = 0;
+            ++row;
+        }
     }
 }
 
@@ -576,12 +679,28 @@ __global__ void __launch_bounds__(32 * kWaveWarps) k_med_rebuild_wave(
 }
 
 // strip-layout rebuild output -> raster plane (blockIdx.y = plane)
+// (4 consecutive pixels of a row per thread: 4-byte stores when W % 4 == 0)
 __global__ void k_deskew(const __grid_constant__ RiceBatch b, const uint8_t *diag_all) {
     const RicePlane &pl = b.pl[blockIdx.y];
     const uint8_t *skew = diag_all + pl.rbase;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pl.n;
-         i += (long long)gridDim.x * blockDim.x)
-        pl.out[i] = skew[skew_index(i, pl.W, pl.H)];
+    const int W = pl.W, W4 = (W + 3) >> 2;
+    const long long n4 = (long long)W4 * pl.H;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(i / W4), c0 = (int)(i - (long long)row * W4) * 4;
+        uint8_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = c0 + q < W ? skew[skew_rc(row, c0 + q, W)] : 0;
+        uint8_t *o = pl.out + (long long)row * W + c0;
+        if ((W & 3) == 0 && ((uintptr_t)pl.out & 3) == 0) {
+            *reinterpret_cast<uint32_t *>(o) = (uint32_t)v[0] | ((uint32_t)v[1] << 8) |
+                                               ((uint32_t)v[2] << 16) | ((uint32_t)v[3] << 24);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (c0 + q < W) o[q] = v[q];
+        }
+    }
 }
 
 // adler32 (zlib) of each rebuilt plane: A = 1 + sum d_i, B = n + sum (n - i) d_i,
