@@ -507,9 +507,11 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
     g = make_uchar4(0, 0, 0, 0);
     if (qy >= 0 && qy < p.H && qx >= 0 && qx < p.W) {
         uint8_t v;
+        // the colour load does not wait for the validity test (one dependent
+        // load fewer per tap; a non-Valid tap's colour is never used)
+        g = load_rgb(p, (size_t)qy * p.W + qx);
         load_depth(p, qy, qx, z, v, nullptr);
         ok = v == FVV_VALID;
-        if (ok) g = load_rgb(p, (size_t)qy * p.W + qx);
     }
 }
 
