@@ -275,6 +275,49 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     for (int r = 0; r < PROWS; ++r) {
         const int iy = y0 + ty + 8 * r;
         const size_t rowbase = (size_t)iy * p.W;
+        if (vec[r] && !p.color_valid) {
+            // the 4 pixels as packed bytes: validity word, flag word, texels
+            // by byte permutes (same values as the per-pixel path below)
+            float z[4];
+            uint32_t v4;
+            if (p.src == kSrcYUV) {
+                uint32_t code[4];
+                uint8_t val[4];
+                yuv_codes4(rm[r].x, rm[r].y, code);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) decode_code(p, code[q], val[q], z[q]);
+                v4 = (uint32_t)val[0] | ((uint32_t)val[1] << 8) | ((uint32_t)val[2] << 16) |
+                     ((uint32_t)val[3] << 24);
+            } else {
+                // decode_mm: Valid with mm == 0 becomes Invalid; z = mm / 1000 on Valid
+                const uint32_t zero =
+                    __byte_perm(__vcmpeq2(rm[r].x, 0u), __vcmpeq2(rm[r].y, 0u), 0x6420);
+                const uint32_t fix = __vcmpeq4(rv[r], 0u) & zero;
+                v4 = (rv[r] & ~fix) | (fix & (0x01010101u * FVV_INVALID));
+                const uint32_t vm = __vcmpeq4(v4, 0u);
+                const uint32_t mm4[4] = {rm[r].x & 0xFFFFu, rm[r].x >> 16, rm[r].y & 0xFFFFu,
+                                         rm[r].y >> 16};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) z[q] = ((vm >> (8 * q)) & 1u) ? mm_to_m(mm4[q]) : 0.0f;
+            }
+            static_assert(FVV_VALID == 0 && kFlagLiveValid == 1 && kFlagLiveBackground == 2,
+                          "packed flag word");
+            vp[r] = v4;
+            nh += __popc(__vcmpeq4(v4, 0x01010101u * FVV_INVALID)) >> 3;
+            const uint32_t fl = (__vcmpeq4(v4, 0u) & 0x01010101u) |
+                                (__vcmpeq4(v4, 0x01010101u * FVV_BACKGROUND) & 0x02020202u);
+            const uint32_t ca = rc[r][0], cb = rc[r][1], cc = rc[r][2];
+            const size_t i0 = rowbase + xb;
+            if (p.texel)
+                *reinterpret_cast<uint4 *>(p.texel + i0) = make_uint4(
+                    __byte_perm(ca, fl, 0x4210), __byte_perm(__byte_perm(ca, cb, 0x0543), fl, 0x5210),
+                    __byte_perm(__byte_perm(cb, cc, 0x0432), fl, 0x6210), __byte_perm(cc, fl, 0x7321));
+            // z is 0 wherever the pixel is not Valid, so the warp depth is z
+            if (p.warp_depth) *reinterpret_cast<float4 *>(p.warp_depth + i0) = make_float4(z[0], z[1], z[2], z[3]);
+            if (p.depth_out) *reinterpret_cast<float4 *>(p.depth_out + i0) = make_float4(z[0], z[1], z[2], z[3]);
+            if (p.validity_out) *reinterpret_cast<uint32_t *>(p.validity_out + i0) = v4;
+            continue;
+        }
         float z[4];
         uint8_t val[4];
         uchar4 g[4];
