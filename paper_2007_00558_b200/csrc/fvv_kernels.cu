@@ -241,11 +241,12 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
     bool vec[PROWS];
     uint2 rm[PROWS];
     uint32_t rv[PROWS], rc[PROWS][3];
+    const bool vcols = xb + 3 < p.W && (p.W & 3) == 0 && p.rgb &&
+                       ((p.src == kSrcMM && p.validity) || p.src == kSrcYUV);
 #pragma unroll
     for (int r = 0; r < PROWS; ++r) {
         const int iy = y0 + ty + 8 * r;
-        vec[r] = iy < p.H && xb + 3 < p.W && (p.W & 3) == 0 && p.rgb &&
-                 ((p.src == kSrcMM && p.validity) || p.src == kSrcYUV);
+        vec[r] = vcols && iy < p.H;
         if (vec[r]) {
             // 16-B aligned vector path (W % 4 == 0; torch/cudaMalloc bases are 256-B aligned)
             const size_t i0 = (size_t)iy * p.W + xb;
