@@ -567,13 +567,14 @@ __device__ __forceinline__ void fill_tap(const PreprocCore &p, int x, int y, int
 // dependent loads per candidate): 4 lanes per candidate (8 candidates per
 // warp pass, 6 independent taps per lane) halve the passes of 8 lanes.
 #ifndef FVV_K1_CTAS
-#define FVV_K1_CTAS 4   // CTAs per SM of the K1 grid
+#define FVV_K1_CTAS 4   // CTAs per SM of the K1 grid, all resident (<= 64 registers;
+                        // at 87 only 2 fit and the grid ran in two latency-bound waves)
 #endif
 #ifndef FVV_K1_LPC
 #define FVV_K1_LPC 4
 #endif
 template <int LPC>
-__global__ void __launch_bounds__(256) k_fill_g8(const __grid_constant__ PreprocBatch batch) {
+__global__ void __launch_bounds__(256, FVV_K1_CTAS) k_fill_g8(const __grid_constant__ PreprocBatch batch) {
     constexpr int G = 32 / LPC, TPL = 24 / LPC;   // candidates per warp, taps per lane
     __shared__ double2 s_w[8][G][24];   // [warp][group][tap] = (w, w * z)
     const BilateralParams &bl = batch.bil;
