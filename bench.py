@@ -74,8 +74,8 @@ def parse():
                     help="frames in flight: steps alternate over this many private renderers "
                          "on their own CUDA streams, so one frame's decode/fill (K0/K1) "
                          "overlaps another's warp/resolve (K2/K3); default 3 for c1/c3 (one "
-                         "ingest per view), 2 for c2/c4, and 1 for c0 whose 0.1 ms steps "
-                         "are bound by the host's launch calls")
+                         "ingest per view), 2 for c2/c4, and 6 for c0, whose 640x360 kernels "
+                         "fill a fraction of the SMs (graph replays of 6 pipelines overlap)")
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
@@ -103,7 +103,7 @@ def parse():
         args.graphs = "on" if args.config == "c0" else "off"
     args.no_graphs = args.graphs == "off"
     if args.pipelines is None:
-        args.pipelines = {"c0": 1, "c1": 3, "c3": 3}.get(args.config, 2)
+        args.pipelines = {"c0": 6, "c1": 3, "c3": 3}.get(args.config, 2)
     return args
 
 

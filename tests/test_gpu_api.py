@@ -678,6 +678,57 @@ def test_captured_step_graph_replays_equal_eager_renders(cuda):
     np.testing.assert_array_equal(r.render([v], [refs])[0].cpu().numpy(), want[1])
 
 
+def test_concurrent_graph_pipelines_equal_eager_renders(cuda):
+    """bench.py's pipelines: private EdgeRenderers, each replaying its own
+    captured ticks on its own CUDA stream, concurrently (c0 runs 4 of them);
+    every pipeline's output equals the eager render of its frame."""
+    import torch
+
+    from paper_2007_00558_b200 import scenes
+    from paper_2007_00558_b200.engine import EdgeRenderer
+
+    wl = scenes.make_workload("c0", scale=2)
+    v, refs = wl.virtuals[0], wl.refs[0]
+    host = _noised_frames(wl, refs, 2, 23)
+
+    def dev(fr):
+        return {cid: tuple(torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+                           .to(cuda) for a in t) for cid, t in fr.items()}
+
+    def renderer():
+        r = EdgeRenderer(wl.rig, private=True)
+        for cid in refs:
+            c = wl.frames[0][cid]
+            r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+        return r
+
+    eager = renderer()
+    want = []
+    for fr in host:
+        eager.ingest_mm_many(fr)
+        want.append(eager.render([v], [refs])[0].cpu().numpy())
+    staged = [dev(fr) for fr in host]
+    P = 4
+    engs = [renderer() for _ in range(P)]
+    streams = [torch.cuda.Stream(cuda) for _ in range(P)]
+    outs = [torch.empty((1,) + want[0].shape, dtype=torch.uint8, device=cuda) for _ in range(P)]
+    graphs = {}
+    for i, e in enumerate(engs):
+        with torch.cuda.stream(streams[i]):
+            for fi in range(2):
+                graphs[i, fi] = e.capture_step(staged[fi], [v], [refs], out=outs[i])
+    torch.cuda.synchronize()
+    for rnd in range(40):
+        for i in range(P):
+            with torch.cuda.stream(streams[i]):
+                graphs[i, (rnd + i) % 2].replay()
+        if rnd % 13 == 0 or rnd == 39:
+            torch.cuda.synchronize()
+            for i in range(P):
+                np.testing.assert_array_equal(outs[i][0].cpu().numpy(), want[(rnd + i) % 2],
+                                              err_msg=f"round {rnd} pipeline {i}")
+
+
 def test_edge_stream_wire_format_equals_per_camera_yuv_ingest(cuda):
     """EdgeStream fed the edge server's wire format (12-bit YUV420 depth,
     pipeline.py:466-472; batched fvv_slots_ingest_yuv, graph replays) gives
