@@ -1525,10 +1525,12 @@ __device__ __forceinline__ bool fetch(const ResolveContrib &c, const DevCam &dst
 #undef FVV_CH
     const double s = dadd(dadd(dadd(w0, w1), w2), w3);
     if (!(s > 1e-12)) return false;
-    const double rs = rcp_nr(s);
-    c0 = div_rcp(c0, s, rs);
-    c1 = div_rcp(c1, s, rs);
-    c2 = div_rcp(c2, s, rs);
+    if (s != 1.0) {  // x / 1.0 is x: most all-Valid windows need no division
+        const double rs = rcp_nr(s);
+        c0 = div_rcp(c0, s, rs);
+        c1 = div_rcp(c1, s, rs);
+        c2 = div_rcp(c2, s, rs);
+    }
     return true;
 }
 
