@@ -747,9 +747,11 @@ cudaError_t launch_preprocess(const PreprocParams &p, cudaStream_t s) {
 __device__ __forceinline__ double proj_rint_r(double f, double x, double z, double r, double c) {
     const double num = dmul(f, x);
     const double ua = fma(num, r, c);
-    const double fl = floor(ua);
-    const double fr = ua - fl;
-    if (fabs(fr - 0.5) > 1e-6 && fabs(ua) < 1e8) return fr > 0.5 ? fl + 1.0 : fl;
+    // |ua - rint(ua)| is ua's exact distance to the nearest integer: more
+    // than 1e-6 away from k + 0.5, the approximate quotient rounds as the
+    // exact one does
+    const double ri = rint(ua);
+    if (fabs(ua - ri) < 0.5 - 1e-6 && fabs(ua) < 1e8) return ri;
     return rint(dadd(ddiv(num, z), c));
 }
 
