@@ -1063,7 +1063,12 @@ int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *stream
         chunks += (size_t)((nbytes[i] * 8 + kRiceChunkBits - 1) / kRiceChunkBits);
     }
     if ((rc = rice_scratch(ctx, px, chunks + n, skew, edge))) return rc;
-    LAUNCH(rice_decode_batch(pl, n, ctx->rice, ctx->stream));
+    {
+        const cudaError_t e = rice_decode_batch(pl, n, ctx->rice, ctx->stream);
+        if (e == cudaErrorLaunchTimeout)  // the rebuild's stall flag (k_med_rebuild_wave)
+            return fail(ctx, FVV_ECUDA, "MED rebuild: a strip never received the row above it");
+        LAUNCH(e);
+    }
     ctx->launches += 6;  // spec, >= 2 sync rounds, scan, emit, rebuild, deskew, adler (counted once)
     for (int i = 0; i < n; ++i) {
         status_out[i] = pl[i].status;
