@@ -466,12 +466,35 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
         __syncthreads();
         // no Valid pixel in the tile and its ring (sky, ray misses): no
         // candidate can reach min_valid > 0, skip the per-pixel counts
+        // (R = 2: the staged rows as Valid bitmasks, bit j of sbits[y][w] =
+        // smem pixel (y, 32 w + j), so a window row is one funnel shift and a
+        // popcount)
+        __shared__ uint32_t sbits[PSR][5];
         {
-            const int nw = (SR * SC + 3) / 4;
             int anyv = 0;
-            for (int i = tid; i < nw; i += 256) {
-                const uint32_t w = reinterpret_cast<const uint32_t *>(sv)[i];
-                anyv |= __vcmpeq4(w, 0u) != 0u;   // a Valid (0) byte
+            if (R == 2) {
+                for (int i = tid; i < SR * 5; i += 256) {
+                    const int y = i / 5, w = i - 5 * y;
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const int c = 32 * w + 4 * g;
+                        if (c < SC) {   // Valid == 0; 4 byte flags -> 4 bits
+                            const uint32_t m =
+                                __vcmpeq4(*reinterpret_cast<const uint32_t *>(sv + y * SC + c), 0u) &
+                                0x01010101u;
+                            bits |= (((m * 0x01020408u) >> 24) & 0xFu) << (4 * g);
+                        }
+                    }
+                    sbits[y][w] = bits;
+                    anyv |= bits != 0u;
+                }
+            } else {
+                const int nw = (SR * SC + 3) / 4;
+                for (int i = tid; i < nw; i += 256) {
+                    const uint32_t w = reinterpret_cast<const uint32_t *>(sv)[i];
+                    anyv |= __vcmpeq4(w, 0u) != 0u;   // a Valid (0) byte
+                }
             }
             if (!__syncthreads_or(anyv) && bl.min_valid > 0) return;
         }
@@ -487,14 +510,12 @@ __global__ void __launch_bounds__(256, FVV_PRE_MINB) k_preprocess(const __grid_c
                 if (((vp[r] >> (8 * q)) & 0xFFu) == FVV_INVALID) {
                     int cnt = 0;
                     if (R == 2) {
-                        // 5-byte window = 4 + 1 bytes out of two aligned words (Valid == 0)
-                        for (int dy = -2; dy <= 2; ++dy) {
-                            const int o = (row + 2 + dy) * SC + x;
-                            const uint32_t *w = reinterpret_cast<const uint32_t *>(sv) + (o >> 2);
-                            const uint64_t span = (((uint64_t)w[1] << 32) | w[0]) >> (8 * (o & 3));
-                            cnt += __popc(__vcmpeq4((uint32_t)span, 0u)) / 8 +
-                                   (((uint32_t)(span >> 32) & 0xFFu) == 0u);
-                        }
+                        // window columns x..x+4 of smem rows row..row+4
+                        const int w = x >> 5, sh = x & 31;
+#pragma unroll
+                        for (int dy = 0; dy < 5; ++dy)
+                            cnt += __popc(__funnelshift_r(sbits[row + dy][w], sbits[row + dy][w + 1], sh) &
+                                          0x1Fu);
                     } else {
                         for (int dy = -R; dy <= R; ++dy)
                             for (int dx = -R; dx <= R; ++dx)
