@@ -426,6 +426,12 @@ class FrameUploader:
                          for _ in range(depth)]
         self.done = [None] * depth        # copy-finished events
         self.free = [None] * depth        # consumer-finished events
+        # event objects reused per slot (a wait is bound to the record it
+        # follows, so re-recording one later is safe); saves their creation
+        # on every tick
+        self._done_ev = [torch.cuda.Event() for _ in range(depth)]
+        self._free_ev = [torch.cuda.Event() for _ in range(depth)]
+        self._lane_ev = [[torch.cuda.Event() for _ in self.extra] for _ in range(depth)]
         self.n = 0
         self.bytes = 0
 
@@ -476,26 +482,29 @@ class FrameUploader:
                     for dst, src in pairs[li::len(streams)]:
                         dst.copy_(src, non_blocking=True)
             self.bytes += sum(src.numel() * src.element_size() for _, src in pairs)
-        for st in self.extra:   # the ticket's event covers every lane
-            ev_l = torch.cuda.Event()
+        for st, ev_l in zip(self.extra, self._lane_ev[slot]):  # the ticket's event covers every lane
             ev_l.record(st)
             self.stream.wait_event(ev_l)
-        ev = torch.cuda.Event()
+        ev = self._done_ev[slot]
         ev.record(self.stream)
         self.done[slot] = ev
         self.n += 1
         return self.n - 1
 
-    def get(self, ticket: int) -> Mapping:
+    def get(self, ticket: int, stream=None) -> Mapping:
+        """The ticket's device buffers; ``stream`` (default: the current one)
+        waits for their copies."""
         slot = ticket % self.depth
-        torch.cuda.current_stream(self.dev).wait_event(self.done[slot])
+        (stream or torch.cuda.current_stream(self.dev)).wait_event(self.done[slot])
         return self.bufs[slot]
 
-    def release(self, ticket: int) -> None:
-        """The current stream is done reading this ticket's buffers."""
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.dev))
-        self.free[ticket % self.depth] = ev
+    def release(self, ticket: int, stream=None) -> None:
+        """``stream`` (default: the current one) is done reading this
+        ticket's buffers."""
+        slot = ticket % self.depth
+        ev = self._free_ev[slot]
+        ev.record(stream or torch.cuda.current_stream(self.dev))
+        self.free[slot] = ev
 
 
 class ResultDownloader:
@@ -523,13 +532,17 @@ class ResultDownloader:
         self.copied = [None] * depth       # D2H of the slot's device + host buffers done
         self.pending = [None] * depth      # (host view, tag) not yet handed to on_done
         self.on_done = on_done
+        # reused per slot: a slot's copy event is re-recorded only after
+        # _retire has waited for its previous record
+        self._ready_ev = [torch.cuda.Event() for _ in range(depth)]
+        self._copied_ev = [torch.cuda.Event() for _ in range(depth)]
 
-    def next_buffer(self) -> torch.Tensor:
-        """The device buffer the next ``put`` downloads; safe to write on the
-        current stream from now on."""
+    def next_buffer(self, stream=None) -> torch.Tensor:
+        """The device buffer the next ``put`` downloads; safe to write on
+        ``stream`` (default: the current one) from now on."""
         slot = self.n % self.depth
         if self.copied[slot] is not None:
-            torch.cuda.current_stream(self.dev).wait_event(self.copied[slot])
+            (stream or torch.cuda.current_stream(self.dev)).wait_event(self.copied[slot])
         return self.bufs[slot]
 
     def _retire(self, slot) -> None:
@@ -541,23 +554,24 @@ class ResultDownloader:
             if self.on_done is not None:
                 self.on_done(view, tag)
 
-    def put(self, views: torch.Tensor, tag=None) -> torch.Tensor:
-        """Queue the copy of ``views`` (after the current stream's work);
-        returns the pinned host tensor it lands in (valid once the copy is
-        done: ``on_done``, ``flush``, or ``depth`` puts later). ``views`` not
-        taken from ``next_buffer()``: the current stream waits for the copy
-        before running anything else, so it cannot be overwritten early."""
+    def put(self, views: torch.Tensor, tag=None, stream=None) -> torch.Tensor:
+        """Queue the copy of ``views`` (after the work queued so far on
+        ``stream``, default the current one); returns the pinned host tensor
+        it lands in (valid once the copy is done: ``on_done``, ``flush``, or
+        ``depth`` puts later). ``views`` not taken from ``next_buffer()``:
+        the stream waits for the copy before running anything else, so it
+        cannot be overwritten early."""
         slot = self.n % self.depth
         self._retire(slot)                 # host slot about to be reused
-        cur = torch.cuda.current_stream(self.dev)
-        ready = torch.cuda.Event()
+        cur = stream or torch.cuda.current_stream(self.dev)
+        ready = self._ready_ev[slot]
         ready.record(cur)
         own = views.untyped_storage().data_ptr() == self.bufs[slot].untyped_storage().data_ptr()
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(ready)
             dst = self.host[slot][:views.shape[0]]
             dst.copy_(views, non_blocking=True)
-            ev = torch.cuda.Event()
+            ev = self._copied_ev[slot]
             ev.record(self.stream)
         if not own:
             views.record_stream(self.stream)
@@ -638,9 +652,10 @@ class EdgeStream:
     def submit(self, frame: Mapping, virtuals: Sequence, refs=None, tag=None) -> torch.Tensor:
         up = self._uploader(frame)
         ticket = up.put(dict(sorted(frame.items())))
-        fr = up.get(ticket)
+        cur = torch.cuda.current_stream(self.dev)
+        fr = up.get(ticket, cur)
         n = len(virtuals)
-        out = self.dl.next_buffer()[:n]
+        out = self.dl.next_buffer(cur)[:n]
         key = None
         if self.graphs is not None and refs is not None:
             key = (id(up), ticket % up.depth, self.dl.n % self.dl.depth,
@@ -669,8 +684,8 @@ class EdgeStream:
             else:
                 self.r.ingest_yuv_many(fr, self.depth_range, hole_closing=self.hole_closing)
             self.r.render(virtuals, refs, out=out)
-        up.release(ticket)
-        return self.dl.put(out, tag)
+        up.release(ticket, cur)
+        return self.dl.put(out, tag, cur)
 
     def flush(self) -> None:
         self.dl.flush()
