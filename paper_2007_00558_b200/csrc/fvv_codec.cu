@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(1024) k_scan_planes(const __grid_constant__ Ri
 }
 
 // residuals of each plane's first n symbols (zig-zag inverse,
-// depthcodec.py:389), into the rebuild's anti-diagonal layout
+// depthcodec.py:389), into the rebuild's strip layout (skew_rc)
 __global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned long long *base,
                             int32_t *res) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -680,9 +680,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps) k_med_rebuild_wave(
 
 // strip-layout rebuild output -> raster plane (blockIdx.y = plane)
 // (4 consecutive pixels of a row per thread: 4-byte stores when W % 4 == 0)
-__global__ void k_deskew(const __grid_constant__ RiceBatch b, const uint8_t *diag_all) {
+__global__ void k_deskew(const __grid_constant__ RiceBatch b, const uint8_t *skew_all) {
     const RicePlane &pl = b.pl[blockIdx.y];
-    const uint8_t *skew = diag_all + pl.rbase;
+    const uint8_t *skew = skew_all + pl.rbase;
     const int W = pl.W, W4 = (W + 3) >> 2;
     const long long n4 = (long long)W4 * pl.H;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
