@@ -1069,7 +1069,7 @@ int fvv_rice_decode_planes(fvv_ctx *ctx, int32_t n, const uint8_t *const *stream
             return fail(ctx, FVV_ECUDA, "MED rebuild: a strip never received the row above it");
         LAUNCH(e);
     }
-    ctx->launches += 6;  // spec, >= 2 sync rounds, scan, emit, rebuild, deskew, adler (counted once)
+    ctx->launches += 12;  // spec, >= 2 sync rounds, 4 scan kernels, emit, rebuild, deskew, adler
     for (int i = 0; i < n; ++i) {
         status_out[i] = pl[i].status;
         adlers_out[i] = pl[i].status ? 0u : pl[i].adler;

@@ -12,19 +12,21 @@
 //           k_scan_blocks exclusive scan of the block sums (one CTA)
 //           k_rice_write  per-block scan, each symbol ORs its k+1 bits into
 //                         the zeroed stream (its q leading zeros are implicit)
-//   decode  k_rice_sync   chunked speculative decoding: every 256-bit chunk
-//                         decodes from an entry guess to its exit; rounds
-//                         re-decode chunks whose entry (= previous chunk's
-//                         exit) changed until none does. Rice codes
-//                         resynchronise within a few symbols, so 2-3 rounds
-//                         settle an exact symbol segmentation
-//           k_scan_blocks symbol base of every chunk
+//   decode  k_rice_spec / k_rice_sync  chunked speculative decoding: every
+//                         128-bit chunk decodes from an entry guess to its
+//                         exit; rounds re-decode chunks whose entry (= the
+//                         previous chunk's exit) changed until none does.
+//                         Rice codes resynchronise within a few symbols, so
+//                         2-3 rounds settle an exact symbol segmentation
+//           k_count_sums / k_scan_blocks / k_count_scan / k_plane_totals
+//                         symbol base of every chunk (one scan over the batch)
 //           k_rice_emit   each chunk writes its residuals
-//           k_med_rebuild_wave  the MED recurrence, one warp per 32-row
-//                         strip (lane = row, skewed by one column per lane,
+//           k_med_rebuild_wave  the MED recurrence, one warp per 128-row
+//                         strip (lane = 4 rows, one column of skew per row,
 //                         neighbours by shuffle), strip edges handed down
 //                         through epoch-tagged global slots; every strip of
 //                         every plane of a batch runs concurrently
+//           k_deskew      strip layout -> raster plane
 //           k_adler       adler32 of the rebuilt plane (zlib.adler32 check)
 
 #include <cstdint>
@@ -122,8 +124,21 @@ __device__ void scan_segment(unsigned long long *v, long long n, unsigned long l
     const long long per = ((n + 31) / 32 + 31) / 32 * 32;  // whole slices per warp
     const long long i0 = (long long)w * per;
     const long long i1 = i0 + per < n ? i0 + per : n;
+#ifndef FVV_SCAN_B
+#define FVV_SCAN_B 8
+#endif
+    constexpr int B = FVV_SCAN_B;  // slices whose loads are in flight together
     unsigned long long x = 0;
-    for (long long i = i0 + lane; i < i1; i += 32) x += v[i];
+    for (long long b0 = i0; b0 < i1; b0 += 32 * B) {
+        unsigned long long y[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const long long i = b0 + 32 * q + lane;
+            y[q] = i < i1 ? v[i] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < B; ++q) x += y[q];
+    }
     for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     if (lane == 0) ws[w] = x;
     __syncthreads();
@@ -137,16 +152,24 @@ __device__ void scan_segment(unsigned long long *v, long long n, unsigned long l
     }
     __syncthreads();
     unsigned long long carry = w ? ws[w - 1] : 0;
-    for (long long base = i0; base < i1; base += 32) {
-        const long long i = base + lane;
-        const unsigned long long y = i < i1 ? v[i] : 0;
-        unsigned long long inc = y;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
+    for (long long b0 = i0; b0 < i1; b0 += 32 * B) {
+        unsigned long long y[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const long long i = b0 + 32 * q + lane;
+            y[q] = i < i1 ? v[i] : 0;
         }
-        if (i < i1) v[i] = carry + inc - y;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const long long i = b0 + 32 * q + lane;
+            unsigned long long inc = y[q];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (i < i1) v[i] = carry + inc - y[q];
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
     }
     if (threadIdx.x == 0) *total = ws[31];
 }
@@ -423,13 +446,62 @@ __global__ void k_rice_sync(const __grid_constant__ RiceBatch b, const long long
     atomicAdd(changed, 1);
 }
 
-// exclusive scan of each plane's chunk counts (one CTA per plane); a
-// plane's total goes to totals[p]
-__global__ void __launch_bounds__(1024) k_scan_planes(const __grid_constant__ RiceBatch b,
-                                                      unsigned long long *v,
-                                                      unsigned long long *totals) {
-    const RicePlane &pl = b.pl[blockIdx.x];
-    scan_segment(v + pl.c0, pl.nchunks, totals + blockIdx.x);
+// Symbol bases: one exclusive scan of the chunk counts over the whole batch,
+// spread over the GPU (block sums, one CTA over the block sums, block-local
+// scans); a plane's symbol index is then base[j] - base[c0 of its plane].
+__global__ void __launch_bounds__(1024) k_count_sums(const unsigned long long *cnt, long long n,
+                                                     unsigned long long *bsum) {
+    __shared__ unsigned long long ws[32];
+    const long long i = (long long)blockIdx.x * 1024 + threadIdx.x;
+    unsigned long long x = i < n ? cnt[i] : 0;
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        x = ws[threadIdx.x];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (threadIdx.x == 0) bsum[blockIdx.x] = x;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_count_scan(const unsigned long long *cnt, long long n,
+                                                     const unsigned long long *boff,
+                                                     unsigned long long *base) {
+    __shared__ unsigned long long ws[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long i = (long long)blockIdx.x * 1024 + threadIdx.x;
+    const unsigned long long x = i < n ? cnt[i] : 0;
+    unsigned long long inc = x;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long t = ws[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        ws[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    if (i < n) base[i] = boff[blockIdx.x] + (w ? ws[w - 1] : 0) + inc - x;
+}
+
+// symbols per plane (the batch's grand total closes the last plane)
+__global__ void k_plane_totals(const __grid_constant__ RiceBatch b, const unsigned long long *base,
+                               const unsigned long long *grand, unsigned long long *totals) {
+    const int p = threadIdx.x;
+    if (p >= b.np) return;
+    const RicePlane &pl = b.pl[p];
+    if (!pl.nchunks) {
+        totals[p] = 0;
+        return;
+    }
+    const long long e = pl.c0 + pl.nchunks;
+    totals[p] = (e < b.nchunks ? base[e] : *grand) - base[pl.c0];
 }
 
 // residuals of each plane's first n symbols (zig-zag inverse,
@@ -440,7 +512,7 @@ __global__ void k_rice_emit(const __grid_constant__ RiceBatch b, const unsigned 
     if (j >= b.nchunks) return;
     const RicePlane &pl = b.pl[plane_of(b, j)];
     long long p = b.entry[j];
-    unsigned long long idx = base[j];
+    unsigned long long idx = base[j] - base[pl.c0];  // the plane's symbol index
     const unsigned long long cnt = b.count[j];
     int32_t *r = res + pl.rbase;
     // raster position of the first symbol; later ones step along the row
@@ -809,10 +881,14 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
             if (round > b.nchunks) return cudaErrorUnknown;  // cannot happen: >= 1 chunk settles per round
         }
         TRACE_EV("segment");
-        if ((e = cudaMemcpyAsync(sc.block, sc.count, sizeof(unsigned long long) * b.nchunks,
-                                 cudaMemcpyDeviceToDevice, s)))
-            return e;
-        k_scan_planes<<<np, 1024, 0, s>>>(b, sc.block, sc.total);
+        // block sums in exit_prev (free after the rounds), grand total in
+        // costs[0] (free until the adler32 pass)
+        const long long nblk = (b.nchunks + 1023) / 1024;
+        unsigned long long *bsum = reinterpret_cast<unsigned long long *>(sc.exit_prev);
+        k_count_sums<<<(unsigned)nblk, 1024, 0, s>>>(b.count, b.nchunks, bsum);
+        k_scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, sc.costs);
+        k_count_scan<<<(unsigned)nblk, 1024, 0, s>>>(b.count, b.nchunks, bsum, sc.block);
+        k_plane_totals<<<1, kRiceMaxPlanes, 0, s>>>(b, sc.block, sc.costs, sc.total);
         if ((e = cudaMemcpyAsync(tot, sc.total, sizeof(unsigned long long) * np,
                                  cudaMemcpyDeviceToHost, s)))
             return e;

@@ -7,7 +7,10 @@
 namespace fvv {
 
 constexpr int kRiceKMax = 14;          // depthcodec.py:380: k in range(15)
-constexpr int kRiceChunkBits = 256;    // decode chunk (speculative segmentation unit)
+#ifndef FVV_RICE_CHUNK
+#define FVV_RICE_CHUNK 128
+#endif
+constexpr int kRiceChunkBits = FVV_RICE_CHUNK;  // decode chunk (speculative segmentation unit)
 constexpr int kMedMaxWidth = 12288;    // MED rebuild: widest plane (strip rows of W + 31 steps)
 
 constexpr int kRiceMaxPlanes = 48;     // planes per decode batch (16 cameras x Y, U, V)
