@@ -889,21 +889,12 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
         k_scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, sc.costs);
         k_count_scan<<<(unsigned)nblk, 1024, 0, s>>>(b.count, b.nchunks, bsum, sc.block);
         k_plane_totals<<<1, kRiceMaxPlanes, 0, s>>>(b, sc.block, sc.costs, sc.total);
-        if ((e = cudaMemcpyAsync(tot, sc.total, sizeof(unsigned long long) * np,
-                                 cudaMemcpyDeviceToHost, s)))
-            return e;
-        if ((e = cudaStreamSynchronize(s))) return e;
         TRACE_EV("scan");
     }
-    // a plane whose stream runs out before its n symbols (a truncated symbol
-    // ends its chain) is reported and left undecoded
-    bool any = false;
-    for (int p = 0; p < np; ++p) {
-        planes[p].status = (long long)tot[p] < planes[p].n ? 1 : 0;
-        b.pl[p].status = planes[p].status;
-        any |= planes[p].status == 0;
-    }
-    if (!any) return cudaSuccess;
+    // no host round trip here: a plane whose stream runs out before its n
+    // symbols (a truncated symbol ends its chain) is found from the totals
+    // read back with the checksums at the end, and reported (its rebuilt
+    // bytes are then meaningless)
     if (b.nchunks) k_rice_emit<<<g, 128, 0, s>>>(b, sc.block, sc.res);
     TRACE_EV("emit");
     // edge tags: a fresh epoch per batch (the slots start zeroed, epoch 0 is
@@ -927,10 +918,14 @@ cudaError_t rice_decode_batch(RicePlane *planes, int np, RiceScratch &sc, cudaSt
         return e;
     if ((e = cudaMemcpyAsync(&stall, sc.wave + 1, sizeof(int), cudaMemcpyDeviceToHost, s)))
         return e;
+    if (b.nchunks && (e = cudaMemcpyAsync(tot, sc.total, sizeof(unsigned long long) * np,
+                                          cudaMemcpyDeviceToHost, s)))
+        return e;
     if ((e = cudaStreamSynchronize(s))) return e;
     TRACE_EV("adler");
     if (stall) return cudaErrorLaunchTimeout;  // a strip never received the row above
     for (int p = 0; p < np; ++p) {
+        planes[p].status = (long long)tot[p] < planes[p].n ? 1 : 0;
         const unsigned long long n = (unsigned long long)planes[p].n;
         const uint32_t A = (uint32_t)((1 + ab[2 * p]) % 65521ull);
         const uint32_t B = (uint32_t)((n % 65521ull + ab[2 * p + 1]) % 65521ull);
