@@ -1357,12 +1357,8 @@ __device__ __forceinline__ double winner_z(const ResolveContrib &c, const DevCam
 // A cell's winner as K3 keeps it in shared memory: the whole 64-bit key, or
 // (WT = uint32_t, for the wider contribution counts, whose mixes need the
 // shared memory) just its source index — the key's depth bits only order the
-// z-buffer, the exact z comes from zsrc. All ones = no winner either way.
-template <typename WT>
-__device__ __forceinline__ WT w_pack(uint64_t key, int b) {
-    if (sizeof(WT) == 8) return (WT)key;
-    return key == kEmpty ? (WT)~0u : (WT)(key & ((1ull << b) - 1));
-}
+// z-buffer, the exact z comes from zsrc. All ones = no winner either way
+// (resolve_cells packs them).
 template <typename WT>
 __device__ __forceinline__ bool w_none(WT w) { return w == (WT)~(WT)0; }
 template <typename WT>
@@ -1394,6 +1390,8 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
     b = hi;
 }
 
+__device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
 // Phase "cells" of one contribution: splat policy + FG cull (synthesis.py:
 // 207-219) for the 10x34 cells around the tile -> winner key (kEmpty = none).
 template <bool DBG, typename WT>
@@ -1401,6 +1399,12 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
                                              const uint64_t *K, WT *swk, uint8_t *sst,
                                              uint64_t gen, int x0, int y0, int tid) {
     int any = 0;
+    // a key is fresh (this view's generation) iff it is below `lim`: older
+    // generations carry larger tags and empty is all ones, so the ring min of
+    // a cell is fresh iff any of its neighbours is (the BG splat test), and a
+    // fresh key is never kEmpty (packs without the empty test)
+    const uint64_t lim = (gen + 1) << kGenShift;
+    const bool fgl = c.layer_fg;
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep) {
         const int i = tid + rep * FNT;
@@ -1409,11 +1413,8 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
         const int qy = y0 - 1 + by, qx = x0 - 1 + bx;
         uint64_t w = kEmpty;
         uint8_t sq = kStageNone;
-        if (qy >= 0 && qy < Hd && qx >= 0 && qx < Wd) {
+        if ((unsigned)qy < (unsigned)Hd && (unsigned)qx < (unsigned)Wd) {
             const int kc = (by + 1) * FKC + bx + 1;
-            // a key is fresh (this view's generation) iff it is below `lim`:
-            // older generations carry larger tags and empty is all ones
-            const uint64_t lim = (gen + 1) << kGenShift;
             w = K[kc];
             if (w < lim) {
                 sq = kStageCenter;
@@ -1421,33 +1422,31 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, int Wd, in
                 const uint64_t n0 = K[kc - FKC - 1], n1 = K[kc - FKC], n2 = K[kc - FKC + 1];
                 const uint64_t n3 = K[kc - 1], n4 = K[kc + 1];
                 const uint64_t n5 = K[kc + FKC - 1], n6 = K[kc + FKC], n7 = K[kc + FKC + 1];
-                const bool f0 = n0 < lim, f1 = n1 < lim, f2 = n2 < lim, f3 = n3 < lim,
-                           f4 = n4 < lim, f5 = n5 < lim, f6 = n6 < lim, f7 = n7 < lim;
-                w = kEmpty;
-                bool keep = f0 | f1 | f2 | f3 | f4 | f5 | f6 | f7;   // any splat at all
-                if (keep && c.layer_fg) {
+                bool keep;
+                if (fgl) {
                     // _neighbor_count (synthesis.py:79-87): in-image centre hits
+                    const bool f0 = n0 < lim, f1 = n1 < lim, f2 = n2 < lim, f3 = n3 < lim,
+                               f4 = n4 < lim, f5 = n5 < lim, f6 = n6 < lim, f7 = n7 < lim;
                     const bool up = qy > 0, dn = qy + 1 < Hd, lf = qx > 0, rt = qx + 1 < Wd;
                     const int cnt = (up && lf && f0) + (up && f1) + (up && rt && f2) + (lf && f3) +
                                     (rt && f4) + (dn && lf && f5) + (dn && f6) + (dn && rt && f7);
                     keep = cnt >= 5;
-                }
-                if (keep) {
+                    if (keep)
+                        w = min_u64(min_u64(min_u64(n0, n1), min_u64(n2, n3)),
+                                    min_u64(min_u64(n4, n5), min_u64(n6, n7)));
+                } else {
                     // the 8-ring min; stale keys compare larger than any fresh one
-                    uint64_t m = n0 < n1 ? n0 : n1;
-                    m = m < n2 ? m : n2;
-                    m = m < n3 ? m : n3;
-                    m = m < n4 ? m : n4;
-                    m = m < n5 ? m : n5;
-                    m = m < n6 ? m : n6;
-                    m = m < n7 ? m : n7;
-                    w = m;
-                    sq = kStageSplat;
+                    w = min_u64(min_u64(min_u64(n0, n1), min_u64(n2, n3)),
+                                min_u64(min_u64(n4, n5), min_u64(n6, n7)));
+                    keep = w < lim;
                 }
+                if (keep) sq = kStageSplat;
+                else w = kEmpty;
             }
             any |= w != kEmpty;
         }
-        swk[i] = w_pack<WT>(w, c.b);
+        if (sizeof(WT) == 8) swk[i] = (WT)w;
+        else swk[i] = sq != kStageNone ? (WT)(w & ((1ull << c.b) - 1)) : (WT)~(WT)0;
         if (DBG) sst[i] = sq;
     }
     return any;
