@@ -79,12 +79,15 @@ def parse():
     ap.add_argument("--extensions", action="store_true",
                     help="enable the two extensions outside the reference (angular blend "
                          "weights, K4 disocclusion inpainting); default is parity mode")
+    ap.add_argument("--e2e-path", default="native", choices=("native", "python"),
+                    help="e2e ticks through the native tick queue (fvv_tickq, one C call per "
+                         "tick) or the Python FrameUploader/ResultDownloader path")
     ap.add_argument("--graphs", default="auto", choices=("auto", "on", "off"),
                     help="replay each step as a captured CUDA graph (EdgeRenderer."
                          "capture_step) instead of host launches; auto = on for c0, whose "
                          "0.05 ms steps are bound by the host's launch calls, off for the "
                          "GPU-bound configs (a graph's device-side canvas generation step "
-                         "costs c1 ~1%); c3, whose every frame has its own view, always "
+                         "costs c1 ~1%%); c3, whose every frame has its own view, always "
                          "launches from the host")
     ap.add_argument("--launch-check", action="store_true",
                     help="launcher/sharding check without GPU work (CPU, gloo): every rank "
@@ -462,7 +465,7 @@ def wire_frame(caps, depth_range):
     return out
 
 
-def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
+def run_e2e(args, wl, engs, frames, views, dev, stream, wire: bool = False):
     """``e2e``: the same metric through the public host-memory API,
     ``engine.EdgeStream`` — every step's live inputs start in pinned host
     memory (RGB of the step's reference cameras + their depth: the 16-bit mm
@@ -524,41 +527,64 @@ def run_e2e(args, wl, eng, frames, views, dev, stream, wire: bool = False):
     def step_frame(s):
         return host[s % n_host]
 
-    es = EdgeStream(eng, max(len(v) for v in views), depth=2, depth_range=drange,
-                    graphs=args.e2e_graphs)
+    # one stream per pipeline (the device measurement's frames in flight):
+    # tick s goes to stream s % P
+    ess = [EdgeStream(e, max(len(v) for v in views), depth=2, depth_range=drange,
+                      graphs=args.e2e_graphs, native=args.e2e_path == "native")
+           for e in engs]
+    es = ess[0]
 
     def run(start, n):
         nv_ = 0
         for s in range(start, start + n):
             vi = step_views(s)
-            es.submit(step_frame(s), [wl.virtuals[v] for v in vi], [wl.refs[v] for v in vi])
+            ess[s % len(ess)].submit(step_frame(s), [wl.virtuals[v] for v in vi],
+                                     [wl.refs[v] for v in vi])
             nv_ += len(vi)
-        es.dl.wait_into(stream)
+        for e in ess:
+            e.wait_into(stream)
         return nv_
 
     # warm-up: at least two laps of the host-frame rotation, so every
     # repeating tick has been captured as a graph before the timed steps
-    run(0, max(args.warmup, 2 * len(host) + 2))
-    es.flush()
+    # (and at least three ticks per buffer slot of every stream)
+    run(0, max(args.warmup, 2 * len(host) + 2, 6 * len(ess)))
+    for e in ess:
+        e.flush()
     torch.cuda.synchronize()
     D.barrier()
-    b0, d0 = es.h2d_bytes, es.d2h_bytes
+
+    def moved():
+        return sum(e.h2d_bytes for e in ess), sum(e.d2h_bytes for e in ess)
+
+    b0, d0 = moved()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for up in es.ups.values():
-        up.stream.wait_event(e0)
-    es.dl.stream.wait_event(e0)
+    for e in ess:
+        for up in e.ups.values():
+            up.stream.wait_event(e0)
+        e.dl.stream.wait_event(e0)
     nv2 = run(args.warmup, args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
-    es.flush()
+    for e in ess:
+        e.flush()
     ms2 = D.max_over_ranks(e0.elapsed_time(e1))
+    b1, d1 = moved()
     return {"value": D.sum_over_ranks(nv2) / (ms2 / 1e3), "unit": "views/s",
-            "h2d_bytes_per_step": (es.h2d_bytes - b0) // args.steps,
-            "d2h_bytes_per_step": (es.d2h_bytes - d0) // args.steps,
+            "h2d_bytes_per_step": (b1 - b0) // args.steps,
+            "d2h_bytes_per_step": (d1 - d0) // args.steps,
+            "streams": len(ess),
             "input": ("12-bit YUV420 depth codes (pipeline.py:466-472) + RGB" if wire else
                       "16-bit mm + validity sidecar (mvdio.py:132) + RGB"),
-            "api": ("engine.EdgeStream.submit: pinned H2D of the tick's single-span receive "
+            "api": ("engine.EdgeStream.submit -> native tick queue (C ABI fvv_tickq_replay / "
+                    "fvv_tickq_submit): pinned H2D of the tick's single-span receive buffer "
+                    "(copy stream) -> "
+                    f"{'fvv_slots_ingest_yuv' if wire else 'fvv_slots_ingest_mm'} + "
+                    "fvv_render_views (CUDA graph replays of repeating ticks) -> D2H into "
+                    "pinned host buffers (download stream), double-buffered"
+                    if es.q is not None else
+                    "engine.EdgeStream.submit: pinned H2D of the tick's single-span receive "
                     "buffer (FrameUploader, copy stream) -> "
                     f"EdgeRenderer.{'ingest_yuv_many' if wire else 'ingest_mm_many'} + render "
                     f"(C ABI {'fvv_slots_ingest_yuv' if wire else 'fvv_slots_ingest_mm'}, "
@@ -764,8 +790,8 @@ def run_ours(args):
     if not args.no_e2e:
         # headline: the edge server's wire format (12-bit YUV420 depth);
         # beside it the mm + validity sidecar form (MVD container, mvdio.py)
-        e2e = run_e2e(args, wl, eng, frames, views, dev, stream, wire=True)
-        e2e_mm = run_e2e(args, wl, eng, frames, views, dev, stream, wire=False)
+        e2e = run_e2e(args, wl, engs, frames, views, dev, stream, wire=True)
+        e2e_mm = run_e2e(args, wl, engs, frames, views, dev, stream, wire=False)
     if rank != 0:
         return 0
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}

@@ -330,6 +330,45 @@ int fvv_render_views(fvv_ctx *ctx, const fvv_camera *virts, int32_t n_views,
                      const int32_t *ref_slots, const double *weights, int32_t n_refs,
                      const fvv_synth_cfg *cfg, uint8_t *rgb_out, uint8_t *provenance_out);
 
+/* ---- render-tick queue (the e2e edge-server loop) ------------------------
+ * pipeline.py:514-547 (EdgeServer.render_tick) fed from host memory, with its
+ * per-tick stream/event work native: each tick's rasters arrive in ONE
+ * pinned host span (a receive buffer); the queue copies it into an HBM
+ * staging slot on its H2D stream, runs the tick's ingest (K0 + K1) and
+ * render (K2 + K3) on the context's stream and copies the views into the
+ * caller's pinned host buffer on its D2H stream (pipeline.py:762-763
+ * on_display), `depth` ticks in flight: tick t reuses the slot of tick
+ * t - depth once that tick's compute and download are done. A tick with a
+ * non-zero key is captured as a CUDA graph on the second occurrence of
+ * (key, slot) and replayed by fvv_tickq_replay (at most max_graphs kept,
+ * least recently used dropped; 0 = never capture). Keys are the caller's
+ * identity of a tick: same cameras, raster offsets, views and references. */
+typedef struct fvv_tickq fvv_tickq;
+int fvv_tickq_create(fvv_ctx *ctx, int32_t depth, int64_t span_bytes, int64_t out_bytes,
+                     int32_t max_graphs, fvv_tickq **out);
+int fvv_tickq_destroy(fvv_tickq *q);
+/* kind 0: offs[4i..4i+3] = byte offsets of camera i's rgb, mm (uint16),
+ * validity (-1: none), unused; kind 1: rgb, y, u, v (12-bit YUV420 codes,
+ * z_near/z_far its depth range). Offsets 16-byte aligned. Views as
+ * fvv_render_views; host_out receives n_views*H*W*3 bytes. *ticket = the
+ * tick's number (fvv_tickq_wait). */
+int fvv_tickq_submit(fvv_tickq *q, const void *host_span, int64_t span_bytes, int32_t kind,
+                     int32_t n_cams, const int32_t *slots, const int64_t *offs, double z_near,
+                     double z_far, int32_t hole_closing, const fvv_camera *virts,
+                     int32_t n_views, const int32_t *ref_slots, const double *weights,
+                     int32_t n_refs, const fvv_synth_cfg *cfg, void *host_out, uint64_t key,
+                     int64_t *ticket);
+/* Replays the graph captured for (key, next slot): *ticket >= 0, or -1 when
+ * there is none (submit the tick instead). */
+int fvv_tickq_replay(fvv_tickq *q, const void *host_span, int64_t span_bytes, void *host_out,
+                     uint64_t key, int64_t *ticket);
+/* Blocks until tick `ticket`'s views are in its host buffer. */
+int fvv_tickq_wait(fvv_tickq *q, int64_t ticket);
+/* cuda_stream waits (on the device) for every download queued so far. */
+int fvv_tickq_fence(fvv_tickq *q, void *cuda_stream);
+int fvv_tickq_stats(fvv_tickq *q, int64_t *ticks, int64_t *h2d_bytes, int64_t *d2h_bytes,
+                    int64_t *replays, int64_t *graphs);
+
 #ifdef __cplusplus
 }
 #endif

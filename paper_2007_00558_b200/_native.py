@@ -40,7 +40,9 @@ EXPORTS = (
     "fvv_set_range_weights", "fvv_rice_stream_bound", "fvv_rice_encode_plane",
     "fvv_rice_decode_plane", "fvv_rice_decode_planes", "fvv_encode_mm", "fvv_rle_decode",
     "fvv_rle_encode", "fvv_slot_reset", "fvv_ctx_device_generation", "fvv_slots_ingest_yuv",
-    "fvv_profile_atomics", "fvv_count_atomics",
+    "fvv_profile_atomics", "fvv_count_atomics", "fvv_tickq_create", "fvv_tickq_destroy",
+    "fvv_tickq_submit", "fvv_tickq_replay", "fvv_tickq_wait", "fvv_tickq_fence",
+    "fvv_tickq_stats",
 )
 KERNELS = {"preprocess": 0, "forward_warp": 1, "resolve": 2, "fill": 3, "other": 4}
 
@@ -137,6 +139,17 @@ _SIGS = {
     "fvv_render_views": ([_VP, C.POINTER(FvvCamera), _I32, C.POINTER(C.c_int32),
                           C.POINTER(C.c_double), _I32, C.POINTER(FvvSynthCfg), _VP, _VP],
                          C.c_int),
+    "fvv_tickq_create": ([_VP, _I32, C.c_int64, C.c_int64, _I32, C.POINTER(C.c_void_p)], C.c_int),
+    "fvv_tickq_destroy": ([_VP], C.c_int),
+    "fvv_tickq_submit": ([_VP, _VP, C.c_int64, _I32, _I32, C.POINTER(C.c_int32),
+                          C.POINTER(C.c_int64), _D, _D, _I32, C.POINTER(FvvCamera), _I32,
+                          C.POINTER(C.c_int32), C.POINTER(C.c_double), _I32,
+                          C.POINTER(FvvSynthCfg), _VP, C.c_uint64, C.POINTER(C.c_int64)],
+                         C.c_int),
+    "fvv_tickq_replay": ([_VP, _VP, C.c_int64, _VP, C.c_uint64, C.POINTER(C.c_int64)], C.c_int),
+    "fvv_tickq_wait": ([_VP, C.c_int64], C.c_int),
+    "fvv_tickq_fence": ([_VP, _VP], C.c_int),
+    "fvv_tickq_stats": ([_VP] + [C.POINTER(C.c_int64)] * 5, C.c_int),
 }
 
 _lib = None

@@ -7,7 +7,9 @@
 #include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "fvv_capture.cuh"
@@ -1468,6 +1470,330 @@ int fvv_composite(fvv_ctx *ctx, const double *fg_color, const uint8_t *fg_valid,
     const double hole[3] = {(double)hole_color[0], (double)hole_color[1], (double)hole_color[2]};
     LAUNCH(launch_composite(fg_color, fg_valid, bg_color, bg_valid, width, height, hole, rgb_out,
                             provenance_out, ctx->stream));
+    return FVV_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Render-tick queue: the e2e edge-server loop (pipeline.py:514-547 render
+// tick, 762-763 on_display) fed from pinned host memory, with every per-tick
+// stream and event operation in native code. Tick t uses buffer slot
+// t % depth: its span is copied into stage[slot] on the H2D stream (after the
+// compute of tick t - depth finished reading that slot), the context's
+// stream waits for it and for the download of tick t - depth out of
+// dout[slot], runs the tick's ingest (K0 + K1) and render (K2 + K3) into
+// dout[slot] — eagerly, or as the CUDA graph captured on the key's second
+// occurrence — and the D2H stream copies the views to the caller's pinned
+// buffer. depth ticks are in flight, so the copies of ticks t+1 / t-1
+// overlap the compute of tick t.
+
+struct fvv_tickq {
+    fvv_ctx *ctx = nullptr;
+    int depth = 0;
+    int64_t span_cap = 0, out_cap = 0;
+    int max_graphs = 0;
+    std::vector<uint8_t *> stage, dout;
+    std::vector<cudaEvent_t> up, done, down;  // span landed / tick's compute done / views landed
+    std::vector<bool> used;
+    // ticks run on the queue's own compute stream (capturable, unlike the
+    // legacy default stream a context may be bound to), ordered after the
+    // context stream's work at submission and before its later work
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp = nullptr;
+    cudaEvent_t entry = nullptr;
+    cudaStream_t saved = nullptr;
+    int64_t n = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0, replays = 0;
+    struct Graph {
+        cudaGraphExec_t exec;
+        int64_t span_bytes, out_bytes, launches;
+        uint64_t last_use;
+    };
+    std::map<std::pair<uint64_t, int>, Graph> graphs;  // (key, slot)
+    std::map<std::pair<uint64_t, int>, uint64_t> seen;  // eager ticks per (key, slot)
+};
+
+namespace {
+
+int tickq_begin(fvv_tickq *q, const void *host_span, int64_t span_bytes, int slot) {
+    fvv_ctx *ctx = q->ctx;
+    if (q->used[slot]) CK(cudaStreamWaitEvent(q->h2d, q->done[slot], 0));
+    CK(cudaMemcpyAsync(q->stage[slot], host_span, (size_t)span_bytes, cudaMemcpyHostToDevice,
+                       q->h2d));
+    CK(cudaEventRecord(q->up[slot], q->h2d));
+    CK(cudaEventRecord(q->entry, ctx->stream));
+    CK(cudaStreamWaitEvent(q->comp, q->entry, 0));
+    CK(cudaStreamWaitEvent(q->comp, q->up[slot], 0));
+    if (q->used[slot]) CK(cudaStreamWaitEvent(q->comp, q->down[slot], 0));
+    q->h2d_bytes += span_bytes;
+    // the tick's library calls go to the compute stream
+    q->saved = ctx->stream;
+    ctx->stream = q->comp;
+    return FVV_OK;
+}
+
+// the context's stream back (after a tick, or after a failed one)
+void tickq_restore(fvv_tickq *q) {
+    if (q->ctx->stream == q->comp) q->ctx->stream = q->saved;
+}
+
+int tickq_end(fvv_tickq *q, void *host_out, int64_t out_bytes, int slot, int64_t *ticket) {
+    fvv_ctx *ctx = q->ctx;
+    tickq_restore(q);
+    CK(cudaEventRecord(q->done[slot], q->comp));
+    CK(cudaStreamWaitEvent(ctx->stream, q->done[slot], 0));
+    CK(cudaStreamWaitEvent(q->d2h, q->done[slot], 0));
+    CK(cudaMemcpyAsync(host_out, q->dout[slot], (size_t)out_bytes, cudaMemcpyDeviceToHost,
+                       q->d2h));
+    CK(cudaEventRecord(q->down[slot], q->d2h));
+    q->used[slot] = true;
+    q->d2h_bytes += out_bytes;
+    if (ticket) *ticket = q->n;
+    ++q->n;
+    return FVV_OK;
+}
+
+void tickq_evict(fvv_tickq *q) {
+    while ((int)q->graphs.size() > q->max_graphs) {
+        auto lru = q->graphs.begin();
+        for (auto it = q->graphs.begin(); it != q->graphs.end(); ++it)
+            if (it->second.last_use < lru->second.last_use) lru = it;
+        cudaGraphExecDestroy(lru->second.exec);
+        q->graphs.erase(lru);
+    }
+    while ((int)q->seen.size() > 4 * q->max_graphs) {
+        auto old = q->seen.begin();
+        for (auto it = q->seen.begin(); it != q->seen.end(); ++it)
+            if (it->second < old->second) old = it;
+        q->seen.erase(old);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fvv_tickq_create(fvv_ctx *ctx, int32_t depth, int64_t span_bytes, int64_t out_bytes,
+                     int32_t max_graphs, fvv_tickq **out) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!out || depth < 1 || depth > 16 || span_bytes <= 0 || out_bytes <= 0 || max_graphs < 0)
+        return fail(ctx, FVV_EINVAL, "tickq_create: bad arguments");
+    *out = nullptr;
+    fvv_tickq *q = new fvv_tickq();
+    q->ctx = ctx;
+    q->depth = depth;
+    q->span_cap = span_bytes;
+    q->out_cap = out_bytes;
+    q->max_graphs = max_graphs;
+    q->stage.assign(depth, nullptr);
+    q->dout.assign(depth, nullptr);
+    q->up.assign(depth, nullptr);
+    q->done.assign(depth, nullptr);
+    q->down.assign(depth, nullptr);
+    q->used.assign(depth, false);
+    cudaError_t e = cudaStreamCreateWithFlags(&q->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q->d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q->comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->entry, cudaEventDisableTiming);
+    for (int i = 0; i < depth && e == cudaSuccess; ++i) {
+        e = cudaMalloc(&q->stage[i], (size_t)span_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&q->dout[i], (size_t)out_bytes);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->up[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->done[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->down[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        fvv_tickq_destroy(q);
+        return fail(ctx, FVV_ECUDA, "tickq_create: %s", cudaGetErrorString(e));
+    }
+    // captured ticks need the device-resident canvas generation
+    if (max_graphs > 0 && (rc = fvv_ctx_device_generation(ctx, 1))) {
+        fvv_tickq_destroy(q);
+        return rc;
+    }
+    *out = q;
+    return FVV_OK;
+}
+
+int fvv_tickq_destroy(fvv_tickq *q) {
+    if (!q) return FVV_EINVAL;
+    cudaSetDevice(q->ctx->device);
+    if (q->h2d) cudaStreamSynchronize(q->h2d);
+    if (q->d2h) cudaStreamSynchronize(q->d2h);
+    if (q->comp) cudaStreamSynchronize(q->comp);
+    for (auto &g : q->graphs) cudaGraphExecDestroy(g.second.exec);
+    for (int i = 0; i < q->depth; ++i) {
+        cudaFree(q->stage[i]);
+        cudaFree(q->dout[i]);
+        if (q->up[i]) cudaEventDestroy(q->up[i]);
+        if (q->done[i]) cudaEventDestroy(q->done[i]);
+        if (q->down[i]) cudaEventDestroy(q->down[i]);
+    }
+    if (q->h2d) cudaStreamDestroy(q->h2d);
+    if (q->d2h) cudaStreamDestroy(q->d2h);
+    if (q->comp) cudaStreamDestroy(q->comp);
+    if (q->entry) cudaEventDestroy(q->entry);
+    delete q;
+    return FVV_OK;
+}
+
+int fvv_tickq_submit(fvv_tickq *q, const void *host_span, int64_t span_bytes, int32_t kind,
+                     int32_t n_cams, const int32_t *slots, const int64_t *offs, double z_near,
+                     double z_far, int32_t hole_closing, const fvv_camera *virts,
+                     int32_t n_views, const int32_t *ref_slots, const double *weights,
+                     int32_t n_refs, const fvv_synth_cfg *cfg, void *host_out, uint64_t key,
+                     int64_t *ticket) {
+    if (!q) return FVV_EINVAL;
+    fvv_ctx *ctx = q->ctx;
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!host_span || !host_out || !offs || !slots || !virts || n_views < 1 || n_cams < 1 ||
+        n_cams > FVV_MAX_REFS || (kind != 0 && kind != 1))
+        return fail(ctx, FVV_EINVAL, "tickq_submit: bad arguments");
+    if (span_bytes <= 0 || span_bytes > q->span_cap)
+        return fail(ctx, FVV_EINVAL, "tickq_submit: span of %lld bytes, the queue holds %lld",
+                    (long long)span_bytes, (long long)q->span_cap);
+    const int64_t out_bytes = (int64_t)n_views * virts[0].width * virts[0].height * 3;
+    if (out_bytes > q->out_cap)
+        return fail(ctx, FVV_EINVAL, "tickq_submit: %d views need %lld output bytes, the queue "
+                    "holds %lld", n_views, (long long)out_bytes, (long long)q->out_cap);
+    for (int i = 0; i < n_cams; ++i) {
+        if (!(slots[i] >= 0 && slots[i] < FVV_MAX_SLOTS && ctx->slots[slots[i]].has_cam))
+            return fail(ctx, FVV_EINVAL, "slot %d has no camera", slots[i]);
+        const fvv_camera &c = ctx->slots[slots[i]].cam;
+        const int64_t px = (int64_t)c.width * c.height;
+        // bytes each raster of the camera occupies in the span
+        const int64_t need[4] = {3 * px, kind == 0 ? 2 * px : px, kind == 0 ? px : px / 4,
+                                 kind == 0 ? 0 : px / 4};
+        for (int r = 0; r < 4; ++r) {
+            const int64_t o = offs[4 * i + r];
+            if (o < 0 && (r == 0 || r == 1 || (kind == 1 && r > 0)))
+                return fail(ctx, FVV_EINVAL, "tickq_submit: camera %d lacks raster %d", i, r);
+            // 16-byte aligned like a device allocation (K0's vector loads)
+            if (o >= 0 && (o + need[r] > span_bytes || (o & 15)))
+                return fail(ctx, FVV_EINVAL, "tickq_submit: raster %d of camera %d lies outside "
+                            "the span or is not 16-byte aligned", r, i);
+        }
+    }
+    const int slot = (int)(q->n % q->depth);
+    const auto gk = std::make_pair(key, slot);
+    if ((rc = tickq_begin(q, host_span, span_bytes, slot))) return rc;
+    // the tick's ingest + render (the context's stream is the queue's now)
+    auto tick = [&]() -> int {
+        const uint8_t *base = q->stage[slot];
+        const uint8_t *p[4][FVV_MAX_REFS];
+        for (int i = 0; i < n_cams; ++i)
+            for (int r = 0; r < 4; ++r)
+                p[r][i] = offs[4 * i + r] >= 0 ? base + offs[4 * i + r] : nullptr;
+        int e;
+        if (kind == 0) {
+            bool all_v = true;
+            for (int i = 0; i < n_cams; ++i) all_v = all_v && p[2][i];
+            e = fvv_slots_ingest_mm(ctx, n_cams, slots, p[0],
+                                    reinterpret_cast<const uint16_t *const *>(p[1]),
+                                    all_v ? p[2] : nullptr, hole_closing);
+        } else {
+            e = fvv_slots_ingest_yuv(ctx, n_cams, slots, p[0], p[1], p[2], p[3], z_near, z_far,
+                                     hole_closing);
+        }
+        if (e) return e;
+        return fvv_render_views(ctx, virts, n_views, ref_slots, weights, n_refs, cfg,
+                                q->dout[slot], nullptr);
+    };
+    // eager, or captured on the key's second occurrence and launched
+    auto run = [&]() -> int {
+        auto it = key != 0 && q->max_graphs > 0 ? q->seen.find(gk) : q->seen.end();
+        if (it != q->seen.end() && it->second != UINT64_MAX) {
+            const int64_t l0 = ctx->launches;
+            CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            const int e = tick();
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+            cudaGraphExec_t exec = nullptr;
+            cudaError_t ei = ec;
+            if (!e && ec == cudaSuccess) ei = cudaGraphInstantiate(&exec, g, 0);
+            if (g) cudaGraphDestroy(g);
+            if (e) return e;  // an argument error: the eager tick would fail alike
+            if (ei == cudaSuccess) {
+                q->seen.erase(it);
+                q->graphs[gk] = {exec, span_bytes, out_bytes, ctx->launches - l0,
+                                 (uint64_t)q->n};
+                tickq_evict(q);
+                CK(cudaGraphLaunch(exec, ctx->stream));
+                return FVV_OK;
+            }
+            // not capturable (e.g. a first-use allocation): this key stays eager
+            cudaGetLastError();
+            ctx->launches = l0;
+            it->second = UINT64_MAX;
+        } else if (it == q->seen.end() && key != 0 && q->max_graphs > 0) {
+            q->seen[gk] = (uint64_t)q->n;
+            tickq_evict(q);
+        }
+        return tick();
+    };
+    if ((rc = run())) {
+        tickq_restore(q);
+        return rc;
+    }
+    return tickq_end(q, host_out, out_bytes, slot, ticket);
+}
+
+int fvv_tickq_replay(fvv_tickq *q, const void *host_span, int64_t span_bytes, void *host_out,
+                     uint64_t key, int64_t *ticket) {
+    if (!q || !ticket) return FVV_EINVAL;
+    fvv_ctx *ctx = q->ctx;
+    *ticket = -1;
+    if (key == 0) return FVV_OK;
+    const int slot = (int)(q->n % q->depth);
+    auto it = q->graphs.find(std::make_pair(key, slot));
+    if (it == q->graphs.end()) return FVV_OK;  // not captured (yet): submit the tick
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!host_span || !host_out || span_bytes != it->second.span_bytes)
+        return fail(ctx, FVV_EINVAL, "tickq_replay: span of %lld bytes, the tick was captured "
+                    "with %lld", (long long)span_bytes, (long long)it->second.span_bytes);
+    if ((rc = tickq_begin(q, host_span, span_bytes, slot))) return rc;
+    const cudaError_t el = cudaGraphLaunch(it->second.exec, ctx->stream);
+    if (el != cudaSuccess) {
+        tickq_restore(q);
+        return fail(ctx, FVV_ECUDA, "tick graph launch: %s", cudaGetErrorString(el));
+    }
+    ctx->launches += it->second.launches;
+    it->second.last_use = (uint64_t)q->n;
+    ++q->replays;
+    return tickq_end(q, host_out, it->second.out_bytes, slot, ticket);
+}
+
+int fvv_tickq_wait(fvv_tickq *q, int64_t ticket) {
+    if (!q) return FVV_EINVAL;
+    fvv_ctx *ctx = q->ctx;
+    if (ticket < 0 || ticket >= q->n) return fail(ctx, FVV_EINVAL, "tickq_wait: no tick %lld", (long long)ticket);
+    // the slot's latest download is this tick's or a later one (the D2H
+    // stream runs in order)
+    CK(cudaEventSynchronize(q->down[ticket % q->depth]));
+    return FVV_OK;
+}
+
+int fvv_tickq_fence(fvv_tickq *q, void *cuda_stream) {
+    if (!q) return FVV_EINVAL;
+    fvv_ctx *ctx = q->ctx;
+    int rc = enter(ctx);
+    if (rc) return rc;
+    for (int i = 0; i < q->depth; ++i)
+        if (q->used[i]) CK(cudaStreamWaitEvent((cudaStream_t)cuda_stream, q->down[i], 0));
+    return FVV_OK;
+}
+
+int fvv_tickq_stats(fvv_tickq *q, int64_t *ticks, int64_t *h2d_bytes, int64_t *d2h_bytes,
+                    int64_t *replays, int64_t *graphs) {
+    if (!q) return FVV_EINVAL;
+    if (ticks) *ticks = q->n;
+    if (h2d_bytes) *h2d_bytes = q->h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = q->d2h_bytes;
+    if (replays) *replays = q->replays;
+    if (graphs) *graphs = (int64_t)q->graphs.size();
     return FVV_OK;
 }
 

@@ -594,6 +594,73 @@ class ResultDownloader:
                 stream.wait_event(ev)
 
 
+class TickQueue:
+    """The native render-tick queue (``fvv_tickq_*``, include/fvv_b200.h):
+    one tick's host span -> HBM staging slot (H2D stream) -> ingest + render
+    on the renderer's stream -> views -> pinned host buffer (D2H stream),
+    ``depth`` ticks in flight, repeating ticks replayed from CUDA graphs —
+    every per-tick stream and event operation in native code. Used by
+    ``EdgeStream`` for frames held in one host allocation."""
+
+    def __init__(self, renderer: "EdgeRenderer", depth: int, span_bytes: int, out_bytes: int,
+                 max_graphs: int):
+        self.ctx = renderer.ctx
+        self.lib = self.ctx.lib
+        h = C.c_void_p()
+        self.ctx.check(self.lib.fvv_tickq_create(self.ctx.h, int(depth), int(span_bytes),
+                                                 int(out_bytes), int(max_graphs), C.byref(h)),
+                       "fvv_tickq_create")
+        self.h = h
+        self.span_bytes, self.out_bytes = int(span_bytes), int(out_bytes)
+        self._t = C.c_int64()
+
+    def replay(self, span_ptr: int, span_bytes: int, out_ptr: int, key: int) -> int:
+        """The captured tick of ``key``: its ticket, or -1 (submit it)."""
+        rc = self.lib.fvv_tickq_replay(self.h, span_ptr, span_bytes, out_ptr, key,
+                                       C.byref(self._t))
+        if rc:
+            self.ctx.check(rc, "fvv_tickq_replay")
+        return self._t.value
+
+    def submit(self, *args) -> int:
+        self.ctx.check(self.lib.fvv_tickq_submit(self.h, *args, C.byref(self._t)),
+                       "fvv_tickq_submit")
+        return self._t.value
+
+    def wait(self, ticket: int) -> None:
+        self.ctx.check(self.lib.fvv_tickq_wait(self.h, int(ticket)), "fvv_tickq_wait")
+
+    def fence(self, stream) -> None:
+        self.ctx.check(self.lib.fvv_tickq_fence(self.h, C.c_void_p(stream.cuda_stream)),
+                       "fvv_tickq_fence")
+
+    def stats(self) -> dict:
+        v = [C.c_int64() for _ in range(5)]
+        self.ctx.check(self.lib.fvv_tickq_stats(self.h, *[C.byref(x) for x in v]),
+                       "fvv_tickq_stats")
+        return dict(zip(("ticks", "h2d_bytes", "d2h_bytes", "replays", "graphs"),
+                        (x.value for x in v)))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.fvv_tickq_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _view_key(v) -> tuple:
+    """A virtual camera's identity for the tick key (intrinsics + pose bytes)."""
+    k = v.intrinsics
+    return (int(k.width), int(k.height), float(k.fx), float(k.fy), float(k.cx), float(k.cy),
+            np.asarray(v.pose.rotation, dtype=np.float64).tobytes(),
+            np.asarray(v.pose.center, dtype=np.float64).tobytes())
+
+
 class EdgeStream:
     """The edge server fed from host memory (the e2e path of bench.py):
     frames of pinned host rasters in, rendered views in pinned host memory
@@ -609,19 +676,27 @@ class EdgeStream:
     views once they are in host memory (pipeline.py:762-763 ``on_display``);
     ``flush()`` drains the last ones. With ``graphs`` (default), a tick whose
     buffers, views and references repeat is replayed from a CUDA graph
-    captured on its second occurrence (EdgeRenderer.capture_step; at most
-    ``max_graphs`` kept, least recently used dropped).
+    captured on its second occurrence (at most ``max_graphs`` kept, least
+    recently used dropped).
+
+    A frame whose rasters all live in one host allocation (the way a receive
+    buffer holds a tick), 16-byte aligned, goes through the native tick queue
+    (``TickQueue``, ``native=True``): one call per tick, its copies, events,
+    ingest, render and graph replays issued in C++. Other frames go through
+    ``FrameUploader`` / ``EdgeRenderer`` / ``ResultDownloader``.
     """
 
     def __init__(self, renderer: "EdgeRenderer", max_views: int, depth: int = 2,
                  on_view=None, hole_closing: bool = True, depth_range=None,
-                 graphs: bool = True, max_graphs: int = 64):
+                 graphs: bool = True, max_graphs: int = 64, native: bool = True):
         self.r = renderer
         dev = torch.device("cuda", renderer.ctx.device)
         self.dev = dev
         k = renderer.rig[0].intrinsics
+        self.max_views = int(max_views)
         self.dl = ResultDownloader((max_views, int(k.height), int(k.width), 3), depth, dev,
                                    on_done=on_view)
+        self.on_view = on_view
         self.depth = depth
         self.ups = {}
         self.hole_closing = hole_closing
@@ -633,6 +708,16 @@ class EdgeStream:
         self.seen = OrderedDict()
         self.max_graphs = max_graphs
         self.graph_launches = 0
+        # native tick queue state
+        self.native = native
+        self.q = None
+        self._qhost = None          # depth pinned host view buffers
+        self._qpend = [None] * depth  # per host buffer: (ticket, views, tag)
+        self._qn = 0
+        self._qkeys = {}            # tick key -> id (ids never reused)
+        self._qnext = 1
+        self._spans = {}            # id(frame) -> (rasters, span layout)
+        self._mode = None           # "native" | "python": the path of the last tick
 
     def _uploader(self, frame):
         key = tuple((cid, tuple(tuple(t.shape) for t in ts)) for cid, ts in sorted(frame.items()))
@@ -643,13 +728,144 @@ class EdgeStream:
 
     @property
     def h2d_bytes(self) -> int:
-        return sum(u.bytes for u in self.ups.values())
+        n = sum(u.bytes for u in self.ups.values())
+        return n + (self.q.stats()["h2d_bytes"] if self.q is not None else 0)
 
     @property
     def d2h_bytes(self) -> int:
-        return self.dl.bytes
+        return self.dl.bytes + (self.q.stats()["d2h_bytes"] if self.q is not None else 0)
+
+    # -- native path ------------------------------------------------------------
+
+    def _span(self, frame: Mapping):
+        """(host pointer, span bytes, kind, camera ids, offsets, layout key) of
+        a frame held in one 16-byte aligned host allocation, else None."""
+        rasters = tuple(t for v in frame.values() for t in v)
+        hit = self._spans.get(id(frame))
+        if hit is not None and len(hit[0]) == len(rasters) and all(
+                a is b for a, b in zip(hit[0], rasters)):
+            return hit[1]
+        per = 4 if self.depth_range is not None else 3
+        ent = None
+        if all(isinstance(t, torch.Tensor) and t.device.type == "cpu" for t in rasters) and \
+                all(len(v) == per for v in frame.values()):
+            lay = FrameUploader._layout(frame)
+            if lay is not None:
+                lo, span, offs = lay
+                base = rasters[0].untyped_storage().data_ptr() + lo
+                flat = [o for v in offs for o in (list(v) + [-1] * (4 - len(v)))]
+                if base % 16 == 0 and all(o % 16 == 0 for o in flat if o >= 0):
+                    cids = list(frame.keys())
+                    ent = (base, span, 0 if per == 3 else 1, cids, flat,
+                           (tuple(cids), tuple(flat), span))
+        if len(self._spans) > 256:
+            self._spans.clear()
+        self._spans[id(frame)] = (rasters, ent)
+        return ent
+
+    def _retire_native(self, slot: int) -> None:
+        pend, self._qpend[slot] = self._qpend[slot], None
+        if pend is not None:
+            self.q.wait(pend[0])
+            if self.on_view is not None:
+                self.on_view(pend[1], pend[2])
+
+    def _flush_native(self) -> None:
+        for i in range(self._qn - self.depth, self._qn):
+            if i >= 0:
+                self._retire_native(i % self.depth)
+
+    def _submit_native(self, frame: Mapping, virtuals: Sequence, refs, tag):
+        ent = self._span(frame)
+        if ent is None:
+            return None
+        base, span, kind, cids, offs, lkey = ent
+        n = len(virtuals)
+        if n > self.max_views:
+            raise ValueError(f"{n} views, the stream holds {self.max_views}")
+        k = virtuals[0].intrinsics
+        H, W = int(k.height), int(k.width)
+        if self.q is None or span > self.q.span_bytes:
+            if self.q is not None:
+                self._flush_native()
+                self.q.close()
+            rk = self.r.rig[0].intrinsics
+            out_bytes = self.max_views * max(H * W, int(rk.height) * int(rk.width)) * 3
+            self.q = TickQueue(self.r, self.depth, span, out_bytes,
+                               self.max_graphs if self.graphs is not None else 0)
+            self._qhost = [torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
+                           for _ in range(self.depth)]
+            self._qn = 0
+        if self._mode == "python":
+            self.dl.flush()
+        self._mode = "native"
+        self.r._bind()
+        slot = self._qn % self.depth
+        self._retire_native(slot)
+        host = self._qhost[slot]
+        views = host[:n * H * W * 3].view(n, H, W, 3)
+        kid = 0
+        if self.graphs is not None and refs is not None:
+            key = (lkey, tuple(_view_key(v) for v in virtuals), tuple(tuple(r) for r in refs),
+                   self.r.cfg)
+            kid = self._qkeys.get(key)
+            if kid is None:
+                if len(self._qkeys) >= 16 * self.max_graphs:
+                    self._qkeys.clear()   # ids are never reused: stale graphs just age out
+                kid = self._qkeys[key] = self._qnext
+                self._qnext += 1
+        l0 = self.r.ctx.launches()
+        ticket = self.q.replay(base, span, host.data_ptr(), kid)
+        if ticket >= 0:
+            self.graph_launches += self.r.ctx.launches() - l0
+        else:
+            # a new tick: the renderer's raster checks and reference plan, then
+            # the eager (or, on its second occurrence, capturing) submit
+            for cid, ts in frame.items():
+                self.r._slot(cid)
+                H2, W2 = self.r._hw(cid)
+                self.r._check(ts[0], cid, "colour", 3)
+                self.r._check(ts[1], cid, "mm raster" if kind == 0 else "Y plane")
+                if kind == 0:
+                    self.r._check(ts[2], cid, "validity")
+                for a, what in (((ts[2], "U plane"), (ts[3], "V plane")) if kind else ()):
+                    if tuple(a.shape) != (H2 // 2, W2 // 2):
+                        raise ValueError(f"camera {cid}: {what} has shape {tuple(a.shape)}, "
+                                         f"its calibration needs {(H2 // 2, W2 // 2)}")
+            self.r.ctx.range_weights(_native._DEFAULT_SIGMA_RANGE)
+            before = set(self.r.ingested)
+            self.r.ingested.update(cids)
+            try:
+                refs2, weights = self.r.plan(virtuals, refs)
+            except ValueError:
+                self.r.ingested = before
+                raise
+            nr = len(refs2[0])
+            dr = self.depth_range
+            ticket = self.q.submit(
+                C.c_void_p(base), span, kind, len(cids),
+                (C.c_int32 * len(cids))(*[self.r.slot[c] for c in cids]),
+                (C.c_int64 * len(offs))(*offs),
+                float(dr.z_near) if dr is not None else 0.0,
+                float(dr.z_far) if dr is not None else 0.0, int(bool(self.hole_closing)),
+                (_native.FvvCamera * n)(*[_native.camera(v) for v in virtuals]), n,
+                (C.c_int32 * (n * nr))(*[self.r.slot[c] for r in refs2 for c in r]),
+                (C.c_double * (n * nr))(*[w for ws in weights for w in ws]), nr,
+                C.byref(_native.synth_cfg(self.r.cfg)), C.c_void_p(host.data_ptr()), kid)
+        self._qpend[slot] = (ticket, views, tag)
+        self._qn += 1
+        return views
+
+    # -- public ---------------------------------------------------------------------
 
     def submit(self, frame: Mapping, virtuals: Sequence, refs=None, tag=None) -> torch.Tensor:
+        if self.native:
+            got = self._submit_native(frame, virtuals, refs, tag)
+            if got is not None:
+                return got
+        if self._mode == "native":
+            self._flush_native()
+        self._mode = "python"
         up = self._uploader(frame)
         ticket = up.put(dict(sorted(frame.items())))
         cur = torch.cuda.current_stream(self.dev)
@@ -687,5 +903,13 @@ class EdgeStream:
         up.release(ticket, cur)
         return self.dl.put(out, tag, cur)
 
+    def wait_into(self, stream) -> None:
+        """``stream`` waits (on the device) for every download queued so far."""
+        self.dl.wait_into(stream)
+        if self.q is not None:
+            self.q.fence(stream)
+
     def flush(self) -> None:
         self.dl.flush()
+        if self.q is not None:
+            self._flush_native()

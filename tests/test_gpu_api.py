@@ -543,8 +543,8 @@ def test_edge_stream_downloads_equal_synchronous_renders(cuda):
             out[cid] = tuple(tup)
         return out
 
-    for mode in ("per-raster", "one span"):
-        es = EdgeStream(renderer(), 1, depth=2,
+    for mode in ("per-raster", "one span", "native"):
+        es = EdgeStream(renderer(), 1, depth=2, native=mode == "native",
                         on_view=lambda host, tag: got.__setitem__(tag, host[0].numpy().copy()))
         for rep in range(2):   # laps: buffers rotate while earlier copies are in flight
             for i, fr in enumerate(frames):
@@ -556,8 +556,14 @@ def test_edge_stream_downloads_equal_synchronous_renders(cuda):
                     pinned = packed(fr)
                 es.submit(pinned, [v], [refs], tag=(mode, rep, i))
         es.flush()
-        assert (next(iter(es.ups.values())).layout is not None) == (mode == "one span")
-    assert len(got) == 4 * len(frames)
+        if mode == "native":
+            # the native tick queue: every tick one span, repeating ticks replayed
+            assert not es.ups and es.q is not None
+            st = es.q.stats()
+            assert st["ticks"] == 2 * len(frames) and st["h2d_bytes"] == es.h2d_bytes
+        else:
+            assert (next(iter(es.ups.values())).layout is not None) == (mode == "one span")
+    assert len(got) == 6 * len(frames)
     for (mode, rep, i), img in got.items():
         assert np.array_equal(img, want[i]), f"{mode}, lap {rep}, frame {i}"
     assert es.h2d_bytes == 2 * sum(a.nbytes for fr in frames for t in fr.values() for a in t)
