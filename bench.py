@@ -563,7 +563,8 @@ def run_e2e(args, wl, engs, frames, views, dev, stream, wire: bool = False):
     for e in ess:
         for up in e.ups.values():
             up.stream.wait_event(e0)
-        e.dl.stream.wait_event(e0)
+        if e._dl is not None:
+            e._dl.stream.wait_event(e0)
     nv2 = run(args.warmup, args.steps)
     e1.record(stream)
     torch.cuda.synchronize()

@@ -694,8 +694,8 @@ class EdgeStream:
         self.dev = dev
         k = renderer.rig[0].intrinsics
         self.max_views = int(max_views)
-        self.dl = ResultDownloader((max_views, int(k.height), int(k.width), 3), depth, dev,
-                                   on_done=on_view)
+        self._dl_shape = (max_views, int(k.height), int(k.width), 3)
+        self._dl = None             # ResultDownloader of the Python path (made on first use)
         self.on_view = on_view
         self.depth = depth
         self.ups = {}
@@ -719,6 +719,13 @@ class EdgeStream:
         self._spans = {}            # id(frame) -> (rasters, span layout)
         self._mode = None           # "native" | "python": the path of the last tick
 
+    @property
+    def dl(self) -> ResultDownloader:
+        if self._dl is None:
+            self._dl = ResultDownloader(self._dl_shape, self.depth, self.dev,
+                                        on_done=self.on_view)
+        return self._dl
+
     def _uploader(self, frame):
         key = tuple((cid, tuple(tuple(t.shape) for t in ts)) for cid, ts in sorted(frame.items()))
         up = self.ups.get(key)
@@ -733,7 +740,8 @@ class EdgeStream:
 
     @property
     def d2h_bytes(self) -> int:
-        return self.dl.bytes + (self.q.stats()["d2h_bytes"] if self.q is not None else 0)
+        n = self._dl.bytes if self._dl is not None else 0
+        return n + (self.q.stats()["d2h_bytes"] if self.q is not None else 0)
 
     # -- native path ------------------------------------------------------------
 
@@ -796,8 +804,8 @@ class EdgeStream:
             self._qhost = [torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
                            for _ in range(self.depth)]
             self._qn = 0
-        if self._mode == "python":
-            self.dl.flush()
+        if self._mode == "python" and self._dl is not None:
+            self._dl.flush()
         self._mode = "native"
         self.r._bind()
         slot = self._qn % self.depth
@@ -905,11 +913,13 @@ class EdgeStream:
 
     def wait_into(self, stream) -> None:
         """``stream`` waits (on the device) for every download queued so far."""
-        self.dl.wait_into(stream)
+        if self._dl is not None:
+            self._dl.wait_into(stream)
         if self.q is not None:
             self.q.fence(stream)
 
     def flush(self) -> None:
-        self.dl.flush()
+        if self._dl is not None:
+            self._dl.flush()
         if self.q is not None:
             self._flush_native()

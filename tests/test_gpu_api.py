@@ -822,3 +822,56 @@ def test_captured_multi_view_tick_equals_eager(cuda):
         out = graphs[rep % 2].replay()
         if rep % 13 == 0 or rep >= 58:
             np.testing.assert_array_equal(out.cpu().numpy(), want[rep % 2], err_msg=f"tick {rep}")
+
+
+def test_tick_queue_argument_errors_and_replay_miss(cuda):
+    """The native tick queue (fvv_tickq_*) rejects spans it cannot hold,
+    misaligned rasters and unknown slots with ValueError (FVV_EINVAL) before
+    any copy, and a replay of a key it never captured returns -1."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2007_00558_b200 import _native, scenes
+    from paper_2007_00558_b200.engine import EdgeRenderer, TickQueue
+
+    wl = scenes.make_workload("c0", scale=2)
+    v, refs = wl.virtuals[0], wl.refs[0]
+    r = EdgeRenderer(wl.rig, private=True)
+    for cid in refs:
+        c = wl.frames[0][cid]
+        r.set_bg_model(cid, c.bg_depth, c.bg_validity)
+    k = wl.rig[0].intrinsics
+    H, W = int(k.height), int(k.width)
+    per = [3 * H * W, 2 * H * W, H * W]
+    span = sum(per) * len(refs)
+    host = torch.zeros(span + 64, dtype=torch.uint8).pin_memory()
+    out = torch.empty(H * W * 3, dtype=torch.uint8).pin_memory()
+    q = TickQueue(r, 2, span, H * W * 3, 8)
+    assert q.replay(host.data_ptr(), span, out.data_ptr(), 12345) == -1
+    offs, o = [], 0
+    for _ in refs:
+        offs += [o, o + per[0], o + per[0] + per[1], -1]
+        o += sum(per)
+
+    def submit(nbytes, offsets, slots):
+        n = len(refs)
+        return q.submit(C.c_void_p(host.data_ptr()), nbytes, 0, n, (C.c_int32 * n)(*slots),
+                        (C.c_int64 * (4 * n))(*offsets), 0.0, 0.0, 1,
+                        (_native.FvvCamera * 1)(_native.camera(v)), 1,
+                        (C.c_int32 * n)(*[r.slot[c] for c in refs]),
+                        (C.c_double * n)(*[1.0] * n), n, C.byref(_native.synth_cfg(r.cfg)),
+                        C.c_void_p(out.data_ptr()), 0)
+
+    slots = [r.slot[c] for c in refs]
+    with pytest.raises(ValueError, match="span"):
+        submit(span + 16, offs, slots)
+    with pytest.raises(ValueError, match="aligned"):
+        submit(span, [x + 8 if x > 0 else x for x in offs], slots)
+    with pytest.raises(ValueError, match="no camera"):
+        submit(span, offs, [63] + slots[1:])
+    assert q.stats()["ticks"] == 0
+    t = submit(span, offs, slots)        # all-zero rasters: a valid (empty) tick
+    q.wait(t)
+    assert q.stats()["ticks"] == 1 and q.stats()["h2d_bytes"] == span
+    q.close()
