@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(NT) k_resolve_generic(const __grid_constant__ 
 // the merged layers held as rounded packed colours in registers.
 
 #ifndef FVV_K3_MINB
-#define FVV_K3_MINB 5
+#define FVV_K3_MINB 6
 #endif
 #ifndef FVV_K3_TY
 #define FVV_K3_TY 8
@@ -1575,8 +1575,27 @@ constexpr int NBUF = FVV_K3_NBUF;  // key tiles in flight (NBUF-1 items ahead of
 // are in flight (cp.async groups) while the current one is shaded, and the
 // cells phase of contribution q+1 runs in the same barrier interval as the
 // per-pixel work of contribution q.
+// dynamic shared memory of a k_resolve_fast CTA: key tiles, winner cells,
+// per-contribution results, rays, (ANG) weights, (DBG) stage bytes
+template <int MAXR, bool ANG>
+constexpr size_t fast_smem() {
+    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(WinnerT<MAXR>) +
+           (size_t)MAXR * 4 * FNT * sizeof(double) + (TX + FTY) * sizeof(double) +
+           (ANG && MAXR <= 3 ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
+}
+
+// Resident CTAs per SM the register budget is sized for: FVV_K3_MINB (6:
+// 40 registers) where that many CTAs' shared memory fits the SM's 228 KB
+// (1 KB reserved per CTA, ~0.2 KB static), else 5 (48 registers). At c1 (3
+// references) 6 CTAs measured 140.7 us against 145.7 at 5 with this build;
+// 7 or 8 (32 registers) spill heavily.
+template <int MAXR, bool ANG>
+constexpr int k3_min_blocks() {
+    return (fast_smem<MAXR, ANG>() + 1024 + 256) * FVV_K3_MINB <= 228 * 1024 ? FVV_K3_MINB : 5;
+}
+
 template <int MAXR, bool DBG, bool ANG>
-__global__ void __launch_bounds__(FNT, FVV_K3_MINB) k_resolve_fast(const __grid_constant__ ResolveParams p) {
+__global__ void __launch_bounds__(FNT, (k3_min_blocks<MAXR, ANG>())) k_resolve_fast(const __grid_constant__ ResolveParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[NBUF];                // TMA completion per buffer
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);          // [NBUF][FKEYS]
@@ -1903,12 +1922,6 @@ static void raise_smem(K kernel, size_t bytes, std::atomic<uint64_t> &done) {
     done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
-template <int MAXR, bool ANG>
-static size_t fast_smem() {
-    return NBUF * FKEYS * sizeof(uint64_t) + 2 * FCELLS * sizeof(WinnerT<MAXR>) +
-           (size_t)MAXR * 4 * FNT * sizeof(double) + (TX + FTY) * sizeof(double) +
-           (ANG && MAXR <= 3 ? (size_t)MAXR * FNT * sizeof(double) : 0) + 2 * FCELLS;
-}
 
 template <int MAXR, bool DBG, bool ANG>
 static void launch_fast(const ResolveParams &p, dim3 grid, cudaStream_t s) {
