@@ -683,7 +683,9 @@ class EdgeStream:
     buffer holds a tick), 16-byte aligned, goes through the native tick queue
     (``TickQueue``, ``native=True``): one call per tick, its copies, events,
     ingest, render and graph replays issued in C++. Other frames go through
-    ``FrameUploader`` / ``EdgeRenderer`` / ``ResultDownloader``.
+    ``FrameUploader`` / ``EdgeRenderer`` / ``ResultDownloader``. Either way
+    the copies are asynchronous: a tick's host rasters must stay unchanged
+    until its views reach ``on_view`` (or ``flush`` returns).
     """
 
     def __init__(self, renderer: "EdgeRenderer", max_views: int, depth: int = 2,
