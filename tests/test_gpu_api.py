@@ -875,3 +875,12 @@ def test_tick_queue_argument_errors_and_replay_miss(cuda):
     q.wait(t)
     assert q.stats()["ticks"] == 1 and q.stats()["h2d_bytes"] == span
     q.close()
+
+
+@pytest.mark.gpu
+def test_graft_entry_smoke(cuda):
+    """The driver's round-end smoke(): one small c0 view through the CUDA
+    path, bit-exact against the oracle, plus the drop-in synthesize_view."""
+    import __graft_entry__
+
+    __graft_entry__.smoke()
