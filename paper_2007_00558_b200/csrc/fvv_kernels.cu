@@ -1390,7 +1390,23 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
     b = hi;
 }
 
-__device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// min of 8 keys: the high words' min by three-input VIMNMX3, then the min of
+// the low words among the keys holding it (exact; 23 instructions against
+// 28 for seven 64-bit compare-and-selects: K3 135.6 -> 134.2 us at c1)
+__device__ __forceinline__ uint64_t min8_u64(uint64_t n0, uint64_t n1, uint64_t n2, uint64_t n3,
+                                             uint64_t n4, uint64_t n5, uint64_t n6, uint64_t n7) {
+    const uint32_t h0 = (uint32_t)(n0 >> 32), h1 = (uint32_t)(n1 >> 32), h2 = (uint32_t)(n2 >> 32),
+                   h3 = (uint32_t)(n3 >> 32), h4 = (uint32_t)(n4 >> 32), h5 = (uint32_t)(n5 >> 32),
+                   h6 = (uint32_t)(n6 >> 32), h7 = (uint32_t)(n7 >> 32);
+    const uint32_t hm = __vimin3_u32(__vimin3_u32(h0, h1, h2), __vimin3_u32(h3, h4, h5), min(h6, h7));
+    const uint32_t l0 = h0 == hm ? (uint32_t)n0 : ~0u, l1 = h1 == hm ? (uint32_t)n1 : ~0u,
+                   l2 = h2 == hm ? (uint32_t)n2 : ~0u, l3 = h3 == hm ? (uint32_t)n3 : ~0u,
+                   l4 = h4 == hm ? (uint32_t)n4 : ~0u, l5 = h5 == hm ? (uint32_t)n5 : ~0u,
+                   l6 = h6 == hm ? (uint32_t)n6 : ~0u, l7 = h7 == hm ? (uint32_t)n7 : ~0u;
+    const uint32_t lm = __vimin3_u32(__vimin3_u32(l0, l1, l2), __vimin3_u32(l3, l4, l5), min(l6, l7));
+    return ((uint64_t)hm << 32) | lm;
+}
 
 // Cells-phase descriptors: a thread's cells (tid, tid + FNT) are the same
 // for every contribution of the tile, so their key-tile offset, in-image bit
@@ -1464,13 +1480,10 @@ __device__ __forceinline__ int resolve_cells(const ResolveContrib &c, const Cell
                                         ((unsigned)(n4 < lim) << 4) | ((unsigned)(n5 < lim) << 5) |
                                         ((unsigned)(n6 < lim) << 6) | ((unsigned)(n7 < lim) << 7);
                     keep = __popc(fm & (dsc >> 16)) >= 5;
-                    if (keep)
-                        w = min_u64(min_u64(min_u64(n0, n1), min_u64(n2, n3)),
-                                    min_u64(min_u64(n4, n5), min_u64(n6, n7)));
+                    if (keep) w = min8_u64(n0, n1, n2, n3, n4, n5, n6, n7);
                 } else {
                     // the 8-ring min; stale keys compare larger than any fresh one
-                    w = min_u64(min_u64(min_u64(n0, n1), min_u64(n2, n3)),
-                                min_u64(min_u64(n4, n5), min_u64(n6, n7)));
+                    w = min8_u64(n0, n1, n2, n3, n4, n5, n6, n7);
                     keep = w < lim;
                 }
                 if (keep) sq = kStageSplat;
